@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark: Gpoints/s hierarchized (fp64) on B200, with the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5|C2|C3|C4] [--impl sgh|reference]
+
+Default workload C5 = BASELINE.json configs[4]: the full combination-grid set
+d=4, n=22 (|l|_1 in {22,21,20,19}), 4,255 grids, 5,143,278,175 points
+(41.1 GB fp64), uniform [-1,1) seeded -- the set BASELINE.json's metric is
+quoted on for 1/2/4/8 GPUs.  A step = one batched hierarchization of every
+grid (all d axis rounds; Alg. 1) through the C ABI.  With N ranks
+(torchrun) the grids are LPT-balanced by point count over the ranks (strong
+scaling: the set is fixed), no data-path collective; the elapsed time is the
+max over ranks.  Inputs (41 GB) are far larger than L2, so no flush is needed.
+
+Single-grid workloads C2/C3/C4 run the same way with one grid (replicated per
+rank; C4 with N > 1 runs the sharded path with its NCCL all-to-all).
+
+--impl reference times the CPU oracle (oracle/, the plain Alg. 1) on this box's
+host cores on a bounded sample of the same workload (the paper has no GPU
+code and no shipped implementation).
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gpoints/s hierarchized (fp64) and achieved HBM GB/s vs B200 roofline, 1/2/4/8 GPU"
+UNIT = "Gpoints/s"
+FALLBACK_HBM = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ workload
+def workload(name):
+    import sgh_inputs as si
+    if name == "C5":
+        cfg = si.CONFIGS["C5"]
+        members = si.combination_set(cfg.d, cfg.n)
+        desc = (f"C5: combination set d={cfg.d} n={cfg.n}, |l|_1 in {{{cfg.n},{cfg.n-1},{cfg.n-2},{cfg.n-3}}}, "
+                f"{len(members)} grids")
+        return members, list(range(len(members))), desc
+    lv = si.CONFIGS[name].levels
+    return [tuple(lv)], [0], f"{name}: single grid level {tuple(lv)}"
+
+
+def d_eff(levels):
+    return sum(1 for l in levels if l > 1)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu_index = gpu_index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ cpu baseline
+def oracle_rate(members, ids, target_cpu_s=12.0, max_points=400_000_000, threads=None, steps=1, warmup=0,
+                seed=13090392):
+    """Time the CPU oracle (plain Alg. 1, one grid per thread) on a bounded,
+    deterministic sample of the workload.  Returns (Gpoints/s, sample desc, cores, per-step times)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    import sgh_inputs as si
+    threads = threads or os.cpu_count() or 1
+    sizes = [si.num_points(l) for l in members]
+    # calibrate single-thread rate on a mid-sized member
+    order = sorted(range(len(members)), key=lambda i: sizes[i])
+    probe = order[len(order) // 2]
+    g = oracle.fill_uniform(sizes[probe], seed, ids[probe])
+    t0 = time.perf_counter()
+    oracle.hierarchize(g, members[probe])
+    rate1 = sizes[probe] / max(time.perf_counter() - t0, 1e-6)
+    budget_pts = min(max_points, int(rate1 * target_cpu_s))
+    # deterministic stride sample over the member list
+    if sum(sizes) <= budget_pts:
+        pick = list(range(len(members)))
+    else:
+        stride = max(1, int(sum(sizes) / budget_pts))
+        pick, tot = [], 0
+        for i in range(0, len(members), stride):
+            if tot + sizes[i] > budget_pts and pick:
+                break
+            pick.append(i)
+            tot += sizes[i]
+        if not pick:
+            pick = [order[0]]
+    grids = [oracle.fill_uniform(sizes[i], seed, ids[i]) for i in pick]
+    npts = sum(sizes[i] for i in pick)
+
+    def run_one(j):
+        oracle.hierarchize(grids[j], members[pick[j]])
+
+    times = []
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for s in range(warmup + steps):
+            t0 = time.perf_counter()
+            list(ex.map(run_one, sorted(range(len(pick)), key=lambda j: -sizes[pick[j]])))
+            dt = time.perf_counter() - t0
+            if s >= warmup:
+                times.append(dt)
+    desc = (f"{len(pick)} of {len(members)} grids ({npts:,} points, every {max(1, len(members)//max(len(pick),1))}th "
+            f"member), plain Alg. 1 oracle, {threads} threads (one grid per thread)")
+    return npts / (sum(times) / len(times)) / 1e9, desc, threads, times, npts
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C5", choices=["C5", "C2", "C3", "C4"])
+    ap.add_argument("--impl", default="sgh", choices=["sgh", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+    return sgh_arm(args, rank, world, local_rank)
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    members, ids, desc = workload(args.workload)
+    rate, sample, cores, times, npts = oracle_rate(members, ids, target_cpu_s=4.0, max_points=200_000_000,
+                                                   steps=args.steps, warmup=args.warmup)
+    ms = 1e3 * sum(times) / len(times)
+    out = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": desc, "sample_points_per_step": npts},
+           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": "the paper's comparison codes (SGpp, Buse et al.) and its own CPU code are not available; "
+                   "the reference arm is this repo's plain C oracle of Alg. 1 on host cores"}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def sgh_arm(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1309_0392_b200 as sgh
+    import sgh_inputs as si
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    members, ids, desc = workload(args.workload)
+    sizes = [si.num_points(l) for l in members]
+    sharded = args.workload == "C4" and world > 1
+    if args.workload == "C5" and world > 1:
+        part = si.lpt_partition(sizes, world)[rank]
+        my_members, my_ids = [members[i] for i in part], [ids[i] for i in part]
+    else:
+        my_members, my_ids = members, ids
+    total_points = sum(sizes) if (args.workload == "C5" or sharded) else sum(sizes) * world
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    stream = torch.cuda.current_stream()
+    if sharded:
+        levels = members[0]
+        b, e = sgh.shard_rows(levels, world, rank)
+        C = sizes[0] // ((1 << levels[-1]) - 1)
+        shard = torch.empty((e - b) * C, dtype=torch.float64, device=dev)
+        sgh.fill_uniform(shard, si.SEED, 0, b * C)
+        comm = sgh.ShardComm()
+        ws = torch.empty(sgh.sharded_workspace_bytes(levels, world) // 8 + 1, dtype=torch.float64, device=dev)
+        step = lambda: comm.transform(shard, levels, ws)  # noqa: E731
+        my_points = shard.numel()
+        deff_pts = d_eff(levels) * my_points
+    else:
+        batch = sgh.GridBatch(my_members, device=dev, grid_ids=my_ids)
+        batch.fill_uniform(si.SEED)
+        step = batch.hierarchize
+        my_points = batch.total_points
+        deff_pts = sum(d_eff(l) * si.num_points(l) for l in my_members)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    n0 = sgh.launch_count()
+    sgh.profile_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = sgh.launch_count() - n0
+    recs = sgh.profile_read()
+    sgh.profile_enable(False)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = total_points / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (live events on the launching stream)
+    peak, peak_src = peak_hbm()
+    per = {}
+    for r in recs:
+        k = r["kernel"]
+        a = per.setdefault(k, {"ms": 0.0, "bytes": 0.0, "launches": 0})
+        a["ms"] += r["ms"]
+        a["bytes"] += r["bytes"]
+        a["launches"] += 1
+    kern_tab = {k: {"launches_per_step": v["launches"] / args.steps,
+                    "share_of_step": v["ms"] / ms if ms else None,
+                    "GBps": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else None}
+                for k, v in per.items()}
+    roof = None
+    if per:
+        dom = max(per, key=lambda k: per[k]["ms"])
+        a = per[dom]
+        achieved = a["bytes"] / (a["ms"] * 1e-3) / 1e9
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tf):
+            try:
+                traffic = json.load(open(tf)).get(args.workload, {}).get(dom)
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": a["bytes"] / a["launches"],
+                "avg_launch_ms": a["ms"] / a["launches"], "peak_source": peak_src}
+    step_s = ms_step * 1e-3
+    model = {"per_axis_GBps": 16.0 * deff_pts / step_s / 1e9 if not sharded else None,
+             "fused_GBps": 16.0 * my_points / step_s / 1e9,
+             "per_axis_frac": (16.0 * deff_pts / step_s / 1e9) / peak if not sharded else None,
+             "note": "rank-0 view: 16 B/point/axis (per-axis model) and 16 B/point (fused floor)"}
+
+    # e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e and not sharded:
+        e2e = run_e2e(sgh, my_members, my_ids, dev, args.e2e_steps, world, rank)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, sample, cores, _t, _n = oracle_rate(members, ids)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong"
+               if (args.workload == "C5" or sharded) else "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic",
+               "config": {"workload": desc, "points": total_points, "bytes": 8 * total_points,
+                          "l2": "inputs larger than L2 (no flush needed)" if 8 * total_points > 2 * 126e6
+                          else "L2 not flushed; input < 2x L2",
+                          "parallelism": (f"grids LPT-balanced over {world} ranks" if args.workload == "C5"
+                                          else ("sharded along x_d, NCCL all-to-all" if sharded else "replicas")),
+                          "seed": si.SEED},
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+               "gpu_launches": launches, "kernels": kern_tab, "model": model}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(sgh, members, ids, dev, steps, world, rank):
+    """Same metric through the public host-buffer API: H2D of every grid, the
+    batched transform and D2H of every result, timed on the device."""
+    import psutil
+    import torch
+
+    import sgh_inputs as si
+    sizes = [si.num_points(l) for l in members]
+    nbytes = 8 * sum(sizes)
+    avail = psutil.virtual_memory().available
+    sub_m, sub_i = members, ids
+    note = "all grids of this rank"
+    if nbytes * 1.3 > avail:
+        # keep within host RAM: a deterministic prefix of the members
+        keep, tot = [], 0
+        for i, s in enumerate(sizes):
+            if (tot + s) * 8 * 1.3 > avail:
+                break
+            keep.append(i)
+            tot += s
+        sub_m, sub_i = [members[i] for i in keep], [ids[i] for i in keep]
+        note = f"{len(keep)} of {len(members)} grids (host RAM bound)"
+    sub_sizes = [si.num_points(l) for l in sub_m]
+    total = sum(sub_sizes)
+    host = torch.empty(total, dtype=torch.float64, pin_memory=True)
+    views, off = [], 0
+    for n in sub_sizes:
+        views.append(host[off:off + n])
+        off += n
+    # inputs: device fill, copied to the pinned host buffers (outside the timed region)
+    tmp = sgh.GridBatch(sub_m, device=dev, grid_ids=sub_i)
+    tmp.fill_uniform(si.SEED)
+    for v, dv in zip(views, tmp.views):
+        v.copy_(dv, non_blocking=True)
+    torch.cuda.synchronize()
+    del tmp
+    buf = torch.empty(sgh.batched_host_buffer_bytes(sub_m) // 8 + 32, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    sgh.transform_batched_host(views, sub_m, buf)   # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        sgh.transform_batched_host(views, sub_m, buf)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": total * world / (ms * 1e-3) / 1e9 if world > 1 else total / (ms * 1e-3) / 1e9,
+            "unit": UNIT, "h2d_bytes_per_step": 8 * total, "d2h_bytes_per_step": 8 * total,
+            "ms_per_step": ms, "steps": steps, "grids": note,
+            "api": "sgh_transform_batched_host (pinned host buffers, chunked H2D/transform/D2H overlap)"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

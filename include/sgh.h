@@ -1,0 +1,225 @@
+/*
+ * sgh.h -- C ABI of libsgh: B200-native (sm_100a) hierarchization of the
+ * anisotropic full grids of the sparse grid combination technique
+ * (arXiv 1309.0392, "hierarchization ... preprocessing step facilitating the
+ * communication").
+ *
+ * Citation format: P:n = PAPER.md line n, S:n = SPEC.md line n (SPEC is a CPU
+ * program spec written from the paper; used for interface conventions only).
+ *
+ * ---------------------------------------------------------------- layout
+ * A grid with level vector l = (l_1..l_d) has n_k = 2^{l_k} - 1 interior
+ * points along axis k ("refinement level 1 consist of one single grid
+ * point"; zero boundary, not stored).  It is stored as N = prod_k n_k IEEE
+ * binary64 values, row-major with x_1 the FASTEST-varying index (P:227
+ * "standard row major order", P:236 / P:292).  The point with 1-based
+ * per-axis indices (i_1..i_d) lives at flat offset sum_k (i_k - 1) S_k with
+ * S_k = prod_{j<k} n_j.  No padding, no alignment requirement beyond 8 bytes.
+ *
+ * ---------------------------------------------------------------- method
+ * Hierarchization (Alg. 1): for k = 1..d in order, every 1-D pole
+ * along axis k is transformed, levels l_k down to 2, point i on level lam
+ * (i = s(2j+1), s = 2^{l_k - lam}):
+ *      x[i] = x[i] - 0.5 * x[i - s];   x[i] = x[i] - 0.5 * x[i + s]
+ * where a predecessor on the boundary (i - s = 0 or i + s = 2^{l_k}) is
+ * absent and that update is skipped.  Dehierarchization is the inverse
+ * base change: levels 2 up to l_k, "+0.5*left then +0.5*right".
+ * Results are bitwise identical to the literal Alg. 1 executed on the CPU
+ * ("Parity"); the same holds for dehierarchization.
+ *
+ * ---------------------------------------------------------------- rules
+ *  - All grid / workspace / shard pointers are DEVICE pointers owned by the
+ *    caller, unless a parameter says "host".  The library never allocates
+ *    device memory inside the hot calls.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call is stream-ordered and asynchronous unless stated otherwise.
+ *  - Buffers are modified in place; the caller guarantees exclusive access
+ *    until the stream reaches the call.  Grids in one batch must not overlap.
+ *  - Arguments are validated before anything is enqueued (all or nothing).
+ *    Status codes only; no exception crosses the ABI.  Launch failures return
+ *    SGH_ERR_CUDA with the detail in sgh_last_error(); asynchronous device
+ *    faults surface at the caller's next synchronisation.
+ *  - There is exactly one backend (CUDA, sm_100a).  No CPU fallback: if no
+ *    suitable device is present the calls return SGH_ERR_CUDA.
+ */
+#ifndef SGH_H
+#define SGH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SGH_OK = 0,
+    SGH_ERR_INVALID_ARGUMENT = 1, /* d<1 or d>SGH_MAX_D, l_k<1, NULL pointer, bad permutation, num_grids<0 */
+    SGH_ERR_CAPACITY = 2,         /* l_k > SGH_MAX_LEVEL or N*8 overflows int64         */
+    SGH_ERR_CUDA = 3,             /* CUDA launch / runtime error; see sgh_last_error()                 */
+    SGH_ERR_NCCL = 4,             /* NCCL error in the sharded path                                     */
+    SGH_ERR_WORKSPACE = 5         /* workspace NULL or smaller than sgh_*_workspace_bytes()             */
+} sgh_status;
+
+#define SGH_MAX_D 16     /* the paper goes up to d = 10 (Fig. fig:10D) */
+#define SGH_MAX_LEVEL 30 /* n_k = 2^30 - 1 points on one axis               */
+
+/* flags for the _ex / batched calls */
+#define SGH_FLAG_NONE 0u
+#define SGH_FLAG_DEHIERARCHIZE 1u /* run the inverse transform instead  */
+
+/* ------------------------------------------------------------ geometry */
+
+/* N = prod_k (2^{l_k} - 1).  levels: host array of d int32.
+ * Returns -1 if the level vector is invalid or N*8 overflows int64. */
+int64_t sgh_num_points(const int32_t *levels, int32_t d);
+
+/* ------------------------------------------------------- single grid */
+
+/* Hierarchize one grid in place (Alg. 1), axes 1..d in order.
+ * grid: device pointer to N doubles (layout above).  levels: host int32[d].
+ * No workspace: uses only in-place per-axis kernels. */
+sgh_status sgh_hierarchize(double *grid, const int32_t *levels, int32_t d, void *stream);
+
+/* Dehierarchize one grid in place (inverse base change; reading R9). */
+sgh_status sgh_dehierarchize(double *grid, const int32_t *levels, int32_t d, void *stream);
+
+/* General single-grid entry.
+ *  axis_order: host int32[d], a permutation of 0..d-1 (0-based axes), or NULL
+ *              for the paper's order 0..d-1 ("for d <- 1..dim").
+ *  axis_mask:  bit k set = transform along axis k; 0 means "all axes".
+ *              (Used by the sharded path: local axes only.)
+ *  flags:      SGH_FLAG_DEHIERARCHIZE for the inverse.
+ * Other orders agree with the paper's only up to rounding (reading R7). */
+sgh_status sgh_transform_ex(double *grid, const int32_t *levels, int32_t d,
+                            const int32_t *axis_order, uint32_t axis_mask,
+                            uint32_t flags, void *stream);
+
+/* ------------------------------------------ batched combination set */
+
+/* Bytes of device workspace the batched calls need for num_grids grids of
+ * dimension d (descriptor tables).  levels: host int32[num_grids][d]. */
+size_t sgh_batched_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags);
+
+/* Hierarchize (or, with SGH_FLAG_DEHIERARCHIZE, dehierarchize) num_grids
+ * independent grids (the combination grids, "hierarchized in parallel").
+ *  grids:     host array of num_grids DEVICE pointers (each N_g doubles).
+ *  levels:    host int32[num_grids][d], row-major (grid g's level vector at g*d).
+ *  workspace: device buffer of >= sgh_batched_workspace_bytes() bytes, 16-byte
+ *             aligned; it holds the per-launch task tables and must not be
+ *             reused by the caller until the stream has passed this call.
+ * One grouped launch per (axis round, phase, kernel kind) over all grids.
+ * Grids of differing d must be padded with trailing level-1 axes. */
+sgh_status sgh_hierarchize_batched(double *const *grids, const int32_t *levels, int32_t d,
+                                   int64_t num_grids, uint32_t flags,
+                                   void *workspace, size_t ws_bytes, void *stream);
+
+/* Device bytes sgh_transform_batched_host() needs: every grid (256-byte
+ * aligned) plus one task table per transfer chunk. */
+size_t sgh_batched_host_buffer_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags);
+
+/* End-to-end variant with HOST buffers (the e2e path): host_grids[g] are host
+ * pointers (pinned for full PCIe speed), transformed in place.
+ * device_buffer: >= sgh_batched_host_buffer_bytes() bytes, 256-byte aligned.
+ * Grids are copied in, transformed and copied back in chunks of ~512 MB; the
+ * copies run on two library-owned streams overlapped with the transform, and
+ * `stream` waits for the last copy-out, so after synchronising `stream` every
+ * host grid holds its result.  Asynchronous w.r.t. the host. */
+sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *levels, int32_t d,
+                                      int64_t num_grids, uint32_t flags,
+                                      void *device_buffer, size_t device_buffer_bytes,
+                                      void *stream);
+
+/* ----------------------------------------------- sharded single grid */
+
+/* Rows [row_begin, row_end) (0-based indices of x_d, the slowest axis) owned
+ * by `rank` of `nranks` when one grid is sharded along x_d.  nranks must be a
+ * power of two <= n_d + 1; shards are the dyadic blocks
+ * [r 2^{l_d - p}, (r+1) 2^{l_d - p}) of 1-based indices intersected with
+ * [1, n_d] (so rank 0 holds one row fewer).  Host-only; no device work. */
+sgh_status sgh_shard_rows(const int32_t *levels, int32_t d, int32_t nranks, int32_t rank,
+                          int64_t *row_begin, int64_t *row_end);
+
+/* Library-owned NCCL communicator created from a 128-byte ncclUniqueId that
+ * the caller broadcasts (e.g. with torch.distributed).  *comm receives an
+ * opaque handle.  Blocking (NCCL init is collective over all ranks). */
+sgh_status sgh_comm_create(void **comm, const void *nccl_unique_id, int32_t nranks, int32_t rank);
+void sgh_comm_destroy(void *comm);
+/* Writes the 128-byte ncclUniqueId into out (host buffer of >= 128 bytes). */
+sgh_status sgh_comm_unique_id(void *out);
+
+/* Workspace bytes of the sharded calls (two all-to-all staging buffers). */
+size_t sgh_sharded_workspace_bytes(const int32_t *levels, int32_t d, int32_t nranks);
+
+/* Hierarchize a grid sharded along x_d over the ranks of `comm`.  shard: this
+ * rank's rows (sgh_shard_rows), row-major, (row_end-row_begin) * prod_{k<d} n_k
+ * doubles.  Axes 1..d-1 are transformed locally; the axis-d pass runs after an
+ * NCCL all-to-all re-shard into column blocks and the result is returned to
+ * row sharding by a second all-to-all.  Collective: every rank must call it.
+ * Bitwise equal to the single-GPU result. */
+sgh_status sgh_hierarchize_sharded(double *shard, const int32_t *levels, int32_t d, void *comm,
+                                   void *workspace, size_t ws_bytes, void *stream);
+sgh_status sgh_dehierarchize_sharded(double *shard, const int32_t *levels, int32_t d, void *comm,
+                                     void *workspace, size_t ws_bytes, void *stream);
+
+/* Test utility: the sharded algorithm above for `nranks` VIRTUAL ranks on the
+ * current device (the all-to-all becomes device-to-device copies).  shards:
+ * host array of nranks device pointers (rank r's rows, sgh_shard_rows).
+ * workspace: nranks * sgh_sharded_workspace_bytes() bytes.  Exercises the same
+ * planning, packing and slab passes as the NCCL path on a single GPU. */
+sgh_status sgh_transform_sharded_loopback(double *const *shards, const int32_t *levels, int32_t d, int32_t nranks,
+                                          uint32_t flags, void *workspace, size_t ws_bytes, void *stream);
+
+/* ----------------------------------------- harness utilities (not the method) */
+
+/* Seeded counter-based fill: value of global flat
+ * index i = index_offset + k is 2*((mix64(key+i)>>11)*2^-53) - 1 with
+ * key = mix64(seed ^ mix64(grid_id)), mix64 = splitmix64. */
+sgh_status sgh_fill_uniform(double *grid, int64_t n, uint64_t seed, uint64_t grid_id,
+                            int64_t index_offset, void *stream);
+
+/* Batched fill: grid g gets grid_id = grid_ids[g] (host int64 array), offset 0. */
+sgh_status sgh_fill_uniform_batched(double *const *grids, const int64_t *sizes, const uint64_t *grid_ids,
+                                    int64_t num_grids, uint64_t seed, void *workspace, size_t ws_bytes,
+                                    void *stream);
+
+/* Order-independent digest sum_i mix64(bits(v_i) ^ (i * 0x9E3779B97F4A7C15))
+ * mod 2^64 over i = index_offset + k.  Writes *out_host; SYNCHRONISES stream. */
+sgh_status sgh_digest(const double *grid, int64_t n, int64_t index_offset, uint64_t *out_host, void *stream);
+
+/* Per-grid digests of a batch into out_host[num_grids]; synchronises. */
+sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_t num_grids,
+                              uint64_t *out_host, void *workspace, size_t ws_bytes, void *stream);
+
+/* Optional per-launch timing of the transform kernels (process-wide).
+ * sgh_profile_enable(1) clears the record list and starts recording: every
+ * transform kernel launch is bracketed by two CUDA events on its own stream.
+ * sgh_profile_enable(0) stops (and clears).  sgh_profile_read fills up to
+ * `capacity` records (waiting for their events) and returns the number of
+ * records; out may be NULL to query the count.  kind: 0 FLAT_SLABS,
+ * 1 FLAT_BLOCKS, 2 STRIDED, 3 REG.  bytes = 16 x points transformed. */
+typedef struct {
+    int32_t kind;
+    int32_t level;    /* pole level for REG, else the task's l */
+    int32_t inverse;  /* 1 for dehierarchization */
+    int32_t reserved;
+    double bytes;     /* algorithmic bytes (one read + one write per point) */
+    double ms;        /* event-timed duration, -1 if unavailable */
+} sgh_launch_record;
+sgh_status sgh_profile_enable(int32_t on);
+int64_t sgh_profile_read(sgh_launch_record *out, int64_t capacity);
+
+/* Number of kernels this library has launched in this process (all calls).
+ * Used by bench.py to report gpu_launches. */
+uint64_t sgh_launch_count(void);
+
+const char *sgh_status_string(sgh_status s);
+/* Detail of the last error on the calling thread ("" if none). */
+const char *sgh_last_error(void);
+/* Library version string. */
+const char *sgh_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGH_H */

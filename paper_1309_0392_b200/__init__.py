@@ -1,0 +1,412 @@
+"""paper_1309_0392_b200 -- B200-native hierarchization of combination-technique grids.
+
+Thin Python binding of the C ABI in ``include/sgh.h`` (libsgh.so, CUDA sm_100a).
+Argument marshalling only: every step of the method runs in the library's
+kernels.  PyTorch provides device memory, streams and process groups.
+
+There is no CPU fallback: importing this module loads ``lib/libsgh.so`` and
+raises ``ImportError`` if it is missing; the transforms require CUDA tensors.
+
+Method (arXiv 1309.0392, Alg. 1): for each axis k = 1..d, every 1-D
+pole is transformed from the nodal to the hierarchical basis, finest level
+first, x[i] -= 0.5*left; x[i] -= 0.5*right; dehierarchization is the
+inverse.  Grids are fp64, row-major with x_1 fastest,
+n_k = 2^{l_k} - 1 points per axis.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Sequence
+
+import torch
+
+__all__ = [
+    "lib", "num_points", "hierarchize", "dehierarchize", "transform", "GridBatch",
+    "hierarchize_batched", "dehierarchize_batched", "batched_workspace_bytes",
+    "transform_batched_host", "batched_host_buffer_bytes",
+    "fill_uniform", "digest", "shard_rows", "ShardComm", "sharded_workspace_bytes",
+    "transform_sharded_loopback", "launch_count", "SGHError",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsgh.so")
+
+FLAG_DEHIERARCHIZE = 1
+STATUS = {0: "SGH_OK", 1: "SGH_ERR_INVALID_ARGUMENT", 2: "SGH_ERR_CAPACITY", 3: "SGH_ERR_CUDA",
+          4: "SGH_ERR_NCCL", 5: "SGH_ERR_WORKSPACE"}
+
+
+class SGHError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: build it with `python paper_1309_0392_b200/build.py` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    vp = ctypes.c_void_p
+    vpp = ctypes.POINTER(ctypes.c_void_p)
+    sz = ctypes.c_size_t
+    st = ctypes.c_int
+    sigs = {
+        "sgh_num_points": (ctypes.c_int64, [i32p, ctypes.c_int32]),
+        "sgh_hierarchize": (st, [vp, i32p, ctypes.c_int32, vp]),
+        "sgh_dehierarchize": (st, [vp, i32p, ctypes.c_int32, vp]),
+        "sgh_transform_ex": (st, [vp, i32p, ctypes.c_int32, i32p, ctypes.c_uint32, ctypes.c_uint32, vp]),
+        "sgh_batched_workspace_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32]),
+        "sgh_hierarchize_batched": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
+        "sgh_batched_host_buffer_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32]),
+        "sgh_transform_batched_host": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
+        "sgh_shard_rows": (st, [i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, i64p, i64p]),
+        "sgh_comm_create": (st, [vpp, vp, ctypes.c_int32, ctypes.c_int32]),
+        "sgh_comm_destroy": (None, [vp]),
+        "sgh_comm_unique_id": (st, [vp]),
+        "sgh_sharded_workspace_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int32]),
+        "sgh_hierarchize_sharded": (st, [vp, i32p, ctypes.c_int32, vp, vp, sz, vp]),
+        "sgh_dehierarchize_sharded": (st, [vp, i32p, ctypes.c_int32, vp, vp, sz, vp]),
+        "sgh_transform_sharded_loopback": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, vp, sz, vp]),
+        "sgh_fill_uniform": (st, [vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, vp]),
+        "sgh_fill_uniform_batched": (st, [vpp, i64p, u64p, ctypes.c_int64, ctypes.c_uint64, vp, sz, vp]),
+        "sgh_digest": (st, [vp, ctypes.c_int64, ctypes.c_int64, u64p, vp]),
+        "sgh_digest_batched": (st, [vpp, i64p, ctypes.c_int64, u64p, vp, sz, vp]),
+        "sgh_launch_count": (ctypes.c_uint64, []),
+        "sgh_profile_enable": (st, [ctypes.c_int32]),
+        "sgh_profile_read": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int64]),
+        "sgh_status_string": (ctypes.c_char_p, [st]),
+        "sgh_last_error": (ctypes.c_char_p, []),
+        "sgh_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_transform_ex",
+            "sgh_batched_workspace_bytes", "sgh_hierarchize_batched", "sgh_batched_host_buffer_bytes",
+            "sgh_transform_batched_host", "sgh_shard_rows", "sgh_comm_create", "sgh_comm_destroy",
+            "sgh_comm_unique_id", "sgh_sharded_workspace_bytes", "sgh_hierarchize_sharded",
+            "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_fill_uniform",
+            "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
+            "sgh_profile_enable", "sgh_profile_read",
+            "sgh_status_string", "sgh_last_error", "sgh_version")
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise SGHError(rc, lib.sgh_last_error().decode())
+
+
+def _levels_arr(levels: Sequence[int]):
+    a = (ctypes.c_int32 * len(levels))(*[int(x) for x in levels])
+    return a, len(levels)
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _grid_ptr(t: torch.Tensor, levels) -> ctypes.c_void_p:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("grid must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != torch.float64:
+        raise TypeError("grid must be float64 (the method is fp64)")
+    if not t.is_contiguous():
+        raise ValueError("grid must be contiguous (row-major, x_1 fastest)")
+    if levels is not None and t.numel() != num_points(levels):
+        raise ValueError(f"grid has {t.numel()} elements, levels {tuple(levels)} need {num_points(levels)}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def num_points(levels: Sequence[int]) -> int:
+    """N = prod (2^l_k - 1).  -1 if invalid / overflowing."""
+    a, d = _levels_arr(levels)
+    return int(lib.sgh_num_points(a, d))
+
+
+def transform(grid: torch.Tensor, levels: Sequence[int], *, inverse: bool = False, axis_order=None,
+              axis_mask: int = 0, stream=None) -> torch.Tensor:
+    """In-place (de)hierarchization of one grid; returns ``grid``."""
+    a, d = _levels_arr(levels)
+    order = None
+    if axis_order is not None:
+        order = (ctypes.c_int32 * d)(*[int(x) for x in axis_order])
+    ptr = _grid_ptr(grid, levels)
+    with torch.cuda.device(grid.device):
+        _check(lib.sgh_transform_ex(ptr, a, d, order, ctypes.c_uint32(axis_mask),
+                                    ctypes.c_uint32(FLAG_DEHIERARCHIZE if inverse else 0), _stream(stream)))
+    return grid
+
+
+def hierarchize(grid: torch.Tensor, levels: Sequence[int], stream=None) -> torch.Tensor:
+    """Alg. 1 in place, axes 1..d."""
+    a, d = _levels_arr(levels)
+    ptr = _grid_ptr(grid, levels)
+    with torch.cuda.device(grid.device):
+        _check(lib.sgh_hierarchize(ptr, a, d, _stream(stream)))
+    return grid
+
+
+def dehierarchize(grid: torch.Tensor, levels: Sequence[int], stream=None) -> torch.Tensor:
+    """Inverse base change in place."""
+    a, d = _levels_arr(levels)
+    ptr = _grid_ptr(grid, levels)
+    with torch.cuda.device(grid.device):
+        _check(lib.sgh_dehierarchize(ptr, a, d, _stream(stream)))
+    return grid
+
+
+def fill_uniform(grid: torch.Tensor, seed: int, grid_id: int = 0, index_offset: int = 0, stream=None) -> torch.Tensor:
+    """Seeded counter-based fill (harness utility; DESIGN.md input recipe)."""
+    with torch.cuda.device(grid.device):
+        _check(lib.sgh_fill_uniform(_grid_ptr(grid, None), grid.numel(), ctypes.c_uint64(seed),
+                                    ctypes.c_uint64(grid_id), int(index_offset), _stream(stream)))
+    return grid
+
+
+def digest(grid: torch.Tensor, index_offset: int = 0, stream=None) -> int:
+    """Order-independent 64-bit digest (synchronises)."""
+    out = ctypes.c_uint64()
+    with torch.cuda.device(grid.device):
+        _check(lib.sgh_digest(_grid_ptr(grid, None), grid.numel(), int(index_offset), ctypes.byref(out),
+                              _stream(stream)))
+    return int(out.value)
+
+
+def launch_count() -> int:
+    """Kernels libsgh has launched in this process."""
+    return int(lib.sgh_launch_count())
+
+
+class _LaunchRecord(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("level", ctypes.c_int32), ("inverse", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("bytes", ctypes.c_double), ("ms", ctypes.c_double)]
+
+
+KIND_NAMES = {0: "flat_slabs", 1: "flat_blocks", 2: "strided", 3: "reg"}
+
+
+def profile_enable(on: bool = True):
+    """Start (clearing) / stop per-launch event timing inside libsgh."""
+    _check(lib.sgh_profile_enable(1 if on else 0))
+
+
+def profile_read():
+    """Per-launch records since profile_enable(True): list of dicts
+    {kernel, level, inverse, bytes, ms} (waits for the events)."""
+    n = int(lib.sgh_profile_read(None, 0))
+    buf = (_LaunchRecord * max(n, 1))()
+    n = int(lib.sgh_profile_read(ctypes.cast(buf, ctypes.c_void_p), n))
+    out = []
+    for r in buf[:n]:
+        name = KIND_NAMES.get(r.kind, str(r.kind)) + (f"<{r.level}>" if r.kind == 3 else "")
+        out.append({"kernel": name, "level": r.level, "inverse": bool(r.inverse), "bytes": r.bytes, "ms": r.ms})
+    return out
+
+
+# ----------------------------------------------------------------- batched
+def _flat_levels(levels_list, d):
+    flat = []
+    for lv in levels_list:
+        if len(lv) != d:
+            raise ValueError("all grids of a batch need the same d (pad with level-1 axes)")
+        flat.extend(int(x) for x in lv)
+    return (ctypes.c_int32 * len(flat))(*flat)
+
+
+def batched_workspace_bytes(levels_list, inverse: bool = False) -> int:
+    if not levels_list:
+        return 0
+    d = len(levels_list[0])
+    return int(lib.sgh_batched_workspace_bytes(_flat_levels(levels_list, d), d, len(levels_list),
+                                               FLAG_DEHIERARCHIZE if inverse else 0))
+
+
+class GridBatch:
+    """A set of combination grids resident in ONE device allocation.
+
+    Grid g occupies ``N_g`` doubles at a 256-byte aligned offset of a single
+    torch buffer; ``views[g]`` is its 1-D float64 view.  The batched transform
+    runs one grouped launch per (axis round, phase, kernel kind) over all
+    grids ("all combination grids are hierarchized in parallel").
+    """
+
+    def __init__(self, levels_list, device=None, grid_ids=None):
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        self.levels = [tuple(int(x) for x in lv) for lv in levels_list]
+        self.d = len(self.levels[0]) if self.levels else 0
+        self.sizes = [num_points(lv) for lv in self.levels]
+        self.grid_ids = list(grid_ids) if grid_ids is not None else list(range(len(self.levels)))
+        offs, off = [], 0
+        for n in self.sizes:
+            offs.append(off)
+            off += (n + 31) // 32 * 32          # 256-byte aligned starts
+        self.offsets = offs
+        self.total_points = sum(self.sizes)
+        self.buffer = torch.empty(max(off, 1), dtype=torch.float64, device=self.device)
+        self.views = [self.buffer[o:o + n] for o, n in zip(offs, self.sizes)]
+        base = self.buffer.data_ptr()
+        G = len(self.levels)
+        self._ptrs = (ctypes.c_void_p * max(G, 1))(*[base + 8 * o for o in offs])
+        self._sizes = (ctypes.c_int64 * max(G, 1))(*self.sizes)
+        self._ids = (ctypes.c_uint64 * max(G, 1))(*self.grid_ids)
+        self._flat = _flat_levels(self.levels, self.d) if G else None
+        ws = max(batched_workspace_bytes(self.levels, False), batched_workspace_bytes(self.levels, True),
+                 self._util_ws_bytes(), 256)
+        self.workspace = torch.empty((ws + 7) // 8, dtype=torch.float64, device=self.device)
+
+    def _util_ws_bytes(self):
+        G = len(self.levels)
+        return ((G * 32 + 255) // 256 * 256 + (G + 1) * 8 + 255) // 256 * 256 + G * 8 + 256
+
+    def __len__(self):
+        return len(self.levels)
+
+    def _ws(self):
+        return ctypes.c_void_p(self.workspace.data_ptr()), self.workspace.numel() * 8
+
+    def transform(self, inverse: bool = False, stream=None):
+        if not self.levels:
+            return self
+        ws, wsb = self._ws()
+        with torch.cuda.device(self.device):
+            _check(lib.sgh_hierarchize_batched(self._ptrs, self._flat, self.d, len(self.levels),
+                                               FLAG_DEHIERARCHIZE if inverse else 0, ws, wsb, _stream(stream)))
+        return self
+
+    def hierarchize(self, stream=None):
+        return self.transform(False, stream)
+
+    def dehierarchize(self, stream=None):
+        return self.transform(True, stream)
+
+    def fill_uniform(self, seed: int, stream=None):
+        if not self.levels:
+            return self
+        ws, wsb = self._ws()
+        with torch.cuda.device(self.device):
+            _check(lib.sgh_fill_uniform_batched(self._ptrs, self._sizes, self._ids, len(self.levels),
+                                                ctypes.c_uint64(seed), ws, wsb, _stream(stream)))
+        return self
+
+    def digests(self, stream=None):
+        G = len(self.levels)
+        if not G:
+            return []
+        out = (ctypes.c_uint64 * G)()
+        ws, wsb = self._ws()
+        with torch.cuda.device(self.device):
+            _check(lib.sgh_digest_batched(self._ptrs, self._sizes, G, out, ws, wsb, _stream(stream)))
+        return [int(x) for x in out]
+
+
+def hierarchize_batched(batch: GridBatch, stream=None) -> GridBatch:
+    return batch.transform(False, stream)
+
+
+def dehierarchize_batched(batch: GridBatch, stream=None) -> GridBatch:
+    return batch.transform(True, stream)
+
+
+def batched_host_buffer_bytes(levels_list, inverse: bool = False) -> int:
+    if not levels_list:
+        return 0
+    d = len(levels_list[0])
+    return int(lib.sgh_batched_host_buffer_bytes(_flat_levels(levels_list, d), d, len(levels_list),
+                                                 FLAG_DEHIERARCHIZE if inverse else 0))
+
+
+def transform_batched_host(host_grids, levels_list, device_buffer: torch.Tensor, inverse: bool = False, stream=None):
+    """End-to-end transform of HOST grids (CPU float64 tensors, pinned for speed),
+    streamed through ``device_buffer`` (>= batched_host_buffer_bytes bytes)."""
+    G = len(host_grids)
+    if G == 0:
+        return
+    d = len(levels_list[0])
+    for h, lv in zip(host_grids, levels_list):
+        if h.is_cuda or h.dtype != torch.float64 or not h.is_contiguous() or h.numel() != num_points(lv):
+            raise ValueError("host grids must be contiguous CPU float64 tensors of the right size")
+    ptrs = (ctypes.c_void_p * G)(*[h.data_ptr() for h in host_grids])
+    with torch.cuda.device(device_buffer.device):
+        _check(lib.sgh_transform_batched_host(ptrs, _flat_levels(levels_list, d), d, G,
+                                              FLAG_DEHIERARCHIZE if inverse else 0,
+                                              ctypes.c_void_p(device_buffer.data_ptr()),
+                                              device_buffer.numel() * device_buffer.element_size(),
+                                              _stream(stream)))
+
+
+# ----------------------------------------------------------------- sharded
+def shard_rows(levels, nranks: int, rank: int):
+    """0-based rows [begin, end) of x_d owned by ``rank`` (host-only)."""
+    a, d = _levels_arr(levels)
+    b, e = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.sgh_shard_rows(a, d, int(nranks), int(rank), ctypes.byref(b), ctypes.byref(e)))
+    return int(b.value), int(e.value)
+
+
+def sharded_workspace_bytes(levels, nranks: int) -> int:
+    a, d = _levels_arr(levels)
+    return int(lib.sgh_sharded_workspace_bytes(a, d, int(nranks)))
+
+
+class ShardComm:
+    """libsgh-owned NCCL communicator; the unique id travels over ``group``."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            _check(lib.sgh_comm_unique_id(buf))
+            uid = torch.tensor(list(buf), dtype=torch.uint8)
+        obj = [uid.tolist()]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        raw = (ctypes.c_uint8 * 128)(*obj[0])
+        h = ctypes.c_void_p()
+        _check(lib.sgh_comm_create(ctypes.byref(h), raw, world, rank))
+        self.handle, self.rank, self.world = h, rank, world
+
+    def transform(self, shard: torch.Tensor, levels, workspace: torch.Tensor, inverse=False, stream=None):
+        a, d = _levels_arr(levels)
+        f = lib.sgh_dehierarchize_sharded if inverse else lib.sgh_hierarchize_sharded
+        with torch.cuda.device(shard.device):
+            _check(f(_grid_ptr(shard, None), a, d, self.handle, ctypes.c_void_p(workspace.data_ptr()),
+                     workspace.numel() * workspace.element_size(), _stream(stream)))
+        return shard
+
+    def close(self):
+        if self.handle:
+            lib.sgh_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def transform_sharded_loopback(shards, levels, workspace: torch.Tensor, inverse=False, stream=None):
+    """All ranks' shards on one device; exchange = device copies (test utility)."""
+    P = len(shards)
+    a, d = _levels_arr(levels)
+    ptrs = (ctypes.c_void_p * P)(*[s.data_ptr() for s in shards])
+    with torch.cuda.device(workspace.device):
+        _check(lib.sgh_transform_sharded_loopback(ptrs, a, d, P, FLAG_DEHIERARCHIZE if inverse else 0,
+                                                  ctypes.c_void_p(workspace.data_ptr()),
+                                                  workspace.numel() * workspace.element_size(), _stream(stream)))

@@ -1,0 +1,527 @@
+// sgh_capi.cu -- the extern "C" surface of libsgh (include/sgh.h): argument
+// validation, the per-axis planner, single-grid and batched drivers, fill and
+// digest utilities.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/sgh.h"
+#include "sgh_common.cuh"
+#include "sgh_plan.hpp"
+
+namespace sgh {
+
+uint64_t host_splitmix_finalise(uint64_t z);
+int64_t util_chunks(int64_t n);
+cudaError_t launch_fill(const FillItem *d_items, const int64_t *d_prefix, int nitems, const FillItem &single,
+                        int64_t total_chunks, cudaStream_t st);
+cudaError_t launch_digest(const FillItem *d_items, const int64_t *d_prefix, int nitems, const FillItem &single,
+                          int64_t total_chunks, unsigned long long *d_out, cudaStream_t st);
+
+// ------------------------------------------------------------ bookkeeping
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+sgh_status cuda_fail(cudaError_t e, const char *where) {
+  set_error(std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+  return SGH_ERR_CUDA;
+}
+
+sgh_status invalid(const char *msg) {
+  set_error(msg);
+  return SGH_ERR_INVALID_ARGUMENT;
+}
+
+// levels: d in [1, SGH_MAX_D], l_k >= 1 -> INVALID; l_k > SGH_MAX_LEVEL or N*8 overflow -> CAPACITY
+sgh_status validate_levels(const int32_t *levels, int32_t d, int64_t *N_out) {
+  if (!levels) return invalid("levels is NULL");
+  if (d < 1 || d > SGH_MAX_D) return invalid("d out of range [1, SGH_MAX_D]");
+  int64_t N = 1;
+  for (int k = 0; k < d; ++k) {
+    if (levels[k] < 1) return invalid("level < 1");
+    if (levels[k] > SGH_MAX_LEVEL) {
+      set_error("level > SGH_MAX_LEVEL");
+      return SGH_ERR_CAPACITY;
+    }
+    const int64_t nk = (int64_t(1) << levels[k]) - 1;
+    if (N > (INT64_MAX / 8) / nk) {
+      set_error("grid size overflows int64 bytes");
+      return SGH_ERR_CAPACITY;
+    }
+    N *= nk;
+  }
+  if (N_out) *N_out = N;
+  return SGH_OK;
+}
+
+// ---------------------------------------------------------------- planner
+static int floor_log2(int64_t x) {
+  int r = -1;
+  while (x) { ++r; x >>= 1; }
+  return r;
+}
+
+void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64_t base, int l,
+               std::vector<Task> &phases) {
+  if (l <= 1 || O <= 0 || S <= 0) return;
+  const int64_t n = (int64_t(1) << l) - 1;
+  Task t;
+  std::memset(&t, 0, sizeof t);
+  t.grid = grid;
+  t.O = O;
+  t.OS = OS;
+  t.PS = PS;
+  t.S = S;
+  t.base = base;
+  t.l = l;
+  const bool contiguous_slabs = (PS == S) && (OS == n * S);
+  if (contiguous_slabs && S < kFlatMaxS) {
+    t.fS = make_fdiv((uint32_t)S);
+    if (n * S <= kFlatT) {                               // whole slabs per tile
+      t.kind = KIND_FLAT_SLABS;
+      t.t = l;
+      t.R = (int32_t)(kFlatT / (n * S));
+      t.tiles = (O + t.R - 1) / t.R;
+      t.fNS = make_fdiv((uint32_t)(n * S));
+      phases.push_back(t);
+      return;
+    }
+    const int tb = floor_log2(kFlatT / S);               // 2^tb * S <= kFlatT < 2^l * S
+    t.kind = KIND_FLAT_BLOCKS;
+    t.t = tb;
+    t.tiles = O << (l - tb);
+    phases.push_back(t);
+    plan_view(grid, O, OS, PS << tb, S, base + ((int64_t(1) << tb) - 1) * PS, l - tb, phases);
+    return;
+  }
+  if (l <= kRegMaxL) {
+    t.kind = KIND_REG;
+    t.t = l;
+    t.tiles = (O * S + kThreads - 1) / kThreads;
+    phases.push_back(t);
+    return;
+  }
+  const int tb = std::min(l, kStridedMaxT);
+  t.kind = KIND_STRIDED;
+  t.t = tb;
+  t.ncb = (S + kStridedW - 1) / kStridedW;
+  t.tiles = (O << (l - tb)) * t.ncb;
+  phases.push_back(t);
+  if (tb < l) plan_view(grid, O, OS, PS << tb, S, base + ((int64_t(1) << tb) - 1) * PS, l - tb, phases);
+}
+
+void plan_axis(double *grid, const int32_t *levels, int d, int k, std::vector<Task> &phases, int64_t rows_last) {
+  int64_t S = 1, O = 1;
+  for (int j = 0; j < k; ++j) S *= (int64_t(1) << levels[j]) - 1;
+  for (int j = k + 1; j < d; ++j) O *= (j == d - 1 && rows_last >= 0) ? rows_last : (int64_t(1) << levels[j]) - 1;
+  const int64_t n = (int64_t(1) << levels[k]) - 1;
+  plan_view(grid, O, n * S, S, S, 0, levels[k], phases);
+}
+
+// ------------------------------------------------- pinned staging ring
+// Task tables are staged in pinned host memory and copied asynchronously into
+// the caller's workspace.  A slot is reused only after its copy has completed.
+struct StagingSlot {
+  void *host = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+};
+struct StagingRing {
+  StagingSlot slot[4];
+  int next = 0;
+};
+static std::mutex g_ring_mu;
+static std::map<int, StagingRing> g_rings;
+
+// copy `bytes` from `src` to device `dst` on `stream` via a pinned slot
+sgh_status staged_upload(void *dst, const void *src, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0) return SGH_OK;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  StagingRing &ring = g_rings[dev];
+  StagingSlot &s = ring.slot[ring.next];
+  ring.next = (ring.next + 1) % 4;
+  if (s.pending) {
+    e = cudaEventSynchronize(s.done);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize(staging)");
+    s.pending = false;
+  }
+  if (!s.done) {
+    e = cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+  }
+  if (s.cap < bytes) {
+    if (s.host) cudaFreeHost(s.host);
+    s.host = nullptr;
+    s.cap = 0;
+    size_t cap = std::max(bytes, size_t(1) << 20);
+    e = cudaHostAlloc(&s.host, cap, cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc(staging)");
+    s.cap = cap;
+  }
+  std::memcpy(s.host, src, bytes);
+  e = cudaMemcpyAsync(dst, s.host, bytes, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(task table)");
+  e = cudaEventRecord(s.done, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(staging)");
+  s.pending = true;
+  return SGH_OK;
+}
+
+// ---------------------------------------------------------- single grid
+static sgh_status transform_single(double *grid, const int32_t *levels, int32_t d, const int32_t *axis_order,
+                                   uint32_t axis_mask, uint32_t flags, void *stream) {
+  int64_t N = 0;
+  sgh_status st = validate_levels(levels, d, &N);
+  if (st != SGH_OK) return st;
+  if (!grid) return invalid("grid is NULL");
+  int order[SGH_MAX_D];
+  if (axis_order) {
+    bool seen[SGH_MAX_D] = {false};
+    for (int k = 0; k < d; ++k) {
+      if (axis_order[k] < 0 || axis_order[k] >= d || seen[axis_order[k]]) return invalid("axis_order is not a permutation");
+      seen[axis_order[k]] = true;
+      order[k] = axis_order[k];
+    }
+  } else {
+    for (int k = 0; k < d; ++k) order[k] = k;
+  }
+  if (axis_mask == 0) axis_mask = 0xffffffffu;
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
+  const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<Task> phases;
+  for (int kk = 0; kk < d; ++kk) {
+    const int k = order[kk];
+    if (!((axis_mask >> k) & 1u)) continue;
+    phases.clear();
+    plan_axis(grid, levels, d, k, phases);
+    if (inv) std::reverse(phases.begin(), phases.end());   // coarse lattice first (H2)
+    for (const Task &t : phases) {
+      cudaError_t e = launch_single(t, inv, s);
+      if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+      count_launch();
+    }
+  }
+  return SGH_OK;
+}
+
+// -------------------------------------------------------------- batched
+struct Segment {
+  int kind, l;
+  size_t task_off;    // index of first task in the table
+  size_t prefix_off;  // index of first prefix entry
+  int32_t ntasks;
+  int64_t tiles;
+  size_t smem;        // max dynamic shared memory over the segment's tasks
+  double points;      // points the segment transforms (profiling)
+};
+
+struct BatchedPlan {
+  std::vector<Task> tasks;
+  std::vector<int64_t> prefix;
+  std::vector<Segment> segs;
+  size_t table_bytes() const {
+    return (tasks.size() * sizeof(Task) + 255) / 256 * 256 + prefix.size() * sizeof(int64_t);
+  }
+};
+
+static void build_batched_plan(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv,
+                               BatchedPlan &P) {
+  std::vector<std::vector<Task>> per(num_grids);
+  for (int k = 0; k < d; ++k) {
+    size_t maxp = 0;
+    for (int64_t g = 0; g < num_grids; ++g) {
+      per[g].clear();
+      plan_axis(grids ? grids[g] : nullptr, levels + g * d, d, k, per[g]);
+      if (inv) std::reverse(per[g].begin(), per[g].end());
+      maxp = std::max(maxp, per[g].size());
+    }
+    for (size_t j = 0; j < maxp; ++j) {
+      // group phase j of all grids by kernel instance (kind, and l for REG)
+      std::map<std::pair<int, int>, std::vector<const Task *>> groups;
+      for (int64_t g = 0; g < num_grids; ++g)
+        if (j < per[g].size()) {
+          const Task &t = per[g][j];
+          groups[{t.kind, t.kind == KIND_REG ? t.l : 0}].push_back(&t);
+        }
+      for (auto &kv : groups) {
+        Segment sg;
+        sg.kind = kv.first.first;
+        sg.l = kv.first.second;
+        sg.task_off = P.tasks.size();
+        sg.prefix_off = P.prefix.size();
+        sg.ntasks = (int32_t)kv.second.size();
+        int64_t acc = 0;
+        sg.smem = 0;
+        sg.points = 0;
+        for (const Task *t : kv.second) {
+          sg.smem = std::max(sg.smem, task_smem(*t));
+          sg.points += task_points(*t);
+          P.tasks.push_back(*t);
+          P.prefix.push_back(acc);
+          acc += t->tiles;
+        }
+        P.prefix.push_back(acc);
+        sg.tiles = acc;
+        P.segs.push_back(sg);
+      }
+    }
+  }
+}
+
+size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv) {
+  BatchedPlan P;
+  build_batched_plan(grids, levels, d, num_grids, inv, P);
+  return P.segs.empty() ? 0 : P.table_bytes();
+}
+
+static sgh_status validate_batch(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
+                                 bool need_grids) {
+  if (num_grids < 0) return invalid("num_grids < 0");
+  if (num_grids == 0) return SGH_OK;
+  if (!levels) return invalid("levels is NULL");
+  if (need_grids && !grids) return invalid("grids is NULL");
+  for (int64_t g = 0; g < num_grids; ++g) {
+    sgh_status st = validate_levels(levels + g * d, d, nullptr);
+    if (st != SGH_OK) return st;
+    if (need_grids && !grids[g]) return invalid("grids[g] is NULL");
+  }
+  return SGH_OK;
+}
+
+sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
+                              uint32_t flags, void *workspace, size_t ws_bytes, cudaStream_t s) {
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
+  sgh_status st = validate_batch(grids, levels, d, num_grids, true);
+  if (st != SGH_OK) return st;
+  if (num_grids == 0) return SGH_OK;
+  const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
+  BatchedPlan P;
+  build_batched_plan(grids, levels, d, num_grids, inv, P);
+  if (P.segs.empty()) return SGH_OK;
+  const size_t bytes = P.table_bytes();
+  if (!workspace || ws_bytes < bytes || (reinterpret_cast<uintptr_t>(workspace) & 15)) {
+    set_error("workspace missing, misaligned or smaller than sgh_batched_workspace_bytes()");
+    return SGH_ERR_WORKSPACE;
+  }
+  std::vector<unsigned char> host(bytes, 0);
+  const size_t prefix_base = (P.tasks.size() * sizeof(Task) + 255) / 256 * 256;
+  std::memcpy(host.data(), P.tasks.data(), P.tasks.size() * sizeof(Task));
+  std::memcpy(host.data() + prefix_base, P.prefix.data(), P.prefix.size() * sizeof(int64_t));
+  st = staged_upload(workspace, host.data(), bytes, s);
+  if (st != SGH_OK) return st;
+  const Task *d_tasks = reinterpret_cast<const Task *>(workspace);
+  const int64_t *d_prefix = reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + prefix_base);
+  for (const Segment &sg : P.segs) {
+    cudaError_t e = launch_table(sg.kind, sg.l, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off, sg.ntasks,
+                                 sg.tiles, sg.smem, sg.points, s);
+    if (e != cudaSuccess) return cuda_fail(e, "grouped kernel launch");
+    count_launch();
+  }
+  return SGH_OK;
+}
+
+// per-device scratch for single-grid digests (allocated once, not in a hot call)
+static std::mutex g_scratch_mu;
+static std::map<int, unsigned long long *> g_digest_scratch;
+
+}  // namespace sgh
+
+using namespace sgh;
+
+extern "C" {
+
+int64_t sgh_num_points(const int32_t *levels, int32_t d) {
+  int64_t N = 0;
+  if (validate_levels(levels, d, &N) != SGH_OK) return -1;
+  return N;
+}
+
+sgh_status sgh_hierarchize(double *grid, const int32_t *levels, int32_t d, void *stream) {
+  return transform_single(grid, levels, d, nullptr, 0u, SGH_FLAG_NONE, stream);
+}
+
+sgh_status sgh_dehierarchize(double *grid, const int32_t *levels, int32_t d, void *stream) {
+  return transform_single(grid, levels, d, nullptr, 0u, SGH_FLAG_DEHIERARCHIZE, stream);
+}
+
+sgh_status sgh_transform_ex(double *grid, const int32_t *levels, int32_t d, const int32_t *axis_order,
+                            uint32_t axis_mask, uint32_t flags, void *stream) {
+  return transform_single(grid, levels, d, axis_order, axis_mask, flags, stream);
+}
+
+size_t sgh_batched_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
+  if (validate_batch(nullptr, levels, d, num_grids, false) != SGH_OK || num_grids == 0) return 0;
+  BatchedPlan P;
+  build_batched_plan(nullptr, levels, d, num_grids, (flags & SGH_FLAG_DEHIERARCHIZE) != 0, P);
+  return P.table_bytes();
+}
+
+sgh_status sgh_hierarchize_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
+                                   uint32_t flags, void *workspace, size_t ws_bytes, void *stream) {
+  return run_batched(grids, levels, d, num_grids, flags, workspace, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+sgh_status sgh_fill_uniform(double *grid, int64_t n, uint64_t seed, uint64_t grid_id, int64_t index_offset,
+                            void *stream) {
+  if (n < 0) return invalid("n < 0");
+  if (n == 0) return SGH_OK;
+  if (!grid) return invalid("grid is NULL");
+  FillItem f{grid, n, host_splitmix_finalise(seed ^ host_splitmix_finalise(grid_id)), index_offset};
+  cudaError_t e = launch_fill(nullptr, nullptr, 1, f, util_chunks(n), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fill launch");
+  count_launch();
+  return SGH_OK;
+}
+
+static sgh_status make_items(double *const *grids, const int64_t *sizes, const uint64_t *grid_ids, int64_t num_grids,
+                             uint64_t seed, std::vector<unsigned char> &host, size_t &prefix_base, int64_t &chunks) {
+  std::vector<FillItem> items(num_grids);
+  std::vector<int64_t> prefix(num_grids + 1);
+  int64_t acc = 0;
+  for (int64_t g = 0; g < num_grids; ++g) {
+    if (!grids[g] || sizes[g] < 0) return invalid("bad grid pointer or size");
+    const uint64_t gid = grid_ids ? grid_ids[g] : 0;
+    items[g] = FillItem{grids[g], sizes[g], host_splitmix_finalise(seed ^ host_splitmix_finalise(gid)), 0};
+    prefix[g] = acc;
+    acc += util_chunks(sizes[g]);
+  }
+  prefix[num_grids] = acc;
+  chunks = acc;
+  prefix_base = (num_grids * sizeof(FillItem) + 255) / 256 * 256;
+  host.assign(prefix_base + (num_grids + 1) * sizeof(int64_t), 0);
+  std::memcpy(host.data(), items.data(), num_grids * sizeof(FillItem));
+  std::memcpy(host.data() + prefix_base, prefix.data(), (num_grids + 1) * sizeof(int64_t));
+  return SGH_OK;
+}
+
+sgh_status sgh_fill_uniform_batched(double *const *grids, const int64_t *sizes, const uint64_t *grid_ids,
+                                    int64_t num_grids, uint64_t seed, void *workspace, size_t ws_bytes,
+                                    void *stream) {
+  if (num_grids < 0) return invalid("num_grids < 0");
+  if (num_grids == 0) return SGH_OK;
+  if (!grids || !sizes) return invalid("grids/sizes is NULL");
+  std::vector<unsigned char> host;
+  size_t pb = 0;
+  int64_t chunks = 0;
+  sgh_status st = make_items(grids, sizes, grid_ids, num_grids, seed, host, pb, chunks);
+  if (st != SGH_OK) return st;
+  if (!workspace || ws_bytes < host.size()) {
+    set_error("workspace too small for batched fill");
+    return SGH_ERR_WORKSPACE;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  st = staged_upload(workspace, host.data(), host.size(), s);
+  if (st != SGH_OK) return st;
+  FillItem dummy{};
+  cudaError_t e = launch_fill(reinterpret_cast<const FillItem *>(workspace),
+                              reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + pb),
+                              (int)num_grids, dummy, chunks, s);
+  if (e != cudaSuccess) return cuda_fail(e, "batched fill launch");
+  count_launch();
+  return SGH_OK;
+}
+
+sgh_status sgh_digest(const double *grid, int64_t n, int64_t index_offset, uint64_t *out_host, void *stream) {
+  if (n < 0 || !out_host) return invalid("bad digest arguments");
+  if (n == 0) { *out_host = 0; return SGH_OK; }
+  if (!grid) return invalid("grid is NULL");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  unsigned long long *acc = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    auto it = g_digest_scratch.find(dev);
+    if (it == g_digest_scratch.end()) {
+      e = cudaMalloc(&acc, sizeof(unsigned long long));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(digest scratch)");
+      g_digest_scratch[dev] = acc;
+    } else {
+      acc = it->second;
+    }
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  e = cudaMemsetAsync(acc, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  FillItem f{const_cast<double *>(grid), n, 0, index_offset};
+  e = launch_digest(nullptr, nullptr, 1, f, util_chunks(n), acc, s);
+  if (e != cudaSuccess) return cuda_fail(e, "digest launch");
+  count_launch();
+  unsigned long long h = 0;
+  e = cudaMemcpyAsync(&h, acc, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(digest)");
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize(digest)");
+  *out_host = h;
+  return SGH_OK;
+}
+
+sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_t num_grids, uint64_t *out_host,
+                              void *workspace, size_t ws_bytes, void *stream) {
+  if (num_grids < 0) return invalid("num_grids < 0");
+  if (num_grids == 0) return SGH_OK;
+  if (!grids || !sizes || !out_host) return invalid("NULL argument");
+  std::vector<unsigned char> host;
+  size_t pb = 0;
+  int64_t chunks = 0;
+  sgh_status st = make_items(grids, sizes, nullptr, num_grids, 0, host, pb, chunks);
+  if (st != SGH_OK) return st;
+  const size_t out_off = (host.size() + 255) / 256 * 256;
+  const size_t need = out_off + num_grids * sizeof(unsigned long long);
+  if (!workspace || ws_bytes < need) {
+    set_error("workspace too small for batched digest");
+    return SGH_ERR_WORKSPACE;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned char *ws = static_cast<unsigned char *>(workspace);
+  unsigned long long *d_out = reinterpret_cast<unsigned long long *>(ws + out_off);
+  cudaError_t e = cudaMemsetAsync(d_out, 0, num_grids * sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  st = staged_upload(ws, host.data(), host.size(), s);
+  if (st != SGH_OK) return st;
+  FillItem dummy{};
+  e = launch_digest(reinterpret_cast<const FillItem *>(ws), reinterpret_cast<const int64_t *>(ws + pb),
+                    (int)num_grids, dummy, chunks, d_out, s);
+  if (e != cudaSuccess) return cuda_fail(e, "batched digest launch");
+  count_launch();
+  e = cudaMemcpyAsync(out_host, d_out, num_grids * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(digests)");
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize(digests)");
+  return SGH_OK;
+}
+
+uint64_t sgh_launch_count(void) { return g_launches.load(); }
+
+const char *sgh_status_string(sgh_status s) {
+  switch (s) {
+    case SGH_OK: return "SGH_OK";
+    case SGH_ERR_INVALID_ARGUMENT: return "SGH_ERR_INVALID_ARGUMENT";
+    case SGH_ERR_CAPACITY: return "SGH_ERR_CAPACITY";
+    case SGH_ERR_CUDA: return "SGH_ERR_CUDA";
+    case SGH_ERR_NCCL: return "SGH_ERR_NCCL";
+    case SGH_ERR_WORKSPACE: return "SGH_ERR_WORKSPACE";
+    default: return "SGH_ERR_UNKNOWN";
+  }
+}
+
+const char *sgh_last_error(void) { return g_last_error.c_str(); }
+
+const char *sgh_version(void) { return "sgh 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

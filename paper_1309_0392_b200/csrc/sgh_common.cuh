@@ -1,0 +1,85 @@
+// sgh_common.cuh -- internal types of libsgh (not part of the C ABI).
+//
+// A hierarchization along one axis of one grid (one iteration of Alg. 1's
+// outer loop) is planned as a short list of PHASES.  Each phase is
+// a Task: a strided "pole view" of the grid plus the kernel kind that runs it.
+//
+// Pole view (all offsets in elements):
+//   element (o, i, r) with o in [0,O), 1-based pole index i in [1, n], n = 2^l-1,
+//   column r in [0,S) lives at   base + o*OS + (i-1)*PS + r.
+// The top-level view of axis k is O = prod_{j>k} n_j, S = prod_{j<k} n_j,
+// PS = S, OS = n_k*S, base = 0 (row-major, x_1 fastest: P:227).
+//
+// Long poles are split into aligned blocks of 2^t points (SURVEY 8(a) a3.iii,
+// derived from P:127 finest-first and P:140 predecessor rule): a point i with
+// tz(i) < t has both predecessors inside [b 2^t, (b+1) 2^t], so a block tile
+// with one halo row computes all its fine points.  The remaining "coarse
+// lattice" {i : 2^t | i} is itself a level-(l-t) pole view with
+//   PS' = 2^t PS,  base' = base + (2^t - 1) PS,
+// handled by a later phase (hierarchize) or an earlier one (dehierarchize).
+#pragma once
+#include <cstdint>
+
+namespace sgh {
+
+constexpr int kThreads = 256;      // every kernel runs 256-thread CTAs
+constexpr int kFlatT = 4096;       // FLAT tile: 2^12 elements (32 KB)
+constexpr int kFlatMaxS = 64;      // FLAT handles views with S < 64 columns
+constexpr int kFlatCap = kFlatT + kFlatMaxS + 2;
+constexpr int kStridedW = 32;      // STRIDED tile width (columns) = one warp
+constexpr int kStridedMaxT = 7;    // STRIDED tile: up to 2^7 + 1 = 129 rows
+constexpr int kRegMaxL = 4;        // REG kernel: poles of up to 15 points in registers
+
+enum Kind : int32_t {
+  KIND_FLAT_SLABS = 0,   // R whole slabs (o) per tile; needs PS==S, OS==n*S, n*S <= kFlatT
+  KIND_FLAT_BLOCKS = 1,  // one 2^t-row block (+halo) of one slab per tile; PS==S, OS==n*S
+  KIND_STRIDED = 2,      // (o, block, 32-column group) tiles, any strides
+  KIND_REG = 3,          // thread per column, whole pole in registers, l <= kRegMaxL
+  KIND_COUNT = 4
+};
+
+// magic-number division for 32-bit numerators < 2^31 (divisor >= 1)
+struct FDiv {
+  uint32_t d, m, s;
+};
+
+inline FDiv make_fdiv(uint32_t d) {
+  FDiv f;
+  f.d = d;
+  uint32_t s = 0;
+  while (s < 32 && (1ull << s) < d) ++s;
+  f.s = s;
+  f.m = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+  return f;
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FDiv &f) {
+  return (__umulhi(x, f.m) + x) >> f.s;
+}
+#endif
+
+struct Task {
+  double *grid;
+  int64_t O, OS, PS, S, base;
+  int64_t tiles;      // CTAs this task needs
+  int64_t ncb;        // STRIDED: column groups per (o, block)
+  int32_t l;          // pole level (n = 2^l - 1)
+  int32_t t;          // block level; t == l means whole poles
+  int32_t kind;
+  int32_t R;          // FLAT_SLABS: slabs per tile
+  FDiv fS;            // division by S   (FLAT kinds, S < 2^31)
+  FDiv fNS;           // division by n*S (FLAT_SLABS)
+};
+
+static_assert(sizeof(Task) % 8 == 0, "Task must stay 8-byte aligned");
+
+// harness utilities (fill / digest) work on lists of these
+struct FillItem {
+  double *ptr;
+  int64_t n;
+  uint64_t key;          // mix64(seed ^ mix64(grid_id)); unused by the digest
+  int64_t index_offset;  // global flat index of ptr[0]
+};
+
+}  // namespace sgh

@@ -1,0 +1,163 @@
+// sgh_host.cu -- end-to-end batched transform on HOST buffers.
+//
+// The combination grids live in host memory (the iterated combination
+// technique's solver owns them); they are streamed through the device in
+// chunks: copy-in on one internal stream, the grouped transform on the
+// caller's stream, copy-out on another, so PCIe traffic in both directions
+// overlaps the transform of neighbouring chunks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "../../include/sgh.h"
+#include "sgh_common.cuh"
+#include "sgh_plan.hpp"
+
+namespace sgh {
+
+constexpr size_t kChunkBytes = size_t(512) << 20;
+
+struct HostLayout {
+  std::vector<size_t> grid_off;              // byte offset of each grid in the device buffer
+  std::vector<std::pair<int64_t, int64_t>> chunks;  // [g0, g1)
+  std::vector<size_t> table_off;             // byte offset of each chunk's task table
+  size_t total = 0;
+};
+
+static sgh_status host_layout(const int32_t *levels, int32_t d, int64_t num_grids, bool inv, HostLayout &L) {
+  L.grid_off.resize(num_grids);
+  size_t off = 0;
+  size_t acc = 0;
+  int64_t g0 = 0;
+  for (int64_t g = 0; g < num_grids; ++g) {
+    int64_t N = 0;
+    sgh_status st = validate_levels(levels + g * d, d, &N);
+    if (st != SGH_OK) return st;
+    L.grid_off[g] = off;
+    const size_t bytes = size_t(N) * 8;
+    off += (bytes + 255) / 256 * 256;
+    acc += bytes;
+    if (acc >= kChunkBytes || g == num_grids - 1) {
+      L.chunks.push_back({g0, g + 1});
+      g0 = g + 1;
+      acc = 0;
+    }
+  }
+  for (auto &c : L.chunks) {
+    L.table_off.push_back(off);
+    const size_t tb = batched_table_bytes(nullptr, levels + c.first * d, d, c.second - c.first, inv);
+    off += (tb + 255) / 256 * 256;
+  }
+  L.total = off;
+  return SGH_OK;
+}
+
+struct HostStreams {
+  cudaStream_t in = nullptr, out = nullptr;
+};
+static std::mutex g_hs_mu;
+static std::map<int, HostStreams> g_hs;
+
+static sgh_status get_streams(HostStreams &hs) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_hs_mu);
+  HostStreams &h = g_hs[dev];
+  if (!h.in) {
+    if ((e = cudaStreamCreateWithFlags(&h.in, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+    if ((e = cudaStreamCreateWithFlags(&h.out, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+  }
+  hs = h;
+  return SGH_OK;
+}
+
+}  // namespace sgh
+
+using namespace sgh;
+
+extern "C" {
+
+size_t sgh_batched_host_buffer_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
+  if (!levels || num_grids <= 0) return 0;
+  HostLayout L;
+  if (host_layout(levels, d, num_grids, (flags & SGH_FLAG_DEHIERARCHIZE) != 0, L) != SGH_OK) return 0;
+  return L.total;
+}
+
+sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *levels, int32_t d,
+                                      int64_t num_grids, uint32_t flags, void *device_buffer,
+                                      size_t device_buffer_bytes, void *stream) {
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
+  if (num_grids < 0) return invalid("num_grids < 0");
+  if (num_grids == 0) return SGH_OK;
+  if (!host_grids || !levels) return invalid("NULL argument");
+  for (int64_t g = 0; g < num_grids; ++g)
+    if (!host_grids[g]) return invalid("host_grids[g] is NULL");
+  const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
+  HostLayout L;
+  sgh_status st = host_layout(levels, d, num_grids, inv, L);
+  if (st != SGH_OK) return st;
+  if (!device_buffer || device_buffer_bytes < L.total || (reinterpret_cast<uintptr_t>(device_buffer) & 255)) {
+    set_error("device_buffer missing, misaligned or smaller than sgh_batched_host_buffer_bytes()");
+    return SGH_ERR_WORKSPACE;
+  }
+  HostStreams hs;
+  if ((st = get_streams(hs)) != SGH_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned char *base = static_cast<unsigned char *>(device_buffer);
+  std::vector<double *> dptr(num_grids);
+  std::vector<int64_t> N(num_grids);
+  for (int64_t g = 0; g < num_grids; ++g) {
+    dptr[g] = reinterpret_cast<double *>(base + L.grid_off[g]);
+    validate_levels(levels + g * d, d, &N[g]);
+  }
+  cudaError_t e;
+  cudaEvent_t ev_start;
+  if ((e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+  cudaEventRecord(ev_start, s);
+  cudaStreamWaitEvent(hs.in, ev_start, 0);
+  cudaStreamWaitEvent(hs.out, ev_start, 0);
+  cudaEventDestroy(ev_start);
+  cudaEvent_t last_out = nullptr;
+  for (size_t c = 0; c < L.chunks.size(); ++c) {
+    const int64_t g0 = L.chunks[c].first, g1 = L.chunks[c].second;
+    for (int64_t g = g0; g < g1; ++g) {
+      e = cudaMemcpyAsync(dptr[g], host_grids[g], size_t(N[g]) * 8, cudaMemcpyHostToDevice, hs.in);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+    }
+    cudaEvent_t ev_in, ev_comp, ev_out;
+    cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_comp, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming);
+    cudaEventRecord(ev_in, hs.in);
+    cudaStreamWaitEvent(s, ev_in, 0);
+    void *ws = base + L.table_off[c];
+    const size_t ws_bytes = (c + 1 < L.table_off.size() ? L.table_off[c + 1] : L.total) - L.table_off[c];
+    st = run_batched(dptr.data() + g0, levels + g0 * d, d, g1 - g0, flags, ws, ws_bytes, s);
+    if (st != SGH_OK) return st;
+    cudaEventRecord(ev_comp, s);
+    cudaStreamWaitEvent(hs.out, ev_comp, 0);
+    for (int64_t g = g0; g < g1; ++g) {
+      e = cudaMemcpyAsync(host_grids[g], dptr[g], size_t(N[g]) * 8, cudaMemcpyDeviceToHost, hs.out);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+    }
+    cudaEventRecord(ev_out, hs.out);
+    cudaEventDestroy(ev_in);
+    cudaEventDestroy(ev_comp);
+    if (last_out) cudaEventDestroy(last_out);
+    last_out = ev_out;
+  }
+  if (last_out) {
+    cudaStreamWaitEvent(s, last_out, 0);
+    cudaEventDestroy(last_out);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "e2e batched");
+  return SGH_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// sgh_plan.hpp -- host-side planning of per-axis passes into kernel phases.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sgh.h"
+#include "sgh_common.cuh"
+
+namespace sgh {
+
+// launchers (sgh_kernels.cu)
+cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream);
+cudaError_t launch_table(int kind, int l, bool inv, const Task *d_tasks, const int64_t *d_prefix,
+                         int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream);
+size_t task_smem(const Task &t);
+
+// per-launch profiling (sgh_profile.cu); a no-op unless sgh_profile_enable(1)
+struct ProfToken {
+  cudaEvent_t start;
+};
+ProfToken prof_begin(cudaStream_t s);
+void prof_end(ProfToken tok, int kind, int l, bool inv, double bytes, cudaStream_t s);
+
+// points a task transforms (= writes): 16 B each is its algorithmic traffic
+inline double task_points(const Task &t) {
+  const int64_t n = (int64_t(1) << t.l) - 1;
+  const int64_t coarse = (t.t < t.l) ? (int64_t(1) << (t.l - t.t)) - 1 : 0;
+  return double(t.O) * double(t.S) * double(n - coarse);
+}
+
+// error bookkeeping (sgh_capi.cu)
+void set_error(const std::string &msg);
+void count_launch(uint64_t k = 1);
+
+// Phases of one pole view in HIERARCHIZATION order (block tiles first, then
+// the coarse lattice).  Dehierarchization runs them in reverse order.
+void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64_t base, int l,
+               std::vector<Task> &phases);
+
+// Phases of the axis-k pass (0-based) of a grid with level vector levels[0..d).
+// rows_last >= 0 overrides the extent of the last axis (a row shard of the
+// grid, sharded path); then k must be < d-1.
+void plan_axis(double *grid, const int32_t *levels, int d, int k, std::vector<Task> &phases,
+               int64_t rows_last = -1);
+
+// helpers shared by the drivers (sgh_capi.cu)
+sgh_status cuda_fail(cudaError_t e, const char *where);
+sgh_status invalid(const char *msg);
+sgh_status validate_levels(const int32_t *levels, int32_t d, int64_t *N_out);
+sgh_status staged_upload(void *dst, const void *src, size_t bytes, cudaStream_t stream);
+// batched driver: transform num_grids grids whose task tables go to `workspace`
+sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
+                       uint32_t flags, void *workspace, size_t ws_bytes, cudaStream_t s);
+size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv);
+
+}  // namespace sgh

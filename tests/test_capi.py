@@ -1,0 +1,104 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol that
+include/sgh.h declares, and its host-only logic (geometry, validation, shard
+ranges, workspace sizing) behaves.  No compute call is made here (no GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1309_0392_b200 as sgh
+import sgh_inputs as si
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "sgh.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sgh_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = _declared_symbols()
+    assert len(names) >= 20
+    L = ctypes.CDLL(sgh.LIB_PATH)
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    assert set(names) == set(sgh.EXPORTED)
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {sgh.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    for bad in ("sm_80", "sm_90", "sm_103"):
+        assert bad not in out
+
+
+def test_num_points():
+    assert sgh.num_points([3]) == 7
+    assert sgh.num_points([1, 1, 1]) == 1
+    assert sgh.num_points([2, 2]) == 9
+    assert sgh.num_points([14, 13]) == 134_193_153
+    assert sgh.num_points([0]) == -1
+    assert sgh.num_points([31]) == -1           # > SGH_MAX_LEVEL
+    assert sgh.num_points([30, 30, 30]) == -1   # N*8 overflows int64
+    assert sgh.num_points([1] * 17) == -1       # d > SGH_MAX_D
+
+
+def test_validation_before_enqueue():
+    """Invalid arguments are rejected on the host before any CUDA call."""
+    i32 = ctypes.c_int32
+    lv = (i32 * 2)(5, 0)
+    rc = sgh.lib.sgh_hierarchize(ctypes.c_void_p(0x1000), lv, 2, None)
+    assert rc == 1 and b"level" in sgh.lib.sgh_last_error()
+    lv = (i32 * 2)(5, 5)
+    assert sgh.lib.sgh_hierarchize(None, lv, 2, None) == 1
+    assert sgh.lib.sgh_hierarchize(ctypes.c_void_p(0x1000), lv, 0, None) == 1
+    big = (i32 * 1)(31)
+    assert sgh.lib.sgh_hierarchize(ctypes.c_void_p(0x1000), big, 1, None) == 2
+    bad_order = (i32 * 2)(0, 0)
+    assert sgh.lib.sgh_transform_ex(ctypes.c_void_p(0x1000), lv, 2, bad_order, 0, 0, None) == 1
+    assert sgh.lib.sgh_transform_ex(ctypes.c_void_p(0x1000), lv, 2, None, 0, 8, None) == 1   # unknown flag
+    # batched: negative count, missing workspace
+    ptrs = (ctypes.c_void_p * 1)(0x1000)
+    assert sgh.lib.sgh_hierarchize_batched(ptrs, lv, 2, -1, 0, None, 0, None) == 1
+    assert sgh.lib.sgh_hierarchize_batched(ptrs, lv, 2, 0, 0, None, 0, None) == 0      # empty batch OK
+    assert sgh.lib.sgh_hierarchize_batched(ptrs, lv, 2, 1, 0, None, 0, None) == 5      # workspace
+    assert sgh.lib.sgh_status_string(5) == b"SGH_ERR_WORKSPACE"
+
+
+def test_shard_rows_dyadic():
+    """Dyadic row shards of x_d: cover [0, n_d) exactly, rank 0
+    one row short, others 2^{l_d - p} rows."""
+    for levels in ([14, 13], [5, 4, 6], [3, 3]):
+        nd = (1 << levels[-1]) - 1
+        for P in (1, 2, 4, 8):
+            if (1 << levels[-1]) < P:
+                continue
+            rows = [sgh.shard_rows(levels, P, r) for r in range(P)]
+            assert rows[0][0] == 0 and rows[-1][1] == nd
+            for (b0, e0), (b1, e1) in zip(rows, rows[1:]):
+                assert e0 == b1
+            blk = 1 << (levels[-1] - P.bit_length() + 1)
+            assert rows[0][1] - rows[0][0] == blk - 1
+            assert all(e - b == blk for b, e in rows[1:])
+    with pytest.raises(sgh.SGHError):
+        sgh.shard_rows([3, 3], 3, 0)          # not a power of two
+    with pytest.raises(sgh.SGHError):
+        sgh.shard_rows([3, 2], 8, 0)          # more ranks than 2^{l_d}
+
+
+def test_workspace_sizing():
+    assert sgh.batched_workspace_bytes([]) == 0
+    c5 = si.combination_set(4, 22)
+    ws = sgh.batched_workspace_bytes(c5)
+    assert 0 < ws < 64 << 20
+    assert sgh.batched_host_buffer_bytes(c5) >= 8 * sum(si.num_points(l) for l in c5)
+    assert sgh.sharded_workspace_bytes([14, 13], 8) >= 2 * 8 * 1024 * 16383
+
+
+def test_no_cpu_fallback():
+    import torch
+    with pytest.raises(TypeError):
+        sgh.hierarchize(torch.zeros(961, dtype=torch.float64), [5, 5])

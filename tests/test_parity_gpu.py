@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: the per-axis kernels keep the oracle's per-point
+operation order, so every comparison here is BITWISE (0 differing 64-bit
+words).  Where the oracle cannot be run at full size (C5: 41 GB) the check is
+against golden digests written from the oracle / survey, plus sampled members
+compared with the oracle one by one.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import sgh_inputs as si
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SD = json.load(open(os.path.join(GOLD, "survey_digests.json")))
+
+
+@pytest.fixture(scope="module")
+def sgh(gpu):
+    import paper_1309_0392_b200 as m
+    return m
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def assert_bitwise(got, want):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    assert got.shape == want.shape
+    diff = np.nonzero(_bits(got) != _bits(want))[0]
+    assert diff.size == 0, f"{diff.size} differing words, first at {diff[:5]}: {got[diff[:3]]} vs {want[diff[:3]]}"
+
+
+def gpu_transform(sgh, u, levels, inverse=False, guard=4096, misalign=True, **kw):
+    """Run the CUDA path on a copy of u placed inside a NaN guard region, at an
+    8-mod-16 byte offset; check the guards are untouched; return the result."""
+    off = guard + (1 if misalign else 0)
+    buf = torch.full((u.size + 2 * off,), float("nan"), dtype=torch.float64, device="cuda")
+    g = buf[off:off + u.size]
+    g.copy_(torch.from_numpy(u))
+    sgh.transform(g, levels, inverse=inverse, **kw)
+    torch.cuda.synchronize()
+    host = buf.cpu().numpy()
+    assert np.all(np.isnan(host[:off])) and np.all(np.isnan(host[off + u.size:])), "guard region written"
+    return host[off:off + u.size].copy()
+
+
+# shapes that hit every kernel kind and edge: l=1 axes, N=1, S just below / at /
+# above the FLAT limit (S=31, 63, 127), long contiguous poles (FLAT_BLOCKS +
+# lattice recursion), long strided poles (STRIDED blocks + lattice), REG poles.
+SHAPES = [
+    (1,), (2,), (3,), (5,), (12,), (13,), (16,), (20,),
+    (1, 1), (1, 7), (7, 1), (2, 2), (5, 5), (3, 4), (2, 13), (13, 2), (6, 6), (6, 9), (7, 7), (7, 12), (5, 14),
+    (1, 1, 1), (3, 1, 4), (2, 5, 3), (4, 4, 4), (8, 2, 6), (1, 9, 2), (5, 5, 5), (2, 2, 10),
+    (2, 2, 2, 2), (1, 3, 1, 3), (3, 4, 3, 5), (4, 1, 5, 2), (6, 6, 2, 2),
+    (2, 3, 2, 3, 2), (1, 1, 1, 1, 9), (3, 2, 1, 2, 3, 2), (2, 2, 2, 2, 2, 2, 2), (2,) * 10,
+]
+
+
+@pytest.mark.parametrize("levels", SHAPES, ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_shape_sweep_bitwise(sgh, levels, inverse):
+    N = si.num_points(levels)
+    u = si.fill_uniform(N, grid_id=(N * 7 + len(levels)) % 9973)
+    want = u.copy()
+    (oracle.dehierarchize if inverse else oracle.hierarchize)(want, levels)
+    got = gpu_transform(sgh, u, levels, inverse=inverse)
+    assert_bitwise(got, want)
+
+
+@pytest.mark.parametrize("levels", [(5, 5), (3, 4, 2), (7, 6, 3), (2, 3, 2, 3)], ids=str)
+def test_axis_orders_and_masks(sgh, levels):
+    """Other axis orders: bitwise vs the oracle run in the same order."""
+    N = si.num_points(levels)
+    u = si.fill_uniform(N, grid_id=17)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        perm = [int(x) for x in rng.permutation(len(levels))]
+        want = oracle.hierarchize(u.copy(), levels, perm)
+        assert_bitwise(gpu_transform(sgh, u, levels, axis_order=perm), want)
+    # axis mask: only axis 0 and the last
+    mask = 1 | (1 << (len(levels) - 1))
+    want = u.copy()
+    oracle.hierarchize_axis(want, levels, 0)
+    if len(levels) > 1:
+        oracle.hierarchize_axis(want, levels, len(levels) - 1)
+    assert_bitwise(gpu_transform(sgh, u, levels, axis_mask=mask), want)
+
+
+@pytest.mark.parametrize("levels", [(5, 5), (8, 8, 8), (10, 4, 4, 4, 4), (14, 13)], ids=["C1", "C2", "C3", "C4"])
+def test_closed_form_bitwise(sgh, levels):
+    """f = prod x(1-x) -> alpha = prod 4^-lambda (BASELINE.json closed form), bitwise, at C1..C4."""
+    f = torch.from_numpy(si.fill_smooth(levels)).cuda()
+    sgh.hierarchize(f, levels)
+    lam = None
+    for l in levels:
+        i = torch.arange(1, 1 << l, device="cuda", dtype=torch.int64)
+        tz = torch.zeros_like(i)
+        for b in range(l):
+            tz += ((i & ((1 << (b + 1)) - 1)) == 0).to(torch.int64)
+        lk = l - tz
+        lam = lk if lam is None else (lk[:, None] + lam[None, :]).reshape(-1)
+    want = torch.ldexp(torch.ones_like(f), -2 * lam)
+    assert torch.equal(f, want)
+
+
+@pytest.mark.parametrize("levels", [(5, 5), (3, 4, 2), (9, 7)], ids=str)
+def test_tent_exact(sgh, levels):
+    f = torch.from_numpy(si.fill_tent(levels, 0.625)).cuda()
+    sgh.hierarchize(f, levels)
+    nz = torch.nonzero(f).flatten().tolist()
+    assert len(nz) == 1 and f[nz[0]].item() == 0.625
+
+
+def test_fill_matches_input_module_and_oracle(sgh):
+    for n, gid, off in [(1, 0, 0), (961, 0, 0), (100_003, 5, 17), (4097, 4254, 1 << 33)]:
+        g = torch.empty(n, dtype=torch.float64, device="cuda")
+        sgh.fill_uniform(g, si.SEED, gid, off)
+        host = g.cpu().numpy()
+        assert_bitwise(host, si.fill_uniform(n, si.SEED, gid, off))
+        assert sgh.digest(g, off) == oracle.digest(host, off)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_config_golden_and_oracle(sgh, name):
+    """Full-size configs: GPU digest == survey golden digest == oracle digest,
+    plus an element-wise bitwise check against the oracle's output."""
+    c = SD["configs"][name]
+    levels = c["levels"]
+    N = si.num_points(levels)
+    g = torch.empty(N, dtype=torch.float64, device="cuda")
+    sgh.fill_uniform(g, SD["seed"], c["grid_id"])
+    assert sgh.digest(g) == int(c["input"], 16)
+    sgh.hierarchize(g, levels)
+    assert sgh.digest(g) == int(c["hierarchized"], 16)
+    want = oracle.fill_uniform(N, SD["seed"], c["grid_id"])
+    oracle.hierarchize(want, levels)
+    assert_bitwise(g.cpu().numpy(), want)
+    assert float(g.abs().max()) == c["max_abs_alpha"]
+    if "dehierarchized_fill" in c:
+        sgh.fill_uniform(g, SD["seed"], c["grid_id"])
+        sgh.dehierarchize(g, levels)
+        assert sgh.digest(g) == int(c["dehierarchized_fill"], 16)
+
+
+@pytest.mark.parametrize("levels", [(8, 8, 8), (14, 13), (10, 4, 4, 4, 4)], ids=["C2", "C4", "C3"])
+def test_round_trip_device(sgh, levels):
+    N = si.num_points(levels)
+    g = torch.empty(N, dtype=torch.float64, device="cuda")
+    sgh.fill_uniform(g, 1, 2)
+    u = g.clone()
+    sgh.hierarchize(g, levels)
+    sgh.dehierarchize(g, levels)
+    err = (g - u).abs().max() / u.abs().max()
+    assert float(err) <= 1e-13
+
+
+# --------------------------------------------------------------- batched
+def _batch_check(sgh, members, ids, inverse=False):
+    b = sgh.GridBatch(members, grid_ids=ids)
+    b.fill_uniform(SD["seed"])
+    b.transform(inverse)
+    torch.cuda.synchronize()
+    for lv, gid, v in zip(members, ids, b.views):
+        want = oracle.fill_uniform(si.num_points(lv), SD["seed"], gid)
+        (oracle.dehierarchize if inverse else oracle.hierarchize)(want, lv)
+        assert_bitwise(v.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_batched_mixed_bitwise(sgh, inverse):
+    rng = np.random.default_rng(11)
+    members = [tuple(int(x) for x in rng.integers(1, 8, size=3)) for _ in range(60)]
+    members += [(1, 1, 1), (13, 1, 2), (1, 12, 1), (2, 2, 11), (7, 7, 3)]
+    _batch_check(sgh, members, list(range(len(members))), inverse)
+
+
+def test_batched_c5_sample_vs_oracle(sgh):
+    """A sample of the C5 set (every 97th member plus the extremes), each compared
+    with the oracle element by element."""
+    cs = si.combination_set(4, 22)
+    ids = sorted(set(list(range(0, len(cs), 97)) + [0, 1, 834, 1329, 1330, 4254]))
+    _batch_check(sgh, [cs[i] for i in ids], ids)
+
+
+def test_batched_c5_full_golden(sgh):
+    """The whole C5 set (4,255 grids, 41 GB) in one batched call: per-grid
+    digests summed == survey golden sums; four members == golden digests."""
+    cs = si.combination_set(4, 22)
+    free, _ = torch.cuda.mem_get_info()
+    if free < 46e9:
+        pytest.skip("needs ~42 GB of free device memory")
+    b = sgh.GridBatch(cs)
+    b.fill_uniform(SD["seed"])
+    din = b.digests()
+    assert sum(din) % (1 << 64) == int(SD["C5"]["sum_input"], 16)
+    b.hierarchize()
+    dh = b.digests()
+    assert sum(dh) % (1 << 64) == int(SD["C5"]["sum_hierarchized"], 16)
+    for gid, m in SD["C5"]["members"].items():
+        assert dh[int(gid)] == int(m["hierarchized"], 16)
+        assert din[int(gid)] == int(m["input"], 16)
+    b.dehierarchize()
+    for gid in (0, 1, 834, 2000, 4254):                # round trip, normwise (reading R10)
+        u = torch.from_numpy(oracle.fill_uniform(si.num_points(cs[gid]), SD["seed"], gid)).cuda()
+        assert float((b.views[gid] - u).abs().max() / u.abs().max()) <= 1e-13
+
+
+def test_batched_host_e2e(sgh):
+    cs = si.combination_set(4, 14)
+    hosts = [torch.from_numpy(si.fill_uniform(si.num_points(lv), SD["seed"], g)).pin_memory()
+             for g, lv in enumerate(cs)]
+    buf = torch.empty(sgh.batched_host_buffer_bytes(cs) // 8 + 64, dtype=torch.float64, device="cuda")
+    sgh.transform_batched_host(hosts, cs, buf)
+    torch.cuda.synchronize()
+    for g, (lv, h) in enumerate(zip(cs, hosts)):
+        want = oracle.hierarchize(si.fill_uniform(si.num_points(lv), SD["seed"], g), lv)
+        assert_bitwise(h.numpy(), want)
+
+
+# --------------------------------------------------------------- sharded
+@pytest.mark.parametrize("levels,P", [((6, 5), 2), ((6, 5), 4), ((5, 4, 6), 8), ((3, 7), 8), ((8, 2, 3, 4), 4),
+                                      ((14, 13), 8)], ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_sharded_loopback_bitwise(sgh, levels, P, inverse):
+    """The sharded algorithm (row shards of x_d, re-shard to column blocks,
+    axis-d pass, re-shard back) on P virtual ranks equals the single-grid
+    oracle bitwise."""
+    N = si.num_points(levels)
+    u = si.fill_uniform(N, grid_id=77)
+    want = u.copy()
+    (oracle.dehierarchize if inverse else oracle.hierarchize)(want, levels)
+    C = N // ((1 << levels[-1]) - 1)
+    shards = []
+    for r in range(P):
+        b, e = sgh.shard_rows(levels, P, r)
+        shards.append(torch.from_numpy(u[b * C:e * C].copy()).cuda())
+    ws = torch.empty(P * sgh.sharded_workspace_bytes(levels, P) // 8, dtype=torch.float64, device="cuda")
+    sgh.transform_sharded_loopback(shards, levels, ws, inverse=inverse)
+    got = torch.cat(shards).cpu().numpy()
+    assert_bitwise(got, want)
+
+
+def test_launch_count_increases(sgh):
+    before = sgh.launch_count()
+    g = torch.zeros(961, dtype=torch.float64, device="cuda")
+    sgh.hierarchize(g, [5, 5])
+    torch.cuda.synchronize()
+    assert sgh.launch_count() > before
