@@ -6,10 +6,12 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/sgh.h"
@@ -107,14 +109,28 @@ void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64
   if (l <= kRegMaxL) {
     t.kind = KIND_REG;
     t.t = l;
-    t.tiles = (O * S + kThreads - 1) / kThreads;
+    const int64_t cols_per_tile = int64_t(kThreads) * std::max(1, 16 / (int)n);   // RegCfg<L>::CPT
+    t.tiles = (O * S + cols_per_tile - 1) / cols_per_tile;
     phases.push_back(t);
     return;
   }
-  const int tb = std::min(l, kStridedMaxT);
+  // tile width: as wide as the columns allow (long contiguous row segments keep
+  // DRAM pages open), rows = 2^t + 1 within the SMEM budget
+  static int wpref = -1;
+  if (wpref < 0) {
+    const char *e = getenv("SGH_STRIDED_W");  // tuning experiment override
+    wpref = e ? atoi(e) : 128;
+    if (wpref != 32 && wpref != 64 && wpref != 128) wpref = 128;
+  }
+  int W = wpref;
+  while (W > 32 && S <= W / 2 + W / 4) W >>= 1;
+  int tmax = 0;
+  while (((int64_t(1) << (tmax + 1)) + 1) * (W + 2) <= kStridedTileDoubles) ++tmax;
+  const int tb = std::min(l, tmax);
   t.kind = KIND_STRIDED;
+  t.W = W;
   t.t = tb;
-  t.ncb = (S + kStridedW - 1) / kStridedW;
+  t.ncb = (S + W - 1) / W;
   t.tiles = (O << (l - tb)) * t.ncb;
   phases.push_back(t);
   if (tb < l) plan_view(grid, O, OS, PS << tb, S, base + ((int64_t(1) << tb) - 1) * PS, l - tb, phases);
@@ -164,13 +180,23 @@ sgh_status staged_upload(void *dst, const void *src, size_t bytes, cudaStream_t 
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
   }
   if (s.cap < bytes) {
-    if (s.host) cudaFreeHost(s.host);
-    s.host = nullptr;
-    s.cap = 0;
-    size_t cap = std::max(bytes, size_t(1) << 20);
-    e = cudaHostAlloc(&s.host, cap, cudaHostAllocDefault);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc(staging)");
-    s.cap = cap;
+    // grow every slot at once (geometrically) so steady-state calls never
+    // allocate pinned memory (cudaHostAlloc synchronises and takes ms)
+    size_t cap = std::max(bytes * 2, size_t(4) << 20);
+    for (StagingSlot &o : ring.slot) {
+      if (o.cap >= cap) continue;
+      if (o.pending) {
+        e = cudaEventSynchronize(o.done);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize(staging)");
+        o.pending = false;
+      }
+      if (o.host) cudaFreeHost(o.host);
+      o.host = nullptr;
+      o.cap = 0;
+      e = cudaHostAlloc(&o.host, cap, cudaHostAllocDefault);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc(staging)");
+      o.cap = cap;
+    }
   }
   std::memcpy(s.host, src, bytes);
   e = cudaMemcpyAsync(dst, s.host, bytes, cudaMemcpyHostToDevice, stream);
@@ -221,7 +247,7 @@ static sgh_status transform_single(double *grid, const int32_t *levels, int32_t 
 
 // -------------------------------------------------------------- batched
 struct Segment {
-  int kind, l;
+  int kind, l, w;
   size_t task_off;    // index of first task in the table
   size_t prefix_off;  // index of first prefix entry
   int32_t ntasks;
@@ -252,16 +278,17 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
     }
     for (size_t j = 0; j < maxp; ++j) {
       // group phase j of all grids by kernel instance (kind, and l for REG)
-      std::map<std::pair<int, int>, std::vector<const Task *>> groups;
+      std::map<std::tuple<int, int, int>, std::vector<const Task *>> groups;
       for (int64_t g = 0; g < num_grids; ++g)
         if (j < per[g].size()) {
           const Task &t = per[g][j];
-          groups[{t.kind, t.kind == KIND_REG ? t.l : 0}].push_back(&t);
+          groups[{t.kind, t.kind == KIND_REG ? t.l : 0, t.kind == KIND_STRIDED ? t.W : 0}].push_back(&t);
         }
       for (auto &kv : groups) {
         Segment sg;
-        sg.kind = kv.first.first;
-        sg.l = kv.first.second;
+        sg.kind = std::get<0>(kv.first);
+        sg.l = std::get<1>(kv.first);
+        sg.w = std::get<2>(kv.first);
         sg.task_off = P.tasks.size();
         sg.prefix_off = P.prefix.size();
         sg.ntasks = (int32_t)kv.second.size();
@@ -327,7 +354,7 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
   const Task *d_tasks = reinterpret_cast<const Task *>(workspace);
   const int64_t *d_prefix = reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + prefix_base);
   for (const Segment &sg : P.segs) {
-    cudaError_t e = launch_table(sg.kind, sg.l, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off, sg.ntasks,
+    cudaError_t e = launch_table(sg.kind, sg.l, sg.w, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off, sg.ntasks,
                                  sg.tiles, sg.smem, sg.points, s);
     if (e != cudaSuccess) return cuda_fail(e, "grouped kernel launch");
     count_launch();

@@ -26,8 +26,8 @@ constexpr int kThreads = 256;      // every kernel runs 256-thread CTAs
 constexpr int kFlatT = 4096;       // FLAT tile: 2^12 elements (32 KB)
 constexpr int kFlatMaxS = 64;      // FLAT handles views with S < 64 columns
 constexpr int kFlatCap = kFlatT + kFlatMaxS + 2;
-constexpr int kStridedW = 32;      // STRIDED tile width (columns) = one warp
-constexpr int kStridedMaxT = 7;    // STRIDED tile: up to 2^7 + 1 = 129 rows
+constexpr int kStridedWMax = 128;  // STRIDED tile width W in {32, 64, 128} columns
+constexpr int kStridedTileDoubles = 4480;  // STRIDED tile budget: (2^t + 1) * (W + 2) doubles (35 KB)
 constexpr int kRegMaxL = 4;        // REG kernel: poles of up to 15 points in registers
 
 enum Kind : int32_t {
@@ -68,6 +68,8 @@ struct Task {
   int32_t t;          // block level; t == l means whole poles
   int32_t kind;
   int32_t R;          // FLAT_SLABS: slabs per tile
+  int32_t W;          // STRIDED: tile width (columns)
+  int32_t pad_;
   FDiv fS;            // division by S   (FLAT kinds, S < 2^31)
   FDiv fNS;           // division by n*S (FLAT_SLABS)
 };

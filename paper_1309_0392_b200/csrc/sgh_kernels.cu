@@ -15,12 +15,19 @@
 //   FLAT_SLABS / FLAT_BLOCKS  views whose slab o is contiguous (PS == S, OS == n S) and S < 64:
 //                             the tile is one contiguous range of global memory.
 //   STRIDED                   32 adjacent columns x (2^t + 1) pole rows, warps read rows coalesced.
-//   REG<L>                    one thread per column holding the whole pole (n <= 31) in registers.
+//   REG<L>                    one thread per column holding the whole pole (n <= 15) in registers.
 // All kernels are persistent: a CTA walks tiles q = blockIdx.x, +gridDim.x, ...
 // over a task table (batched) or a single task (one grid).
+//
+// Memory-level parallelism: a tile is staged with cp.async (LDGSTS) -- every
+// thread issues all of its copies back to back, so the whole tile (up to 33 KB
+// per CTA, ~200 KB per SM) is in flight at once -- 16-byte copies on the
+// aligned body of contiguous ranges, 8-byte copies otherwise (rows of odd
+// length are only 8-byte aligned: SURVEY H1).
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "sgh_common.cuh"
 #include "sgh_plan.hpp"
@@ -34,6 +41,37 @@ struct Src {
   int64_t total_tiles;
   Task single;
 };
+
+// ------------------------------------------------------------- async copies
+__device__ __forceinline__ void cp_async8(double *sdst, const double *gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double *sdst, const double *gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// 8-byte phase of a global address (0: 16-byte aligned, 1: 8 mod 16)
+__device__ __forceinline__ int phase8(const double *p) { return (int)((reinterpret_cast<uintptr_t>(p) >> 3) & 1); }
+
+// Copy len doubles gsrc[0..len) -> sdst[0..len) where sdst and gsrc have the
+// same 16-byte phase: 8-byte head/tail, 16-byte body.  Issue only.
+__device__ __forceinline__ void copy_range_async(double *sdst, const double *gsrc, int len) {
+  if (len <= 0) return;
+  const int head = phase8(gsrc) ? 1 : 0;
+  const int pairs = (len - head) >> 1;
+  const int tail = len - head - 2 * pairs;
+  if (head && threadIdx.x == 0) cp_async8(sdst, gsrc);
+  if (tail && threadIdx.x == kThreads - 1) cp_async8(sdst + len - 1, gsrc + len - 1);
+  const double *g = gsrc + head;
+  double *s = sdst + head;
+#pragma unroll 4
+  for (int p = threadIdx.x; p < pairs; p += kThreads) cp_async16(s + 2 * p, g + 2 * p);
+}
 
 // Task index owning tile q.  `idx` is the cursor from the previous tile of this
 // CTA (tiles only increase), so the scan is amortised O(1).
@@ -70,7 +108,7 @@ __device__ __forceinline__ void for_each_tile(const Src &src, F &&body) {
 // Tile = R consecutive slabs (o0 .. o0+R-1), each n*S contiguous doubles.
 template <bool INV>
 __global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__ Src src) {
-  extern __shared__ double sm[];  // R*n*S doubles (<= kFlatT)
+  extern __shared__ __align__(16) double smem[];  // 1 + R*n*S doubles (<= kFlatT + 1)
   for_each_tile(src, [&](const Task &T, int64_t q) {
     const int l = T.l;
     const int n = (1 << l) - 1;
@@ -81,8 +119,9 @@ __global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__
     const int len = ns * nS;
     const FDiv fS = T.fS, fNS = T.fNS;
     double *__restrict__ g = T.grid + T.base + o0 * T.OS;
-#pragma unroll 4
-    for (int e = threadIdx.x; e < len; e += kThreads) sm[e] = g[e];
+    double *sm = smem + phase8(g);                      // same 16-byte phase as g
+    copy_range_async(sm, g, len);
+    cp_async_wait_all();
     __syncthreads();
     if (!INV) {
       for (int e = threadIdx.x; e < len; e += kThreads) {
@@ -116,7 +155,6 @@ __global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__
         }
         __syncthreads();
       }
-#pragma unroll 4
       for (int e = threadIdx.x; e < len; e += kThreads) g[e] = sm[e];
     }
     __syncthreads();
@@ -130,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__
 // points owned by another phase (read-only halo here).
 template <bool INV>
 __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant__ Src src) {
-  extern __shared__ double sm[];  // (2^t + 1) * S doubles
+  extern __shared__ __align__(16) double smem[];  // 1 + (2^t + 1) * S doubles
   for_each_tile(src, [&](const Task &T, int64_t q) {
     const int t = T.t;
     const int B = 1 << t;
@@ -143,14 +181,11 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
     const int rb_lo = (b == 0) ? 1 : 0;                    // row 0 of block 0 is the boundary
     const int rb_hi = (b == (1 << nb_log) - 1) ? B - 1 : B;  // row 2^l is the boundary
     const FDiv fS = T.fS;
-    // global offset of local element e = rb*S + r is  row0 + e
-    const int64_t row0 = T.base + o * T.OS + (int64_t)(i0 - 1) * S;
-    double *__restrict__ g = T.grid;
-    {
-      const int e0 = rb_lo * S, e1 = (rb_hi + 1) * S;
-#pragma unroll 4
-      for (int e = e0 + threadIdx.x; e < e1; e += kThreads) sm[e] = g[row0 + e];
-    }
+    // global element of local e = rb*S + r is  gr[e]
+    double *__restrict__ gr = T.grid + T.base + o * T.OS + (int64_t)(i0 - 1) * S;
+    double *sm = smem + phase8(gr);
+    copy_range_async(sm + rb_lo * S, gr + rb_lo * S, (rb_hi - rb_lo + 1) * S);
+    cp_async_wait_all();
     __syncthreads();
     if (!INV) {
       const int e1 = B * S;
@@ -162,7 +197,7 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
         double x = sm[e];
         if (i - s >= 1) x = x - 0.5 * sm[e - sS];
         if (i + s <= n) x = x - 0.5 * sm[e + sS];
-        g[row0 + e] = x;
+        gr[e] = x;
       }
     } else {
       for (int s = B >> 1; s >= 1; s >>= 1) {              // block-local levels, coarse -> fine
@@ -182,8 +217,7 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
         __syncthreads();
       }
       const int e1 = B * S;
-#pragma unroll 4
-      for (int e = S + threadIdx.x; e < e1; e += kThreads) g[row0 + e] = sm[e];
+      for (int e = S + threadIdx.x; e < e1; e += kThreads) gr[e] = sm[e];
     }
     __syncthreads();
   });
@@ -191,12 +225,42 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
 
 // ------------------------------------------------------------------- STRIDED
 // Tile = (o, block b, column group cb): rows rb = 0..2^t (pole index b 2^t + rb),
-// columns c0 .. c0+31.  Warp w moves rows w, w+8, ...; lane = column, so every
-// row segment is one coalesced 256-byte access.  t == l means the whole pole.
-template <bool INV>
+// W adjacent columns c0 .. c0+W-1 (W = 32/64/128, T.W).  t == l: whole pole.
+// SMEM rows have stride W + 2 doubles (16-byte aligned) and element c of row
+// rb sits at rb*(W+2) + c + par(rb), par = the 8-byte phase of the row's global
+// start, so global 16-byte pairs land on 16-byte aligned SMEM and are copied
+// with 16-byte cp.async.cg (no L1 allocation); the odd head / tail element of a
+// row uses an 8-byte copy.
+template <int W>
+__device__ __forceinline__ void strided_load_rows(double *sm, const double *rowbase, int64_t PS, int par0,
+                                                  int i0, int rb_lo, int rb_hi, int wc) {
+  constexpr int RS = W + 2;
+  constexpr int P = W / 2;          // 16-byte slots per row
+  constexpr int LOGP = (P == 16) ? 4 : (P == 32) ? 5 : 6;
+  const int psodd = (int)(PS & 1);
+  const int nslots = (rb_hi - rb_lo + 1) * P;
+#pragma unroll 4
+  for (int p = threadIdx.x; p < nslots; p += kThreads) {
+    const int rb = rb_lo + (p >> LOGP);
+    const int k = p & (P - 1);
+    const int i = i0 + rb;
+    const int par = (par0 + (i - 1) * psodd) & 1;
+    const double *gr = rowbase + (int64_t)(i - 1) * PS;
+    double *sr = sm + rb * RS + par;
+    const int npairs = (wc - par) >> 1;
+    const int c = par + 2 * k;
+    if (k < npairs) cp_async16(sr + c, gr + c);
+    if (k == P - 1 && par) cp_async8(sr, gr);                       // head element 0
+    const int last = par + 2 * npairs;                              // first element not covered
+    if (k == P - 2 && last < wc) cp_async8(sr + last, gr + last);   // tail element
+  }
+}
+
+template <bool INV, int W>
 __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Src src) {
-  extern __shared__ double sm_raw[];  // (2^t + 1) rows of kStridedW doubles
-  auto sm = reinterpret_cast<double (*)[kStridedW]>(sm_raw);
+  extern __shared__ __align__(16) double sm[];  // (2^t + 1) rows of W + 2 doubles
+  constexpr int RS = W + 2;
+  constexpr int CPL = W / 32;                    // columns per lane
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr int kWarps = kThreads / 32;
@@ -208,27 +272,37 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
     const int64_t rest = q / T.ncb;
     const int b = (int)(rest & ((1 << nb_log) - 1));
     const int64_t o = rest >> nb_log;
-    const int64_t c0 = cb * kStridedW;
-    const bool active = (c0 + lane) < T.S;
+    const int64_t c0 = cb * W;
+    const int wc = (int)min((int64_t)W, T.S - c0);
     const int n = (1 << T.l) - 1;
     const int i0 = b * B;
     const int rb_lo = (i0 == 0) ? 1 : 0;
     const int rb_hi = min(B, n - i0);
     const int64_t PS = T.PS;
-    double *__restrict__ g = T.grid + T.base + o * T.OS + c0 + lane - PS;  // + i*PS -> element (o,i,c0+lane)
-#pragma unroll 4
-    for (int rb = rb_lo + warp; rb <= rb_hi; rb += kWarps)
-      if (active) sm[rb][lane] = g[(int64_t)(i0 + rb) * PS];
+    const int psodd = (int)(PS & 1);
+    double *__restrict__ rowbase = T.grid + T.base + o * T.OS + c0;  // element (o, i, c0+c) = rowbase[(i-1)PS + c]
+    const int par0 = phase8(rowbase);
+    strided_load_rows<W>(sm, rowbase, PS, par0, i0, rb_lo, rb_hi, wc);
+    cp_async_wait_all();
     __syncthreads();
+    auto row = [&](int rb) -> double * { return sm + rb * RS + ((par0 + (i0 + rb - 1) * psodd) & 1); };
     const int rhi = (t == T.l) ? n : B - 1;
     if (!INV) {
       for (int rb = 1 + warp; rb <= rhi; rb += kWarps) {
         const int i = i0 + rb;
         const int s = rb & -rb;
-        double x = sm[rb][lane];
-        if (i - s >= 1) x = x - 0.5 * sm[rb - s][lane];
-        if (i + s <= n) x = x - 0.5 * sm[rb + s][lane];
-        if (active) g[(int64_t)i * PS] = x;
+        const double *xm = row(rb), *xl = row(rb - s), *xr = row(rb + s);
+        double *gout = rowbase + (int64_t)(i - 1) * PS;
+#pragma unroll
+        for (int u = 0; u < CPL; ++u) {
+          const int c = lane + 32 * u;
+          if (c < wc) {
+            double x = xm[c];
+            if (i - s >= 1) x = x - 0.5 * xl[c];
+            if (i + s <= n) x = x - 0.5 * xr[c];
+            gout[c] = x;
+          }
+        }
       }
     } else {
       const int s_top = (t == T.l) ? (B >> 2) : (B >> 1);
@@ -237,16 +311,28 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
         for (int j = warp; j < cnt; j += kWarps) {
           const int rb = s * (2 * j + 1);
           const int i = i0 + rb;
-          double x = sm[rb][lane];
-          if (i - s >= 1) x = x + 0.5 * sm[rb - s][lane];
-          if (i + s <= n) x = x + 0.5 * sm[rb + s][lane];
-          sm[rb][lane] = x;
+          double *xm = row(rb);
+          const double *xl = row(rb - s), *xr = row(rb + s);
+#pragma unroll
+          for (int u = 0; u < CPL; ++u) {
+            const int c = lane + 32 * u;
+            double x = xm[c];
+            if (i - s >= 1) x = x + 0.5 * xl[c];
+            if (i + s <= n) x = x + 0.5 * xr[c];
+            xm[c] = x;
+          }
         }
         __syncthreads();
       }
-#pragma unroll 4
-      for (int rb = 1 + warp; rb <= rhi; rb += kWarps)
-        if (active) g[(int64_t)(i0 + rb) * PS] = sm[rb][lane];
+      for (int rb = 1 + warp; rb <= rhi; rb += kWarps) {
+        const double *xm = row(rb);
+        double *gout = rowbase + (int64_t)(i0 + rb - 1) * PS;
+#pragma unroll
+        for (int u = 0; u < CPL; ++u) {
+          const int c = lane + 32 * u;
+          if (c < wc) gout[c] = xm[c];
+        }
+      }
     }
     __syncthreads();
   });
@@ -254,44 +340,64 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
 
 // ----------------------------------------------------------------------- REG
 // One thread per column (o, r); the whole pole of n = 2^L - 1 points lives in
-// registers; the level structure is resolved at compile time.
+// registers; the level structure is resolved at compile time.  Each thread
+// handles CPT columns (c, c + 256, ...) so that ~16 independent loads are in
+// flight per thread.  A tile = kThreads * CPT columns.
+template <int L>
+struct RegCfg {
+  static constexpr int n = (1 << L) - 1;
+  static constexpr int CPT = (16 / n) > 0 ? (16 / n) : 1;
+};
+
 template <int L, bool INV>
 __global__ void __launch_bounds__(kThreads) k_reg(const __grid_constant__ Src src) {
-  constexpr int n = (1 << L) - 1;
+  constexpr int n = RegCfg<L>::n;
+  constexpr int CPT = RegCfg<L>::CPT;
   for_each_tile(src, [&](const Task &T, int64_t q) {
-    const int64_t gcol = q * kThreads + threadIdx.x;
-    if (gcol >= T.O * T.S) return;
-    const int64_t o = gcol / T.S;
-    const int64_t r = gcol - o * T.S;
-    double *__restrict__ p = T.grid + T.base + o * T.OS + r;
+    const int64_t ncol = T.O * T.S;
     const int64_t PS = T.PS;
-    double v[n];
+    double *p[CPT];
+    double v[CPT][n];
 #pragma unroll
-    for (int i = 0; i < n; ++i) v[i] = p[i * PS];
-    if (!INV) {
-      // v keeps the values entering the sweep; results go straight to memory
+    for (int c = 0; c < CPT; ++c) {
+      const int64_t gcol = (q * CPT + c) * kThreads + threadIdx.x;
+      p[c] = nullptr;
+      if (gcol < ncol) {
+        const int64_t o = gcol / T.S;
+        const int64_t r = gcol - o * T.S;
+        p[c] = T.grid + T.base + o * T.OS + r;
 #pragma unroll
-      for (int i = 1; i <= n; ++i) {
-        const int s = i & -i;
-        double x = v[i - 1];
-        if (i - s >= 1) x = x - 0.5 * v[i - s - 1];
-        if (i + s <= n) x = x - 0.5 * v[i + s - 1];
-        p[(i - 1) * PS] = x;
+        for (int i = 0; i < n; ++i) v[c][i] = p[c][i * PS];
       }
-    } else {
+    }
 #pragma unroll
-      for (int lam = 2; lam <= L; ++lam) {
-        const int s = 1 << (L - lam);
+    for (int c = 0; c < CPT; ++c) {
+      if (!p[c]) continue;
+      if (!INV) {
+        // v keeps the values entering the sweep; results go straight to memory
 #pragma unroll
-        for (int i = s; i <= n; i += 2 * s) {
-          double x = v[i - 1];
-          if (i - s >= 1) x = x + 0.5 * v[i - s - 1];
-          if (i + s <= n) x = x + 0.5 * v[i + s - 1];
-          v[i - 1] = x;
+        for (int i = 1; i <= n; ++i) {
+          const int s = i & -i;
+          double x = v[c][i - 1];
+          if (i - s >= 1) x = x - 0.5 * v[c][i - s - 1];
+          if (i + s <= n) x = x - 0.5 * v[c][i + s - 1];
+          p[c][(i - 1) * PS] = x;
         }
-      }
+      } else {
 #pragma unroll
-      for (int i = 0; i < n; ++i) p[i * PS] = v[i];
+        for (int lam = 2; lam <= L; ++lam) {
+          const int s = 1 << (L - lam);
+#pragma unroll
+          for (int i = s; i <= n; i += 2 * s) {
+            double x = v[c][i - 1];
+            if (i - s >= 1) x = x + 0.5 * v[c][i - s - 1];
+            if (i + s <= n) x = x + 0.5 * v[c][i + s - 1];
+            v[c][i - 1] = x;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < n; ++i) p[c][i * PS] = v[c][i];
+      }
     }
   });
 }
@@ -299,17 +405,22 @@ __global__ void __launch_bounds__(kThreads) k_reg(const __grid_constant__ Src sr
 // ------------------------------------------------------------ host launchers
 using KernelFn = void (*)(Src);
 
-static KernelFn kernel_for(int kind, int l, bool inv) {
+static KernelFn kernel_for(int kind, int l, int w, bool inv) {
   switch (kind) {
     case KIND_FLAT_SLABS: return inv ? k_flat_slabs<true> : k_flat_slabs<false>;
     case KIND_FLAT_BLOCKS: return inv ? k_flat_blocks<true> : k_flat_blocks<false>;
-    case KIND_STRIDED: return inv ? k_strided<true> : k_strided<false>;
+    case KIND_STRIDED:
+      switch (w) {
+        case 32: return inv ? k_strided<true, 32> : k_strided<false, 32>;
+        case 64: return inv ? k_strided<true, 64> : k_strided<false, 64>;
+        case 128: return inv ? k_strided<true, 128> : k_strided<false, 128>;
+        default: return nullptr;
+      }
     case KIND_REG:
       switch (l) {
         case 2: return inv ? k_reg<2, true> : k_reg<2, false>;
         case 3: return inv ? k_reg<3, true> : k_reg<3, false>;
         case 4: return inv ? k_reg<4, true> : k_reg<4, false>;
-        case 5: return inv ? k_reg<5, true> : k_reg<5, false>;
         default: return nullptr;
       }
     default: return nullptr;
@@ -320,9 +431,9 @@ static KernelFn kernel_for(int kind, int l, bool inv) {
 size_t task_smem(const Task &t) {
   const int64_t n = (int64_t(1) << t.l) - 1;
   switch (t.kind) {
-    case KIND_FLAT_SLABS: return size_t(t.R) * size_t(n * t.S) * 8;
-    case KIND_FLAT_BLOCKS: return size_t((int64_t(1) << t.t) + 1) * size_t(t.S) * 8;
-    case KIND_STRIDED: return size_t((int64_t(1) << t.t) + 1) * kStridedW * 8;
+    case KIND_FLAT_SLABS: return (size_t(t.R) * size_t(n * t.S) + 2) * 8;            // +1 phase shift
+    case KIND_FLAT_BLOCKS: return (size_t((int64_t(1) << t.t) + 1) * size_t(t.S) + 2) * 8;
+    case KIND_STRIDED: return size_t((int64_t(1) << t.t) + 1) * size_t(t.W + 2) * 8;
     default: return 0;
   }
 }
@@ -347,7 +458,7 @@ static int resident_ctas(KernelFn fn, size_t smem) {
 
 // Launch one task (single grid).  Returns the CUDA error of the launch.
 cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
-  KernelFn fn = kernel_for(task.kind, task.l, inv);
+  KernelFn fn = kernel_for(task.kind, task.l, task.W, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = nullptr;
@@ -368,9 +479,9 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
 
 // Launch a group of tasks of one kernel instance from a device task table;
 // smem = max task_smem over the group.
-cudaError_t launch_table(int kind, int l, bool inv, const Task *d_tasks, const int64_t *d_prefix,
+cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
                          int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream) {
-  KernelFn fn = kernel_for(kind, l, inv);
+  KernelFn fn = kernel_for(kind, l, w, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = d_tasks;

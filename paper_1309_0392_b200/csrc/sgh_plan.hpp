@@ -13,7 +13,7 @@ namespace sgh {
 
 // launchers (sgh_kernels.cu)
 cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream);
-cudaError_t launch_table(int kind, int l, bool inv, const Task *d_tasks, const int64_t *d_prefix,
+cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
                          int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream);
 size_t task_smem(const Task &t);
 
