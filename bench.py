@@ -184,6 +184,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--per-axis", action="store_true",
+                    help="one HBM round trip per axis (disable the multi-axis FUSED kernel)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -253,7 +255,8 @@ def sgh_arm(args, rank, world, local_rank):
     else:
         batch = sgh.GridBatch(my_members, device=dev, grid_ids=my_ids)
         batch.fill_uniform(si.SEED)
-        step = batch.hierarchize
+        fuse = not args.per_axis
+        step = lambda: batch.hierarchize(fuse=fuse)  # noqa: E731
         my_points = batch.total_points
         deff_pts = sum(d_eff(l) * si.num_points(l) for l in my_members)
 

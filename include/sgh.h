@@ -67,6 +67,8 @@ typedef enum {
 /* flags for the _ex / batched calls */
 #define SGH_FLAG_NONE 0u
 #define SGH_FLAG_DEHIERARCHIZE 1u /* run the inverse transform instead  */
+#define SGH_FLAG_PER_AXIS 2u      /* one HBM round trip per axis: disable the multi-axis
+                                     FUSED kernel (a4); results are bitwise identical */
 
 /* ------------------------------------------------------------ geometry */
 

@@ -33,6 +33,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libsgh.so")
 
 FLAG_DEHIERARCHIZE = 1
+FLAG_PER_AXIS = 2
 STATUS = {0: "SGH_OK", 1: "SGH_ERR_INVALID_ARGUMENT", 2: "SGH_ERR_CAPACITY", 3: "SGH_ERR_CUDA",
           4: "SGH_ERR_NCCL", 5: "SGH_ERR_WORKSPACE"}
 
@@ -136,9 +137,16 @@ def num_points(levels: Sequence[int]) -> int:
     return int(lib.sgh_num_points(a, d))
 
 
+def _flags(inverse: bool, fuse: bool = True) -> int:
+    return (FLAG_DEHIERARCHIZE if inverse else 0) | (0 if fuse else FLAG_PER_AXIS)
+
+
 def transform(grid: torch.Tensor, levels: Sequence[int], *, inverse: bool = False, axis_order=None,
-              axis_mask: int = 0, stream=None) -> torch.Tensor:
-    """In-place (de)hierarchization of one grid; returns ``grid``."""
+              axis_mask: int = 0, fuse: bool = True, stream=None) -> torch.Tensor:
+    """In-place (de)hierarchization of one grid; returns ``grid``.
+
+    fuse=False forces one HBM round trip per axis (no multi-axis FUSED tiles);
+    the result is bitwise identical either way."""
     a, d = _levels_arr(levels)
     order = None
     if axis_order is not None:
@@ -146,7 +154,7 @@ def transform(grid: torch.Tensor, levels: Sequence[int], *, inverse: bool = Fals
     ptr = _grid_ptr(grid, levels)
     with torch.cuda.device(grid.device):
         _check(lib.sgh_transform_ex(ptr, a, d, order, ctypes.c_uint32(axis_mask),
-                                    ctypes.c_uint32(FLAG_DEHIERARCHIZE if inverse else 0), _stream(stream)))
+                                    ctypes.c_uint32(_flags(inverse, fuse)), _stream(stream)))
     return grid
 
 
@@ -226,12 +234,12 @@ def _flat_levels(levels_list, d):
     return (ctypes.c_int32 * len(flat))(*flat)
 
 
-def batched_workspace_bytes(levels_list, inverse: bool = False) -> int:
+def batched_workspace_bytes(levels_list, inverse: bool = False, fuse: bool = True) -> int:
     if not levels_list:
         return 0
     d = len(levels_list[0])
     return int(lib.sgh_batched_workspace_bytes(_flat_levels(levels_list, d), d, len(levels_list),
-                                               FLAG_DEHIERARCHIZE if inverse else 0))
+                                               _flags(inverse, fuse)))
 
 
 class GridBatch:
@@ -265,8 +273,8 @@ class GridBatch:
         self._sizes = (ctypes.c_int64 * max(G, 1))(*self.sizes)
         self._ids = (ctypes.c_uint64 * max(G, 1))(*self.grid_ids)
         self._flat = _flat_levels(self.levels, self.d) if G else None
-        ws = max(batched_workspace_bytes(self.levels, False), batched_workspace_bytes(self.levels, True),
-                 self._util_ws_bytes(), 256)
+        ws = max([batched_workspace_bytes(self.levels, inv, fz) for inv in (False, True) for fz in (False, True)]
+                 + [self._util_ws_bytes(), 256])
         self.workspace = torch.empty((ws + 7) // 8, dtype=torch.float64, device=self.device)
 
     def _util_ws_bytes(self):
@@ -279,20 +287,20 @@ class GridBatch:
     def _ws(self):
         return ctypes.c_void_p(self.workspace.data_ptr()), self.workspace.numel() * 8
 
-    def transform(self, inverse: bool = False, stream=None):
+    def transform(self, inverse: bool = False, stream=None, fuse: bool = True):
         if not self.levels:
             return self
         ws, wsb = self._ws()
         with torch.cuda.device(self.device):
             _check(lib.sgh_hierarchize_batched(self._ptrs, self._flat, self.d, len(self.levels),
-                                               FLAG_DEHIERARCHIZE if inverse else 0, ws, wsb, _stream(stream)))
+                                               _flags(inverse, fuse), ws, wsb, _stream(stream)))
         return self
 
-    def hierarchize(self, stream=None):
-        return self.transform(False, stream)
+    def hierarchize(self, stream=None, fuse: bool = True):
+        return self.transform(False, stream, fuse)
 
-    def dehierarchize(self, stream=None):
-        return self.transform(True, stream)
+    def dehierarchize(self, stream=None, fuse: bool = True):
+        return self.transform(True, stream, fuse)
 
     def fill_uniform(self, seed: int, stream=None):
         if not self.levels:

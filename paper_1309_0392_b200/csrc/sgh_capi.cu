@@ -144,6 +144,88 @@ void plan_axis(double *grid, const int32_t *levels, int d, int k, std::vector<Ta
   plan_view(grid, O, n * S, S, S, 0, levels[k], phases);
 }
 
+// Whole-pole multi-axis group [a, b).  Returns false if the
+// group's tile does not fit the FUSED budget.
+static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, int b, Task &t) {
+  int64_t Sa = 1, P = 1, O = 1;
+  int busy = 0;
+  for (int k = 0; k < a; ++k) Sa *= (int64_t(1) << levels[k]) - 1;
+  for (int k = a; k < b; ++k) {
+    P *= (int64_t(1) << levels[k]) - 1;
+    busy += levels[k] > 1;
+  }
+  for (int k = b; k < d; ++k) O *= (int64_t(1) << levels[k]) - 1;
+  if (busy < 2 || b - a > 16) return false;
+  std::memset(&t, 0, sizeof t);
+  t.grid = grid;
+  t.kind = KIND_FUSED;
+  t.m = b - a;
+  t.P = (int32_t)std::min<int64_t>(P, INT32_MAX);
+  int64_t R = 1;
+  for (int k = a; k < b; ++k) {
+    t.gl[k - a] = (int8_t)levels[k];
+    t.gR[k - a] = (int32_t)R;
+    t.fR[k - a] = make_fdiv((uint32_t)R);
+    R *= (int64_t(1) << levels[k]) - 1;
+  }
+  t.base = 0;
+  t.S = Sa;
+  t.O = O;
+  t.l = levels[a];
+  if (Sa == 1) {
+    if (P > kFusedT) return false;
+    t.W = 1;
+    t.R = (int32_t)(kFusedT / P);
+    t.OS = P;
+    t.tiles = (O + t.R - 1) / t.R;
+    return true;
+  }
+  const int W = Sa >= 24 ? 32 : (Sa >= 12 ? 16 : 8);
+  if (P * (W + 2) > kFusedT + kFusedT / 16) return false;
+  t.W = W;
+  t.R = 1;
+  t.OS = P * Sa;
+  t.ncb = (Sa + W - 1) / W;
+  t.tiles = O * t.ncb;
+  return true;
+}
+
+// Passes of a whole grid (hierarchization order inside each pass).  With
+// `fuse`, a DP over consecutive axis groups picks the fewest HBM round trips:
+// a group is either one axis (per-axis kernels) or a run of axes whose whole
+// poles fit one FUSED tile.  The axis order stays 1..d, so results
+// are bitwise equal to the per-axis path.
+void plan_grid(double *grid, const int32_t *levels, int d, bool fuse, std::vector<std::vector<Task>> &passes) {
+  passes.clear();
+  std::vector<int> cost(d + 1, 1 << 20), from(d + 1, -1);
+  cost[0] = 0;
+  for (int i = 0; i < d; ++i) {
+    if (cost[i] >= (1 << 20)) continue;
+    const int c1 = cost[i] + (levels[i] > 1 ? 1 : 0);     // one axis
+    if (c1 < cost[i + 1]) { cost[i + 1] = c1; from[i + 1] = i; }
+    if (!fuse) continue;
+    Task t;
+    for (int j = i + 2; j <= d; ++j) {
+      if (!plan_fused_group(grid, levels, d, i, j, t)) continue;
+      if (cost[i] + 1 < cost[j] || (cost[i] + 1 == cost[j] && from[j] < i)) { cost[j] = cost[i] + 1; from[j] = i; }
+    }
+  }
+  std::vector<std::pair<int, int>> groups;
+  for (int j = d; j > 0; j = from[j]) groups.push_back({from[j], j});
+  std::reverse(groups.begin(), groups.end());
+  for (auto &g : groups) {
+    std::vector<Task> phases;
+    if (g.second - g.first == 1) {
+      plan_axis(grid, levels, d, g.first, phases);
+    } else {
+      Task t;
+      plan_fused_group(grid, levels, d, g.first, g.second, t);
+      phases.push_back(t);
+    }
+    if (!phases.empty()) passes.push_back(std::move(phases));
+  }
+}
+
 // ------------------------------------------------- pinned staging ring
 // Task tables are staged in pinned host memory and copied asynchronously into
 // the caller's workspace.  A slot is reused only after its copy has completed.
@@ -225,10 +307,25 @@ static sgh_status transform_single(double *grid, const int32_t *levels, int32_t 
   } else {
     for (int k = 0; k < d; ++k) order[k] = k;
   }
+  const bool all_axes = (axis_mask == 0) || ((axis_mask & ((d >= 32) ? 0xffffffffu : ((1u << d) - 1))) ==
+                                             ((d >= 32) ? 0xffffffffu : ((1u << d) - 1)));
   if (axis_mask == 0) axis_mask = 0xffffffffu;
-  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS)) return invalid("unknown flags");
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!axis_order && all_axes) {
+    std::vector<std::vector<Task>> passes;
+    plan_grid(grid, levels, d, (flags & SGH_FLAG_PER_AXIS) == 0, passes);
+    for (auto &phases : passes) {
+      if (inv) std::reverse(phases.begin(), phases.end());   // coarse lattice first (H2)
+      for (const Task &t : phases) {
+        cudaError_t e = launch_single(t, inv, s);
+        if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+        count_launch();
+      }
+    }
+    return SGH_OK;
+  }
   std::vector<Task> phases;
   for (int kk = 0; kk < d; ++kk) {
     const int k = order[kk];
@@ -266,13 +363,19 @@ struct BatchedPlan {
 };
 
 static void build_batched_plan(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv,
-                               BatchedPlan &P) {
+                               BatchedPlan &P, bool fuse = true) {
+  std::vector<std::vector<std::vector<Task>>> all(num_grids);
+  size_t rounds = 0;
+  for (int64_t g = 0; g < num_grids; ++g) {
+    plan_grid(grids ? grids[g] : nullptr, levels + g * d, d, fuse, all[g]);
+    rounds = std::max(rounds, all[g].size());
+  }
   std::vector<std::vector<Task>> per(num_grids);
-  for (int k = 0; k < d; ++k) {
+  for (size_t k = 0; k < rounds; ++k) {
     size_t maxp = 0;
     for (int64_t g = 0; g < num_grids; ++g) {
       per[g].clear();
-      plan_axis(grids ? grids[g] : nullptr, levels + g * d, d, k, per[g]);
+      if (k < all[g].size()) per[g] = all[g][k];
       if (inv) std::reverse(per[g].begin(), per[g].end());
       maxp = std::max(maxp, per[g].size());
     }
@@ -282,7 +385,8 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
       for (int64_t g = 0; g < num_grids; ++g)
         if (j < per[g].size()) {
           const Task &t = per[g][j];
-          groups[{t.kind, t.kind == KIND_REG ? t.l : 0, t.kind == KIND_STRIDED ? t.W : 0}].push_back(&t);
+          groups[{t.kind, t.kind == KIND_REG ? t.l : 0, (t.kind == KIND_STRIDED || t.kind == KIND_FUSED) ? t.W : 0}]
+              .push_back(&t);
         }
       for (auto &kv : groups) {
         Segment sg;
@@ -310,9 +414,10 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
   }
 }
 
-size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv) {
+size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv,
+                           bool fuse) {
   BatchedPlan P;
-  build_batched_plan(grids, levels, d, num_grids, inv, P);
+  build_batched_plan(grids, levels, d, num_grids, inv, P, fuse);
   return P.segs.empty() ? 0 : P.table_bytes();
 }
 
@@ -332,13 +437,13 @@ static sgh_status validate_batch(double *const *grids, const int32_t *levels, in
 
 sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
                               uint32_t flags, void *workspace, size_t ws_bytes, cudaStream_t s) {
-  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS)) return invalid("unknown flags");
   sgh_status st = validate_batch(grids, levels, d, num_grids, true);
   if (st != SGH_OK) return st;
   if (num_grids == 0) return SGH_OK;
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   BatchedPlan P;
-  build_batched_plan(grids, levels, d, num_grids, inv, P);
+  build_batched_plan(grids, levels, d, num_grids, inv, P, (flags & SGH_FLAG_PER_AXIS) == 0);
   if (P.segs.empty()) return SGH_OK;
   const size_t bytes = P.table_bytes();
   if (!workspace || ws_bytes < bytes || (reinterpret_cast<uintptr_t>(workspace) & 15)) {
@@ -394,7 +499,8 @@ sgh_status sgh_transform_ex(double *grid, const int32_t *levels, int32_t d, cons
 size_t sgh_batched_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
   if (validate_batch(nullptr, levels, d, num_grids, false) != SGH_OK || num_grids == 0) return 0;
   BatchedPlan P;
-  build_batched_plan(nullptr, levels, d, num_grids, (flags & SGH_FLAG_DEHIERARCHIZE) != 0, P);
+  build_batched_plan(nullptr, levels, d, num_grids, (flags & SGH_FLAG_DEHIERARCHIZE) != 0, P,
+                     (flags & SGH_FLAG_PER_AXIS) == 0);
   return P.table_bytes();
 }
 

@@ -29,13 +29,15 @@ constexpr int kFlatCap = kFlatT + kFlatMaxS + 2;
 constexpr int kStridedWMax = 128;  // STRIDED tile width W in {32, 64, 128} columns
 constexpr int kStridedTileDoubles = 4480;  // STRIDED tile budget: (2^t + 1) * (W + 2) doubles (35 KB)
 constexpr int kRegMaxL = 4;        // REG kernel: poles of up to 15 points in registers
+constexpr int kFusedT = 8192;      // FUSED tile budget (doubles, excluding row padding)
 
 enum Kind : int32_t {
   KIND_FLAT_SLABS = 0,   // R whole slabs (o) per tile; needs PS==S, OS==n*S, n*S <= kFlatT
   KIND_FLAT_BLOCKS = 1,  // one 2^t-row block (+halo) of one slab per tile; PS==S, OS==n*S
   KIND_STRIDED = 2,      // (o, block, 32-column group) tiles, any strides
   KIND_REG = 3,          // thread per column, whole pole in registers, l <= kRegMaxL
-  KIND_COUNT = 4
+  KIND_FUSED = 4,        // whole poles of a run of consecutive axes in one tile
+  KIND_COUNT = 5
 };
 
 // magic-number division for 32-bit numerators < 2^31 (divisor >= 1)
@@ -72,6 +74,17 @@ struct Task {
   int32_t pad_;
   FDiv fS;            // division by S   (FLAT kinds, S < 2^31)
   FDiv fNS;           // division by n*S (FLAT_SLABS)
+  // FUSED: axes a..a+m-1 of the grid transformed together, whole poles.
+  //   W == 1: the group starts at a unit-stride axis; a unit = P contiguous
+  //           doubles at base + u*P (O units), a tile = R units.
+  //   W  > 1: a unit = (o, column group): P rows of W columns at
+  //           base + o*OS + row*S + cb*W + c, ncb column groups.
+  // Inside a unit, axis j of the group has row stride gR[j] = prod_{i<j} n_i.
+  int32_t m;          // axes in the group
+  int32_t P;          // rows per unit = prod of the group's n_k
+  int8_t gl[16];      // the group's levels
+  int32_t gR[16];     // row strides
+  FDiv fR[16];        // division by gR[j]
 };
 
 static_assert(sizeof(Task) % 8 == 0, "Task must stay 8-byte aligned");

@@ -236,7 +236,7 @@ __device__ __forceinline__ void strided_load_rows(double *sm, const double *rowb
                                                   int i0, int rb_lo, int rb_hi, int wc) {
   constexpr int RS = W + 2;
   constexpr int P = W / 2;          // 16-byte slots per row
-  constexpr int LOGP = (P == 16) ? 4 : (P == 32) ? 5 : 6;
+  constexpr int LOGP = (P == 4) ? 2 : (P == 8) ? 3 : (P == 16) ? 4 : (P == 32) ? 5 : 6;
   const int psodd = (int)(PS & 1);
   const int nslots = (rb_hi - rb_lo + 1) * P;
 #pragma unroll 4
@@ -338,6 +338,124 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
   });
 }
 
+// ---------------------------------------------------------------------- FUSED
+// Several consecutive axes a..a+m-1 in ONE round trip: the
+// tile holds whole poles of every axis of the group, so Alg. 1
+// runs axis by axis, level by level, in place in SMEM -- exactly the oracle's
+// per-point operation order (axes ascending, levels finest first, left then
+// right), hence bitwise parity.  Dehierarchization: axes ascending, levels
+// coarse to fine (reading R9).
+//   W == 1: the group starts at a unit-stride axis; the tile is R units of P
+//           contiguous doubles (one contiguous global range).
+//   W  > 1: the tile is P rows of W adjacent columns (row stride S); rows are
+//           staged with 16-byte cp.async pairs as in STRIDED.
+__device__ __forceinline__ FDiv device_fdiv(uint32_t d) {
+  FDiv f;
+  f.d = d;
+  uint32_t s = 0;
+  while (s < 32 && (1ull << s) < d) ++s;
+  f.s = s;
+  f.m = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+  return f;
+}
+
+template <bool INV, int W>
+__global__ void __launch_bounds__(kThreads) k_fused(const __grid_constant__ Src src) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr int RS = (W == 1) ? 1 : W + 2;
+  constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : 5;
+  for_each_tile(src, [&](const Task &T, int64_t q) {
+    const int P = T.P;
+    double *gbase;
+    double *sm;
+    int units = 1, wc = 1, par0 = 0, sodd = 0;
+    int64_t S = 1;
+    if (W == 1) {
+      const int64_t u0 = q * T.R;
+      units = (int)min((int64_t)T.R, T.O - u0);
+      gbase = T.grid + T.base + u0 * P;
+      sm = smem + phase8(gbase);
+      copy_range_async(sm, gbase, units * P);
+    } else {
+      const int64_t cb = q % T.ncb;
+      const int64_t o = q / T.ncb;
+      const int64_t c0 = cb * W;
+      S = T.S;
+      wc = (int)min((int64_t)W, S - c0);
+      gbase = T.grid + T.base + o * T.OS + c0;      // (row r, col c) at gbase[r*S + c]
+      par0 = phase8(gbase);
+      sodd = (int)(S & 1);
+      sm = smem;
+      strided_load_rows<W == 1 ? 32 : W>(sm, gbase, S, par0, 1, 0, P - 1, wc);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    auto at = [&](int row, int c) -> double & {
+      if (W == 1) return sm[row];
+      return sm[row * RS + ((par0 + row * sodd) & 1) + c];
+    };
+    const int rows_total = units * P;
+    for (int j = 0; j < T.m; ++j) {                   // axes ascending
+      const int l = T.gl[j];
+      if (l <= 1) continue;
+      const int n = (1 << l) - 1;
+      const int R = T.gR[j];
+      const FDiv fR = T.fR[j];
+      const int Ok = rows_total / (n * R);
+      // unit-stride axis of a contiguous tile: lanes run across poles (odd
+      // stride n -> conflict-free SMEM banks) instead of along one pole
+      const bool across = (W == 1) && (R == 1);
+      const FDiv fO = device_fdiv((uint32_t)Ok);
+      for (int st = 0; st < l - 1; ++st) {
+        const int lam = INV ? 2 + st : l - st;        // hier: finest first; dehier: coarse first
+        const int s = 1 << (l - lam);
+        const int lh = lam - 1;
+        const int cnt = (Ok << lh) * R * W;
+        for (int idx = threadIdx.x; idx < cnt; idx += kThreads) {
+          int c = 0, rk, jx, oo;
+          if (across) {
+            jx = (int)fdiv((uint32_t)idx, fO);
+            oo = idx - jx * Ok;
+            rk = 0;
+          } else {
+            c = idx & (W - 1);
+            const int rest = idx >> LOGW;
+            const int q2 = (int)fdiv((uint32_t)rest, fR);
+            rk = rest - q2 * R;
+            jx = q2 & ((1 << lh) - 1);
+            oo = q2 >> lh;
+          }
+          if (W > 1 && c >= wc) continue;
+          const int i = s * (2 * jx + 1);
+          const int row = (oo * n + (i - 1)) * R + rk;
+          double x = at(row, c);
+          if (!INV) {
+            if (i - s >= 1) x = x - 0.5 * at(row - s * R, c);   // left predecessor
+            if (i + s <= n) x = x - 0.5 * at(row + s * R, c);   // right predecessor
+          } else {
+            if (i - s >= 1) x = x + 0.5 * at(row - s * R, c);
+            if (i + s <= n) x = x + 0.5 * at(row + s * R, c);
+          }
+          at(row, c) = x;
+        }
+        __syncthreads();
+      }
+    }
+    if (W == 1) {
+      const int len = rows_total;
+      for (int e = threadIdx.x; e < len; e += kThreads) gbase[e] = sm[e];
+    } else {
+      const int cnt = P * W;
+      for (int idx = threadIdx.x; idx < cnt; idx += kThreads) {
+        const int c = idx & (W - 1);
+        const int row = idx >> LOGW;
+        if (c < wc) gbase[(int64_t)row * S + c] = at(row, c);
+      }
+    }
+    __syncthreads();
+  });
+}
+
 // ----------------------------------------------------------------------- REG
 // One thread per column (o, r); the whole pole of n = 2^L - 1 points lives in
 // registers; the level structure is resolved at compile time.  Each thread
@@ -416,6 +534,14 @@ static KernelFn kernel_for(int kind, int l, int w, bool inv) {
         case 128: return inv ? k_strided<true, 128> : k_strided<false, 128>;
         default: return nullptr;
       }
+    case KIND_FUSED:
+      switch (w) {
+        case 1: return inv ? k_fused<true, 1> : k_fused<false, 1>;
+        case 8: return inv ? k_fused<true, 8> : k_fused<false, 8>;
+        case 16: return inv ? k_fused<true, 16> : k_fused<false, 16>;
+        case 32: return inv ? k_fused<true, 32> : k_fused<false, 32>;
+        default: return nullptr;
+      }
     case KIND_REG:
       switch (l) {
         case 2: return inv ? k_reg<2, true> : k_reg<2, false>;
@@ -434,6 +560,8 @@ size_t task_smem(const Task &t) {
     case KIND_FLAT_SLABS: return (size_t(t.R) * size_t(n * t.S) + 2) * 8;            // +1 phase shift
     case KIND_FLAT_BLOCKS: return (size_t((int64_t(1) << t.t) + 1) * size_t(t.S) + 2) * 8;
     case KIND_STRIDED: return size_t((int64_t(1) << t.t) + 1) * size_t(t.W + 2) * 8;
+    case KIND_FUSED:
+      return t.W == 1 ? (size_t(t.R) * size_t(t.P) + 2) * 8 : size_t(t.P) * size_t(t.W + 2) * 8;
     default: return 0;
   }
 }

@@ -26,6 +26,7 @@ void prof_end(ProfToken tok, int kind, int l, bool inv, double bytes, cudaStream
 
 // points a task transforms (= writes): 16 B each is its algorithmic traffic
 inline double task_points(const Task &t) {
+  if (t.kind == KIND_FUSED) return double(t.O) * double(t.P) * double(t.S);   // every point, once
   const int64_t n = (int64_t(1) << t.l) - 1;
   const int64_t coarse = (t.t < t.l) ? (int64_t(1) << (t.l - t.t)) - 1 : 0;
   return double(t.O) * double(t.S) * double(n - coarse);
@@ -54,6 +55,8 @@ sgh_status staged_upload(void *dst, const void *src, size_t bytes, cudaStream_t 
 // batched driver: transform num_grids grids whose task tables go to `workspace`
 sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
                        uint32_t flags, void *workspace, size_t ws_bytes, cudaStream_t s);
-size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv);
+size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv,
+                           bool fuse = true);
+void plan_grid(double *grid, const int32_t *levels, int d, bool fuse, std::vector<std::vector<Task>> &passes);
 
 }  // namespace sgh

@@ -63,17 +63,21 @@ SHAPES = [
     (1, 1, 1), (3, 1, 4), (2, 5, 3), (4, 4, 4), (8, 2, 6), (1, 9, 2), (5, 5, 5), (2, 2, 10),
     (2, 2, 2, 2), (1, 3, 1, 3), (3, 4, 3, 5), (4, 1, 5, 2), (6, 6, 2, 2),
     (2, 3, 2, 3, 2), (1, 1, 1, 1, 9), (3, 2, 1, 2, 3, 2), (2, 2, 2, 2, 2, 2, 2), (2,) * 10,
+    # multi-axis FUSED groups: contiguous (W=1) and column (W=8/16/32) tiles
+    (1, 1, 5, 5), (5, 3, 3), (3, 4, 4, 2), (6, 6, 5, 5), (2, 3, 6, 6), (4, 2, 3, 7), (10, 4, 4, 4), (1, 3, 1, 4, 4),
+    (7, 6, 6), (3, 5, 6), (2, 2, 6, 5, 1),
 ]
 
 
 @pytest.mark.parametrize("levels", SHAPES, ids=str)
 @pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
-def test_shape_sweep_bitwise(sgh, levels, inverse):
+@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "per_axis"])
+def test_shape_sweep_bitwise(sgh, levels, inverse, fuse):
     N = si.num_points(levels)
     u = si.fill_uniform(N, grid_id=(N * 7 + len(levels)) % 9973)
     want = u.copy()
     (oracle.dehierarchize if inverse else oracle.hierarchize)(want, levels)
-    got = gpu_transform(sgh, u, levels, inverse=inverse)
+    got = gpu_transform(sgh, u, levels, inverse=inverse, fuse=fuse)
     assert_bitwise(got, want)
 
 
@@ -165,10 +169,10 @@ def test_round_trip_device(sgh, levels):
 
 
 # --------------------------------------------------------------- batched
-def _batch_check(sgh, members, ids, inverse=False):
+def _batch_check(sgh, members, ids, inverse=False, fuse=True):
     b = sgh.GridBatch(members, grid_ids=ids)
     b.fill_uniform(SD["seed"])
-    b.transform(inverse)
+    b.transform(inverse, fuse=fuse)
     torch.cuda.synchronize()
     for lv, gid, v in zip(members, ids, b.views):
         want = oracle.fill_uniform(si.num_points(lv), SD["seed"], gid)
@@ -177,19 +181,22 @@ def _batch_check(sgh, members, ids, inverse=False):
 
 
 @pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
-def test_batched_mixed_bitwise(sgh, inverse):
+@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "per_axis"])
+def test_batched_mixed_bitwise(sgh, inverse, fuse):
     rng = np.random.default_rng(11)
     members = [tuple(int(x) for x in rng.integers(1, 8, size=3)) for _ in range(60)]
     members += [(1, 1, 1), (13, 1, 2), (1, 12, 1), (2, 2, 11), (7, 7, 3)]
-    _batch_check(sgh, members, list(range(len(members))), inverse)
+    _batch_check(sgh, members, list(range(len(members))), inverse, fuse)
 
 
-def test_batched_c5_sample_vs_oracle(sgh):
+@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "per_axis"])
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_batched_c5_sample_vs_oracle(sgh, fuse, inverse):
     """A sample of the C5 set (every 97th member plus the extremes), each compared
     with the oracle element by element."""
     cs = si.combination_set(4, 22)
     ids = sorted(set(list(range(0, len(cs), 97)) + [0, 1, 834, 1329, 1330, 4254]))
-    _batch_check(sgh, [cs[i] for i in ids], ids)
+    _batch_check(sgh, [cs[i] for i in ids], ids, inverse, fuse)
 
 
 def test_batched_c5_full_golden(sgh):
