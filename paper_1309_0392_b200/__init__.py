@@ -203,7 +203,7 @@ class _LaunchRecord(ctypes.Structure):
                 ("reserved", ctypes.c_int32), ("bytes", ctypes.c_double), ("ms", ctypes.c_double)]
 
 
-KIND_NAMES = {0: "flat_slabs", 1: "flat_blocks", 2: "strided", 3: "reg"}
+KIND_NAMES = {0: "flat_slabs", 1: "flat_blocks", 2: "strided", 3: "reg", 4: "fused"}
 
 
 def profile_enable(on: bool = True):

@@ -347,8 +347,14 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
 // coarse to fine (reading R9).
 //   W == 1: the group starts at a unit-stride axis; the tile is R units of P
 //           contiguous doubles (one contiguous global range).
-//   W  > 1: the tile is P rows of W adjacent columns (row stride S); rows are
-//           staged with 16-byte cp.async pairs as in STRIDED.
+//   W  > 1: the tile is P rows of W adjacent columns (row stride S, always odd:
+//           a product of odd n_k).  SMEM rows have the ODD stride W+1 and start
+//           at the global 8-byte phase, so every row's 16-byte global pairs land
+//           16-byte aligned and element (row, c) sits at sm[row*(W+1) + c]: a
+//           pole has one uniform SMEM stride.
+// Per axis, when the tile holds enough poles, each thread owns whole poles and
+// runs the levels serially in SMEM (no division per point, no barrier inside
+// the axis); otherwise all threads sweep one level at a time (barrier per level).
 __device__ __forceinline__ FDiv device_fdiv(uint32_t d) {
   FDiv f;
   f.d = d;
@@ -359,17 +365,106 @@ __device__ __forceinline__ FDiv device_fdiv(uint32_t d) {
   return f;
 }
 
+// rows 0..P-1 of W columns (wc valid), global row r at g + r*S (S odd), SMEM row r at sb + r*(W+1).
+// Lane = (sub-row, 16-byte slot): one warp instruction covers 32/(W/2) rows.
+template <int W>
+__device__ __forceinline__ void fused_load_rows(double *sb, const double *g, int64_t S, int par0, int P, int wc) {
+  constexpr int RS = W + 1;
+  constexpr int NP = W / 2;                       // 16-byte slots per row
+  constexpr int RPI = 32 / NP;                    // rows per warp instruction
+  constexpr int STEP = RPI * (kThreads / 32);     // rows per CTA iteration
+  const int lane = threadIdx.x & 31;
+  const int k = lane % NP;
+  int r = (threadIdx.x >> 5) * RPI + lane / NP;
+  const double *gr = g + (int64_t)r * S;
+  double *sr = sb + r * RS;
+  const int64_t gstep = (int64_t)STEP * S;
+#pragma unroll 4
+  for (; r < P; r += STEP, gr += gstep, sr += STEP * RS) {
+    const int par = (par0 + r) & 1;
+    const int npairs = (wc - par) >> 1;
+    const int c = par + 2 * k;
+    if (k < npairs) cp_async16(sr + c, gr + c);
+    if (k == NP - 1 && par) cp_async8(sr, gr);
+    const int last = par + 2 * npairs;
+    if (k == NP - 2 && last < wc) cp_async8(sr + last, gr + last);
+  }
+}
+
+// Alg. 1 on one pole held in registers (l <= 5): load n points from SMEM,
+// transform with the level structure resolved at compile time, store back.
+// Hierarchization reads the values entering the axis (one-pass stencil,
+// bitwise equal to the in-place level order).
+template <int L, bool INV>
+__device__ __forceinline__ void pole_regs(double *p, int STR) {
+  constexpr int n = (1 << L) - 1;
+  double v[n];
+#pragma unroll
+  for (int i = 0; i < n; ++i) v[i] = p[i * STR];
+  if (!INV) {
+#pragma unroll
+    for (int i = 1; i <= n; ++i) {
+      const int s = i & -i;
+      double x = v[i - 1];
+      if (i - s >= 1) x = x - 0.5 * v[i - s - 1];
+      if (i + s <= n) x = x - 0.5 * v[i + s - 1];
+      p[(i - 1) * STR] = x;
+    }
+  } else {
+#pragma unroll
+    for (int lam = 2; lam <= L; ++lam) {
+      const int s = 1 << (L - lam);
+#pragma unroll
+      for (int i = s; i <= n; i += 2 * s) {
+        double x = v[i - 1];
+        if (i - s >= 1) x = x + 0.5 * v[i - s - 1];
+        if (i + s <= n) x = x + 0.5 * v[i + s - 1];
+        v[i - 1] = x;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < n; ++i) p[i * STR] = v[i];
+  }
+}
+
+// Alg. 1 on one pole of n = 2^l - 1 points at p[0], p[STR], ... (serial)
+template <bool INV>
+__device__ __forceinline__ void pole_serial(double *p, int l, int STR) {
+  const int n = (1 << l) - 1;
+  if (!INV) {
+    for (int s = 1; s < (1 << (l - 1)); s <<= 1) {        // levels l .. 2, finest first
+#pragma unroll 2
+      for (int i = s; i <= n; i += 2 * s) {
+        double x = p[(i - 1) * STR];
+        if (i - s >= 1) x = x - 0.5 * p[(i - s - 1) * STR];
+        if (i + s <= n) x = x - 0.5 * p[(i + s - 1) * STR];
+        p[(i - 1) * STR] = x;
+      }
+    }
+  } else {
+    for (int s = 1 << (l - 2); s >= 1; s >>= 1) {           // levels 2 .. l (reading R9)
+#pragma unroll 2
+      for (int i = s; i <= n; i += 2 * s) {
+        double x = p[(i - 1) * STR];
+        if (i - s >= 1) x = x + 0.5 * p[(i - s - 1) * STR];
+        if (i + s <= n) x = x + 0.5 * p[(i + s - 1) * STR];
+        p[(i - 1) * STR] = x;
+      }
+    }
+  }
+}
+
 template <bool INV, int W>
-__global__ void __launch_bounds__(kThreads) k_fused(const __grid_constant__ Src src) {
+__global__ void __launch_bounds__(kThreads, 3) k_fused(const __grid_constant__ Src src) {
   extern __shared__ __align__(16) double smem[];
-  constexpr int RS = (W == 1) ? 1 : W + 2;
+  constexpr int RS = (W == 1) ? 1 : W + 1;
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : 5;
   for_each_tile(src, [&](const Task &T, int64_t q) {
     const int P = T.P;
     double *gbase;
-    double *sm;
-    int units = 1, wc = 1, par0 = 0, sodd = 0;
+    int units = 1, wc = 1;
     int64_t S = 1;
+    double *sm;
     if (W == 1) {
       const int64_t u0 = q * T.R;
       units = (int)min((int64_t)T.R, T.O - u0);
@@ -383,17 +478,12 @@ __global__ void __launch_bounds__(kThreads) k_fused(const __grid_constant__ Src 
       S = T.S;
       wc = (int)min((int64_t)W, S - c0);
       gbase = T.grid + T.base + o * T.OS + c0;      // (row r, col c) at gbase[r*S + c]
-      par0 = phase8(gbase);
-      sodd = (int)(S & 1);
-      sm = smem;
-      strided_load_rows<W == 1 ? 32 : W>(sm, gbase, S, par0, 1, 0, P - 1, wc);
+      const int par0 = phase8(gbase);
+      sm = smem + par0;
+      fused_load_rows<(W == 1 ? 8 : W)>(sm, gbase, S, par0, P, wc);
     }
     cp_async_wait_all();
     __syncthreads();
-    auto at = [&](int row, int c) -> double & {
-      if (W == 1) return sm[row];
-      return sm[row * RS + ((par0 + row * sodd) & 1) + c];
-    };
     const int rows_total = units * P;
     for (int j = 0; j < T.m; ++j) {                   // axes ascending
       const int l = T.gl[j];
@@ -402,54 +492,80 @@ __global__ void __launch_bounds__(kThreads) k_fused(const __grid_constant__ Src 
       const int R = T.gR[j];
       const FDiv fR = T.fR[j];
       const int Ok = rows_total / (n * R);
-      // unit-stride axis of a contiguous tile: lanes run across poles (odd
-      // stride n -> conflict-free SMEM banks) instead of along one pole
-      const bool across = (W == 1) && (R == 1);
-      const FDiv fO = device_fdiv((uint32_t)Ok);
-      for (int st = 0; st < l - 1; ++st) {
-        const int lam = INV ? 2 + st : l - st;        // hier: finest first; dehier: coarse first
-        const int s = 1 << (l - lam);
-        const int lh = lam - 1;
-        const int cnt = (Ok << lh) * R * W;
-        for (int idx = threadIdx.x; idx < cnt; idx += kThreads) {
-          int c = 0, rk, jx, oo;
-          if (across) {
-            jx = (int)fdiv((uint32_t)idx, fO);
-            oo = idx - jx * Ok;
-            rk = 0;
-          } else {
-            c = idx & (W - 1);
-            const int rest = idx >> LOGW;
-            const int q2 = (int)fdiv((uint32_t)rest, fR);
-            rk = rest - q2 * R;
-            jx = q2 & ((1 << lh) - 1);
-            oo = q2 >> lh;
+      const int npoles = Ok * R * W;
+      if (npoles >= 2 * kThreads / 3) {
+        // pole owners: a pole = (oo, rk, c); lanes run over c (W > 1) or rk / oo
+        const int STR = R * RS;
+        auto run = [&](auto op) {
+          for (int p = threadIdx.x; p < npoles; p += kThreads) {
+            const int c = p & (W - 1);
+            const int rest = p >> LOGW;
+            const int oo = (int)fdiv((uint32_t)rest, fR);
+            const int rk = rest - oo * R;
+            op(sm + (oo * n * R + rk) * RS + c);
           }
-          if (W > 1 && c >= wc) continue;
-          const int i = s * (2 * jx + 1);
-          const int row = (oo * n + (i - 1)) * R + rk;
-          double x = at(row, c);
-          if (!INV) {
-            if (i - s >= 1) x = x - 0.5 * at(row - s * R, c);   // left predecessor
-            if (i + s <= n) x = x - 0.5 * at(row + s * R, c);   // right predecessor
-          } else {
-            if (i - s >= 1) x = x + 0.5 * at(row - s * R, c);
-            if (i + s <= n) x = x + 0.5 * at(row + s * R, c);
-          }
-          at(row, c) = x;
+        };
+        switch (l) {
+          case 2: run([&](double *pp) { pole_regs<2, INV>(pp, STR); }); break;
+          case 3: run([&](double *pp) { pole_regs<3, INV>(pp, STR); }); break;
+          case 4: run([&](double *pp) { pole_regs<4, INV>(pp, STR); }); break;
+          default: run([&](double *pp) { pole_serial<INV>(pp, l, STR); }); break;
         }
         __syncthreads();
+      } else {
+        // few long poles: all threads sweep one level at a time
+        const FDiv fO = device_fdiv((uint32_t)Ok);
+        const bool across = (W == 1) && (R == 1);
+        for (int st = 0; st < l - 1; ++st) {
+          const int lam = INV ? 2 + st : l - st;
+          const int s = 1 << (l - lam);
+          const int lh = lam - 1;
+          const int cnt = (Ok << lh) * R * W;
+          for (int idx = threadIdx.x; idx < cnt; idx += kThreads) {
+            int c = 0, rk, jx, oo;
+            if (across) {
+              jx = (int)fdiv((uint32_t)idx, fO);
+              oo = idx - jx * Ok;
+              rk = 0;
+            } else {
+              c = idx & (W - 1);
+              const int rest = idx >> LOGW;
+              const int q2 = (int)fdiv((uint32_t)rest, fR);
+              rk = rest - q2 * R;
+              jx = q2 & ((1 << lh) - 1);
+              oo = q2 >> lh;
+            }
+            const int i = s * (2 * jx + 1);
+            double *x0 = sm + ((oo * n + (i - 1)) * R + rk) * RS + c;
+            const int sd = s * R * RS;
+            double x = *x0;
+            if (!INV) {
+              if (i - s >= 1) x = x - 0.5 * x0[-sd];      // left predecessor
+              if (i + s <= n) x = x - 0.5 * x0[sd];       // right predecessor
+            } else {
+              if (i - s >= 1) x = x + 0.5 * x0[-sd];
+              if (i + s <= n) x = x + 0.5 * x0[sd];
+            }
+            *x0 = x;
+          }
+          __syncthreads();
+        }
       }
     }
     if (W == 1) {
-      const int len = rows_total;
-      for (int e = threadIdx.x; e < len; e += kThreads) gbase[e] = sm[e];
+      for (int e = threadIdx.x; e < rows_total; e += kThreads) gbase[e] = sm[e];
     } else {
-      const int cnt = P * W;
-      for (int idx = threadIdx.x; idx < cnt; idx += kThreads) {
-        const int c = idx & (W - 1);
-        const int row = idx >> LOGW;
-        if (c < wc) gbase[(int64_t)row * S + c] = at(row, c);
+      constexpr int RPI = 32 / W;                   // rows per warp instruction
+      constexpr int STEP = RPI * (kThreads / 32);
+      const int lane = threadIdx.x & 31;
+      const int c = lane % W;
+      int row = (threadIdx.x >> 5) * RPI + lane / W;
+      double *gr = gbase + (int64_t)row * S + c;
+      const double *sr = sm + row * RS + c;
+      const int64_t gstep = (int64_t)STEP * S;
+      if (c < wc) {
+#pragma unroll 4
+        for (; row < P; row += STEP, gr += gstep, sr += STEP * RS) *gr = *sr;
       }
     }
     __syncthreads();
@@ -561,7 +677,7 @@ size_t task_smem(const Task &t) {
     case KIND_FLAT_BLOCKS: return (size_t((int64_t(1) << t.t) + 1) * size_t(t.S) + 2) * 8;
     case KIND_STRIDED: return size_t((int64_t(1) << t.t) + 1) * size_t(t.W + 2) * 8;
     case KIND_FUSED:
-      return t.W == 1 ? (size_t(t.R) * size_t(t.P) + 2) * 8 : size_t(t.P) * size_t(t.W + 2) * 8;
+      return t.W == 1 ? (size_t(t.R) * size_t(t.P) + 2) * 8 : (size_t(t.P) * size_t(t.W + 1) + 2) * 8;
     default: return 0;
   }
 }
@@ -575,6 +691,10 @@ static int resident_ctas(KernelFn fn, size_t smem) {
   static int ncache = 0;
   for (int i = 0; i < ncache; ++i)
     if (cache[i].fn == fn && cache[i].dev == dev && cache[i].smem == smem) return cache[i].ctas;
+  if (smem > 48 * 1024) {
+    // opt in to large dynamic shared memory (FUSED tiles up to ~70 KB)
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  }
   int ctas = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, kThreads, smem) != cudaSuccess || ctas < 1) ctas = 1;
   int sms = 148;
