@@ -142,6 +142,16 @@ sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *
 sgh_status sgh_shard_rows(const int32_t *levels, int32_t d, int32_t nranks, int32_t rank,
                           int64_t *row_begin, int64_t *row_end);
 
+/* The whole exchange plan of the sharded path (host-only): for every rank q,
+ * its x_d rows [row_begin[q], row_begin[q]+rows[q]) and its column block
+ * [col_begin[q], col_begin[q]+cols[q]) of the flattened x_1..x_{d-1} index
+ * (col_begin[q] = floor(q C / P), C = prod_{k<d} n_k).  Forward re-shard: rank
+ * s sends rows(s) x cols(q) (row-major, packed) to rank q, which places it at
+ * row row_begin[s] of its n_d x cols(q) slab.  Output arrays hold nranks entries.
+ * Requires d >= 2. */
+sgh_status sgh_shard_layout(const int32_t *levels, int32_t d, int32_t nranks, int64_t *row_begin, int64_t *rows,
+                            int64_t *col_begin, int64_t *cols);
+
 /* Library-owned NCCL communicator created from a 128-byte ncclUniqueId that
  * the caller broadcasts (e.g. with torch.distributed).  *comm receives an
  * opaque handle.  Blocking (NCCL init is collective over all ranks). */

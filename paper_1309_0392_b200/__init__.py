@@ -25,7 +25,7 @@ __all__ = [
     "lib", "num_points", "hierarchize", "dehierarchize", "transform", "GridBatch",
     "hierarchize_batched", "dehierarchize_batched", "batched_workspace_bytes",
     "transform_batched_host", "batched_host_buffer_bytes",
-    "fill_uniform", "digest", "shard_rows", "ShardComm", "sharded_workspace_bytes",
+    "fill_uniform", "digest", "shard_rows", "shard_layout", "ShardComm", "sharded_workspace_bytes",
     "transform_sharded_loopback", "launch_count", "SGHError",
 ]
 
@@ -67,6 +67,7 @@ def _load():
         "sgh_batched_host_buffer_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32]),
         "sgh_transform_batched_host": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
         "sgh_shard_rows": (st, [i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, i64p, i64p]),
+        "sgh_shard_layout": (st, [i32p, ctypes.c_int32, ctypes.c_int32, i64p, i64p, i64p, i64p]),
         "sgh_comm_create": (st, [vpp, vp, ctypes.c_int32, ctypes.c_int32]),
         "sgh_comm_destroy": (None, [vp]),
         "sgh_comm_unique_id": (st, [vp]),
@@ -95,7 +96,7 @@ def _load():
 lib = _load()
 EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_transform_ex",
             "sgh_batched_workspace_bytes", "sgh_hierarchize_batched", "sgh_batched_host_buffer_bytes",
-            "sgh_transform_batched_host", "sgh_shard_rows", "sgh_comm_create", "sgh_comm_destroy",
+            "sgh_transform_batched_host", "sgh_shard_rows", "sgh_shard_layout", "sgh_comm_create", "sgh_comm_destroy",
             "sgh_comm_unique_id", "sgh_sharded_workspace_bytes", "sgh_hierarchize_sharded",
             "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
@@ -364,6 +365,15 @@ def shard_rows(levels, nranks: int, rank: int):
     b, e = ctypes.c_int64(), ctypes.c_int64()
     _check(lib.sgh_shard_rows(a, d, int(nranks), int(rank), ctypes.byref(b), ctypes.byref(e)))
     return int(b.value), int(e.value)
+
+
+def shard_layout(levels, nranks: int):
+    """The library's exchange plan for a grid sharded along x_d over nranks:
+    dict of lists row_begin, rows, col_begin, cols (host-only)."""
+    a, d = _levels_arr(levels)
+    arrs = [(ctypes.c_int64 * nranks)() for _ in range(4)]
+    _check(lib.sgh_shard_layout(a, d, int(nranks), *arrs))
+    return {k: [int(x) for x in v] for k, v in zip(("row_begin", "rows", "col_begin", "cols"), arrs)}
 
 
 def sharded_workspace_bytes(levels, nranks: int) -> int:

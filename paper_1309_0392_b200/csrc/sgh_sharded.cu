@@ -285,6 +285,24 @@ sgh_status sgh_shard_rows(const int32_t *levels, int32_t d, int32_t nranks, int3
   return shard_rows_impl(levels, d, nranks, rank, row_begin, row_end);
 }
 
+sgh_status sgh_shard_layout(const int32_t *levels, int32_t d, int32_t nranks, int64_t *row_begin, int64_t *rows,
+                            int64_t *col_begin, int64_t *cols) {
+  if (!row_begin || !rows || !col_begin || !cols) return invalid("NULL output pointer");
+  ShardGeom G;
+  sgh_status st = validate_levels(levels, d, nullptr);
+  if (st != SGH_OK) return st;
+  int64_t b, e;
+  if ((st = shard_rows_impl(levels, d, nranks, 0, &b, &e)) != SGH_OK) return st;
+  if ((st = make_geom(levels, d, nranks, 0, G)) != SGH_OK) return st;
+  for (int q = 0; q < nranks; ++q) {
+    row_begin[q] = G.row_begin[q];
+    rows[q] = G.rows[q];
+    col_begin[q] = G.col_begin[q];
+    cols[q] = G.cols[q];
+  }
+  return SGH_OK;
+}
+
 sgh_status sgh_comm_unique_id(void *out) {
   if (!out) return invalid("out is NULL");
   ncclUniqueId id;

@@ -1,0 +1,151 @@
+"""Multi-process (world size 2, gloo, CPU) tests of the N > 1 host logic.
+
+The GPU pool gives one GPU per call, so the NCCL paths cannot be run with two
+ranks here.  These tests run the SAME decomposition on CPU processes:
+
+* sharded grid: the library's own exchange plan
+  (``sgh_shard_layout``, host-only C++), row shards of x_d, local axes,
+  packing into column blocks, the point-to-point all-to-all (as the library's
+  grouped ncclSend/ncclRecv), the axis-d pass on the slab, the way back --
+  with the oracle as the per-rank compute.  The result must equal the
+  single-process oracle bitwise.
+* combination set (a6): LPT partition over ranks covers every grid exactly once
+  and is balanced; per-rank digests gathered over gloo match the oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _init(rank, world, port):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _exchange(sends, recv_shapes, rank, world):
+    """all-to-all over point-to-point messages (gloo has no alltoall)."""
+    recvs = [None] * world
+    reqs = []
+    for q in range(world):
+        if q == rank:
+            recvs[q] = sends[q].copy()
+            continue
+        buf = torch.empty(int(np.prod(recv_shapes[q])), dtype=torch.float64)
+        recvs[q] = buf
+        reqs.append(dist.irecv(buf, src=q))
+    for q in range(world):
+        if q != rank:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(sends[q]).ravel()), dst=q))
+    for r in reqs:
+        r.wait()
+    return [np.asarray(recvs[q]).reshape(recv_shapes[q]) for q in range(world)]
+
+
+def _sharded_worker(rank, world, port, levels, inverse):
+    _init(rank, world, port)
+    import oracle
+    import paper_1309_0392_b200 as sgh
+    import sgh_inputs as si
+    L = sgh.shard_layout(levels, world)
+    assert sgh.shard_rows(levels, world, rank) == (L["row_begin"][rank], L["row_begin"][rank] + L["rows"][rank])
+    nd = (1 << levels[-1]) - 1
+    C = si.num_points(levels) // nd
+    rb, R = L["row_begin"][rank], L["rows"][rank]
+    shard = si.fill_uniform(R * C, si.SEED, 3, rb * C).reshape(R, C)
+    op = oracle.dehierarchize if inverse else oracle.hierarchize
+    # 1. local axes 1..d-1: every x_d plane is a (d-1)-dim grid
+    for r in range(R):
+        plane = np.ascontiguousarray(shard[r])
+        op(plane, levels[:-1])
+        shard[r] = plane
+    # 2. pack column blocks and exchange (forward re-shard)
+    sends = [shard[:, L["col_begin"][q]:L["col_begin"][q] + L["cols"][q]] for q in range(world)]
+    recvs = _exchange(sends, [(L["rows"][q], L["cols"][rank]) for q in range(world)], rank, world)
+    slab = np.concatenate(recvs, axis=0)
+    assert slab.shape == (nd, L["cols"][rank])
+    # 3. the axis-d pass: complete poles along x_d
+    for c in range(slab.shape[1]):
+        pole = np.ascontiguousarray(slab[:, c])
+        op(pole, [levels[-1]])
+        slab[:, c] = pole
+    # 4. back to row shards
+    sends = [slab[L["row_begin"][q]:L["row_begin"][q] + L["rows"][q], :] for q in range(world)]
+    recvs = _exchange(sends, [(R, L["cols"][q]) for q in range(world)], rank, world)
+    for q in range(world):
+        shard[:, L["col_begin"][q]:L["col_begin"][q] + L["cols"][q]] = recvs[q]
+    # 5. gather and compare with the single-process oracle, bitwise
+    flat = torch.from_numpy(np.ascontiguousarray(shard).ravel())
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([flat.numel()]))
+    mx = int(max(s.item() for s in sizes))
+    pad = torch.zeros(mx, dtype=torch.float64)
+    pad[:flat.numel()] = flat
+    parts = [torch.zeros(mx, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    if rank == 0:
+        got = np.concatenate([p[:int(s.item())].numpy() for p, s in zip(parts, sizes)])
+        want = op(si.fill_uniform(si.num_points(levels), si.SEED, 3), levels)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), "sharded decomposition differs"
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("levels", [(6, 5), (3, 4, 5), (5, 2, 6), (2, 3, 2, 4)], ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_sharded_decomposition_gloo(levels, inverse):
+    mp.spawn(_sharded_worker, args=(2, _free_port(), levels, inverse), nprocs=2, join=True)
+
+
+def _c5_worker(rank, world, port):
+    _init(rank, world, port)
+    import oracle
+    import sgh_inputs as si
+    cs = si.combination_set(4, 22)
+    sizes = [si.num_points(l) for l in cs]
+    parts = si.lpt_partition(sizes, world)
+    mine = parts[rank]
+    allparts = [None] * world
+    dist.all_gather_object(allparts, mine)
+    ids = sorted(i for p in allparts for i in p)
+    assert ids == list(range(len(cs)))
+    loads = [sum(sizes[i] for i in p) for p in allparts]
+    assert max(loads) / (sum(loads) / world) < 1.0001
+    # each rank hierarchizes its smallest few members; digests gathered over gloo
+    small = sorted(mine, key=lambda i: sizes[i])[:6]
+    dig = {}
+    for i in small:
+        g = oracle.fill_uniform(sizes[i], si.SEED, i)
+        oracle.hierarchize(g, cs[i])
+        dig[i] = oracle.digest(g)
+    alld = [None] * world
+    dist.all_gather_object(alld, dig)
+    if rank == 0:
+        merged = {k: v for d in alld for k, v in d.items()}
+        assert len(merged) == 6 * world
+        for i, v in merged.items():
+            g = oracle.fill_uniform(sizes[i], si.SEED, i)
+            assert oracle.digest(oracle.hierarchize(g, cs[i])) == v
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_c5_partition_gloo():
+    mp.spawn(_c5_worker, args=(2, _free_port()), nprocs=2, join=True)
