@@ -146,7 +146,18 @@ void plan_axis(double *grid, const int32_t *levels, int d, int k, std::vector<Ta
 
 // Whole-pole multi-axis group [a, b).  Returns false if the
 // group's tile does not fit the FUSED budget.
+static int fused_budget() {
+  static int T = -1;
+  if (T < 0) {
+    const char *e = getenv("SGH_FUSED_T");  // tuning experiment override
+    T = e ? atoi(e) : kFusedT;
+    if (T < 1024 || T > 12288) T = kFusedT;
+  }
+  return T;
+}
+
 static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, int b, Task &t) {
+  const int64_t kFusedT = fused_budget();
   int64_t Sa = 1, P = 1, O = 1;
   int busy = 0;
   for (int k = 0; k < a; ++k) Sa *= (int64_t(1) << levels[k]) - 1;
@@ -180,8 +191,17 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
     t.tiles = (O + t.R - 1) / t.R;
     return true;
   }
-  const int W = Sa >= 24 ? 32 : (Sa >= 12 ? 16 : 8);
-  if (P * (W + 2) > kFusedT + kFusedT / 16) return false;
+  static int wmax = -1;
+  if (wmax < 0) {
+    const char *e = getenv("SGH_FUSED_W");  // tuning experiment override (8..128)
+    wmax = e ? atoi(e) : 128;
+    if (wmax != 8 && wmax != 16 && wmax != 32 && wmax != 64 && wmax != 128) wmax = 128;
+  }
+  // widest tile that fits: long contiguous row segments keep DRAM efficient
+  int W = 8;
+  while (W < wmax && W < Sa) W <<= 1;
+  while (W > 8 && P * (W + 1) > kFusedT + kFusedT / 16) W >>= 1;
+  if (P * (W + 1) > kFusedT + kFusedT / 16) return false;
   t.W = W;
   t.R = 1;
   t.OS = P * Sa;
@@ -190,24 +210,53 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
   return true;
 }
 
+// Estimated time per byte (1 / TB/s) of a pass, from the kernels' measured
+// B200 throughput (profiles/r01): wide contiguous tiles stream best, narrow
+// column tiles lose DRAM efficiency.
+static double pass_cost(const std::vector<Task> &phases) {
+  double c = 0;
+  for (size_t i = 0; i < phases.size(); ++i) {
+    const Task &t = phases[i];
+    double bw;
+    switch (t.kind) {
+      case KIND_FLAT_SLABS:
+      case KIND_FLAT_BLOCKS: bw = 5.6; break;
+      case KIND_REG: bw = 5.0; break;
+      case KIND_STRIDED: bw = t.W >= 128 ? 4.8 : (t.W >= 64 ? 4.6 : 3.9); break;
+      case KIND_FUSED:
+        bw = t.W == 1 ? 5.2 : t.W >= 128 ? 4.6 : t.W >= 64 ? 4.3 : t.W >= 32 ? 4.0 : t.W >= 16 ? 3.3 : 2.2;
+        break;
+      default: bw = 4.0;
+    }
+    // later phases are coarse lattices: a small fraction of the points, latency bound
+    c += (i == 0) ? 1.0 / bw : 2.0 * task_points(t) / std::max(1.0, task_points(phases[0])) / 1.0;
+  }
+  return c;
+}
+
 // Passes of a whole grid (hierarchization order inside each pass).  With
-// `fuse`, a DP over consecutive axis groups picks the fewest HBM round trips:
-// a group is either one axis (per-axis kernels) or a run of axes whose whole
-// poles fit one FUSED tile.  The axis order stays 1..d, so results
-// are bitwise equal to the per-axis path.
+// `fuse`, a DP over consecutive axis groups picks the plan of least estimated
+// time: a group is either one axis (per-axis kernels) or a run of axes whose
+// whole poles fit one FUSED tile.  The axis order stays 1..d, so the
+// results are bitwise equal to the per-axis path.
 void plan_grid(double *grid, const int32_t *levels, int d, bool fuse, std::vector<std::vector<Task>> &passes) {
   passes.clear();
-  std::vector<int> cost(d + 1, 1 << 20), from(d + 1, -1);
+  const double kInf = 1e30;
+  std::vector<double> cost(d + 1, kInf);
+  std::vector<int> from(d + 1, -1);
   cost[0] = 0;
   for (int i = 0; i < d; ++i) {
-    if (cost[i] >= (1 << 20)) continue;
-    const int c1 = cost[i] + (levels[i] > 1 ? 1 : 0);     // one axis
+    if (cost[i] >= kInf) continue;
+    std::vector<Task> ph;
+    plan_axis(grid, levels, d, i, ph);
+    const double c1 = cost[i] + (ph.empty() ? 0.0 : pass_cost(ph));
     if (c1 < cost[i + 1]) { cost[i + 1] = c1; from[i + 1] = i; }
     if (!fuse) continue;
     Task t;
     for (int j = i + 2; j <= d; ++j) {
       if (!plan_fused_group(grid, levels, d, i, j, t)) continue;
-      if (cost[i] + 1 < cost[j] || (cost[i] + 1 == cost[j] && from[j] < i)) { cost[j] = cost[i] + 1; from[j] = i; }
+      const double cj = cost[i] + pass_cost(std::vector<Task>{t});
+      if (cj < cost[j] - 1e-12) { cost[j] = cj; from[j] = i; }
     }
   }
   std::vector<std::pair<int, int>> groups;

@@ -29,7 +29,7 @@ constexpr int kFlatCap = kFlatT + kFlatMaxS + 2;
 constexpr int kStridedWMax = 128;  // STRIDED tile width W in {32, 64, 128} columns
 constexpr int kStridedTileDoubles = 4480;  // STRIDED tile budget: (2^t + 1) * (W + 2) doubles (35 KB)
 constexpr int kRegMaxL = 4;        // REG kernel: poles of up to 15 points in registers
-constexpr int kFusedT = 8192;      // FUSED tile budget (doubles, excluding row padding)
+constexpr int kFusedT = 8192;      // FUSED tile budget per pipeline stage (doubles, excl. row padding)
 
 enum Kind : int32_t {
   KIND_FLAT_SLABS = 0,   // R whole slabs (o) per tile; needs PS==S, OS==n*S, n*S <= kFlatT

@@ -38,6 +38,7 @@ struct Src {
   const Task *tasks;      // device task table, or nullptr -> use `single`
   const int64_t *prefix;  // device exclusive prefix of task tiles, ntasks+1 entries
   int32_t ntasks;
+  int32_t stage_doubles;  // FUSED: SMEM doubles per pipeline stage (2 stages)
   int64_t total_tiles;
   Task single;
 };
@@ -54,6 +55,9 @@ __device__ __forceinline__ void cp_async16(double *sdst, const double *gsrc) {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // 8-byte phase of a global address (0: 16-byte aligned, 1: 8 mod 16)
 __device__ __forceinline__ int phase8(const double *p) { return (int)((reinterpret_cast<uintptr_t>(p) >> 3) & 1); }
@@ -368,6 +372,28 @@ __device__ __forceinline__ FDiv device_fdiv(uint32_t d) {
 // rows 0..P-1 of W columns (wc valid), global row r at g + r*S (S odd), SMEM row r at sb + r*(W+1).
 // Lane = (sub-row, 16-byte slot): one warp instruction covers 32/(W/2) rows.
 template <int W>
+__device__ __forceinline__ void fused_load_rows_wide(double *sb, const double *g, int64_t S, int par0, int P, int wc) {
+  constexpr int RS = W + 1;
+  constexpr int NP = W / 2;                       // 16-byte slots per row (32 or 64)
+  constexpr int LOGP = (NP == 32) ? 5 : 6;
+  const int nslots = P * NP;
+#pragma unroll 4
+  for (int p = threadIdx.x; p < nslots; p += kThreads) {
+    const int r = p >> LOGP;
+    const int k = p & (NP - 1);
+    const int par = (par0 + r) & 1;
+    const double *gr = g + (int64_t)r * S;
+    double *sr = sb + r * RS;
+    const int npairs = (wc - par) >> 1;
+    const int c = par + 2 * k;
+    if (k < npairs) cp_async16(sr + c, gr + c);
+    if (k == NP - 1 && par) cp_async8(sr, gr);
+    const int last = par + 2 * npairs;
+    if (k == NP - 2 && last < wc) cp_async8(sr + last, gr + last);
+  }
+}
+
+template <int W>
 __device__ __forceinline__ void fused_load_rows(double *sb, const double *g, int64_t S, int par0, int P, int wc) {
   constexpr int RS = W + 1;
   constexpr int NP = W / 2;                       // 16-byte slots per row
@@ -454,36 +480,50 @@ __device__ __forceinline__ void pole_serial(double *p, int l, int STR) {
   }
 }
 
+// geometry of one FUSED tile
+struct FusedTile {
+  double *g;   // global base: W == 1 start of the range; W > 1 row 0 at column c0
+  int units;   // W == 1: units in this tile
+  int wc;      // W > 1: valid columns
+  int par;     // 8-byte phase of g (SMEM data starts at stage + par)
+};
+
+template <int W>
+__device__ __forceinline__ FusedTile fused_tile(const Task &T, int64_t q) {
+  FusedTile f;
+  if (W == 1) {
+    const int64_t u0 = q * T.R;
+    f.units = (int)min((int64_t)T.R, T.O - u0);
+    f.g = T.grid + T.base + u0 * T.P;
+    f.wc = 1;
+  } else {
+    const int64_t cb = q % T.ncb;
+    const int64_t o = q / T.ncb;
+    const int64_t c0 = cb * W;
+    f.units = 1;
+    f.wc = (int)min((int64_t)W, T.S - c0);
+    f.g = T.grid + T.base + o * T.OS + c0;        // (row r, col c) at g[r*S + c]
+  }
+  f.par = phase8(f.g);
+  return f;
+}
+
+template <int W>
+__device__ __forceinline__ void fused_issue(const Task &T, const FusedTile &f, double *stage) {
+  if (W == 1) copy_range_async(stage + f.par, f.g, f.units * T.P);
+  else if (W >= 64) fused_load_rows_wide<(W >= 64 ? W : 64)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
+  else fused_load_rows<(W == 1 || W >= 64 ? 8 : W)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
+}
+
+// all axes of the group on a staged tile, then the store
 template <bool INV, int W>
-__global__ void __launch_bounds__(kThreads, 3) k_fused(const __grid_constant__ Src src) {
-  extern __shared__ __align__(16) double smem[];
+__device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTile &f, double *sm) {
   constexpr int RS = (W == 1) ? 1 : W + 1;
-  constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : 5;
-  for_each_tile(src, [&](const Task &T, int64_t q) {
-    const int P = T.P;
-    double *gbase;
-    int units = 1, wc = 1;
-    int64_t S = 1;
-    double *sm;
-    if (W == 1) {
-      const int64_t u0 = q * T.R;
-      units = (int)min((int64_t)T.R, T.O - u0);
-      gbase = T.grid + T.base + u0 * P;
-      sm = smem + phase8(gbase);
-      copy_range_async(sm, gbase, units * P);
-    } else {
-      const int64_t cb = q % T.ncb;
-      const int64_t o = q / T.ncb;
-      const int64_t c0 = cb * W;
-      S = T.S;
-      wc = (int)min((int64_t)W, S - c0);
-      gbase = T.grid + T.base + o * T.OS + c0;      // (row r, col c) at gbase[r*S + c]
-      const int par0 = phase8(gbase);
-      sm = smem + par0;
-      fused_load_rows<(W == 1 ? 8 : W)>(sm, gbase, S, par0, P, wc);
-    }
-    cp_async_wait_all();
-    __syncthreads();
+  constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
+  const int P = T.P;
+  const int units = f.units, wc = f.wc;
+  const int64_t S = T.S;
+  double *gbase = f.g;
     const int rows_total = units * P;
     for (int j = 0; j < T.m; ++j) {                   // axes ascending
       const int l = T.gl[j];
@@ -553,23 +593,91 @@ __global__ void __launch_bounds__(kThreads, 3) k_fused(const __grid_constant__ S
       }
     }
     if (W == 1) {
-      for (int e = threadIdx.x; e < rows_total; e += kThreads) gbase[e] = sm[e];
+      for (int e = threadIdx.x; e < rows_total; e += kThreads) __stcg(gbase + e, sm[e]);
     } else {
-      constexpr int RPI = 32 / W;                   // rows per warp instruction
+      constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
+      constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
       constexpr int STEP = RPI * (kThreads / 32);
       const int lane = threadIdx.x & 31;
-      const int c = lane % W;
-      int row = (threadIdx.x >> 5) * RPI + lane / W;
-      double *gr = gbase + (int64_t)row * S + c;
-      const double *sr = sm + row * RS + c;
+      const int c0 = (W >= 32) ? lane : lane % W;
+      int row = (threadIdx.x >> 5) * RPI + ((W >= 32) ? 0 : lane / W);
+      double *gr = gbase + (int64_t)row * S;
+      const double *sr = sm + row * RS;
       const int64_t gstep = (int64_t)STEP * S;
-      if (c < wc) {
-#pragma unroll 4
-        for (; row < P; row += STEP, gr += gstep, sr += STEP * RS) *gr = *sr;
+#pragma unroll 2
+      for (; row < P; row += STEP, gr += gstep, sr += STEP * RS) {
+#pragma unroll
+        for (int u = 0; u < CPL; ++u) {
+          const int c = c0 + 32 * u;
+          if (c < wc) __stcg(gr + c, sr[c]);
+        }
       }
     }
+}
+
+// Persistent, double-buffered: while a CTA transforms tile k in one SMEM stage,
+// the cp.async copies of tile k+1 fill the other, so HBM reads overlap the
+// SMEM work instead of alternating with it.
+template <bool INV, int W, int STAGES>
+__global__ void __launch_bounds__(kThreads, (STAGES == 1 ? 3 : 2)) k_fused(const __grid_constant__ Src src) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ Task s_task[2];                      // descriptors of the two in-flight tiles
+  int64_t q = blockIdx.x;
+  if (q >= src.total_tiles) return;
+  int idx = -1;
+  auto stage_task = [&](Task *dst, const Task *from) {
+    const uint64_t *a = reinterpret_cast<const uint64_t *>(from);
+    uint64_t *b = reinterpret_cast<uint64_t *>(dst);
+    for (int i = threadIdx.x; i < (int)(sizeof(Task) / 8); i += kThreads) b[i] = a[i];
+  };
+  auto ref = [&](int64_t qq, int64_t &ql) -> const Task * {
+    if (!src.tasks) {
+      ql = qq;
+      return &src.single;
+    }
+    idx = (idx < 0) ? first_task(src, qq) : advance_task(src, idx, qq);
+    ql = qq - __ldg(&src.prefix[idx]);
+    return &src.tasks[idx];
+  };
+  int64_t ql;
+  const Task *Tc = ref(q, ql);
+  FusedTile fc = fused_tile<W>(*Tc, ql);
+  fused_issue<W>(*Tc, fc, smem);
+  cp_async_commit();
+  stage_task(&s_task[0], Tc);
+  for (int k = 0;; ++k) {
+    double *cur = smem + (STAGES == 2 ? (k & 1) * src.stage_doubles : 0);
+    const int64_t qn = q + gridDim.x;
+    const bool more = qn < src.total_tiles;
+    const Task *Tn = Tc;
+    FusedTile fn = fc;
+    if (STAGES == 2 && more) {
+      int64_t qln;
+      Tn = ref(qn, qln);
+      fn = fused_tile<W>(*Tn, qln);
+      fused_issue<W>(*Tn, fn, smem + ((k + 1) & 1) * src.stage_doubles);
+      cp_async_commit();
+      stage_task(&s_task[(k + 1) & 1], Tn);
+      cp_async_wait<1>();                         // tile k has landed (tile k+1 may be in flight)
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-  });
+    fused_compute_store<INV, W>(s_task[STAGES == 2 ? (k & 1) : 0], fc, cur + fc.par);
+    __syncthreads();                              // the stage is free for the next load
+    if (!more) break;
+    q = qn;
+    if (STAGES == 1) {                            // single stage: load the next tile now
+      int64_t qln;
+      Tn = ref(qn, qln);
+      fn = fused_tile<W>(*Tn, qln);
+      fused_issue<W>(*Tn, fn, smem);
+      cp_async_commit();
+      stage_task(&s_task[0], Tn);
+    }
+    Tc = Tn;
+    fc = fn;
+  }
 }
 
 // ----------------------------------------------------------------------- REG
@@ -639,6 +747,16 @@ __global__ void __launch_bounds__(kThreads) k_reg(const __grid_constant__ Src sr
 // ------------------------------------------------------------ host launchers
 using KernelFn = void (*)(Src);
 
+// FUSED pipeline depth: 1 (default) or 2 stages (tuning override SGH_FUSED_STAGES)
+int fused_stages() {
+  static int st = -1;
+  if (st < 0) {
+    const char *e = getenv("SGH_FUSED_STAGES");
+    st = (e && atoi(e) == 2) ? 2 : 1;
+  }
+  return st;
+}
+
 static KernelFn kernel_for(int kind, int l, int w, bool inv) {
   switch (kind) {
     case KIND_FLAT_SLABS: return inv ? k_flat_slabs<true> : k_flat_slabs<false>;
@@ -651,11 +769,24 @@ static KernelFn kernel_for(int kind, int l, int w, bool inv) {
         default: return nullptr;
       }
     case KIND_FUSED:
+      if (fused_stages() == 2) {
+        switch (w) {
+          case 1: return inv ? k_fused<true, 1, 2> : k_fused<false, 1, 2>;
+          case 8: return inv ? k_fused<true, 8, 2> : k_fused<false, 8, 2>;
+          case 16: return inv ? k_fused<true, 16, 2> : k_fused<false, 16, 2>;
+          case 32: return inv ? k_fused<true, 32, 2> : k_fused<false, 32, 2>;
+          case 64: return inv ? k_fused<true, 64, 2> : k_fused<false, 64, 2>;
+          case 128: return inv ? k_fused<true, 128, 2> : k_fused<false, 128, 2>;
+          default: return nullptr;
+        }
+      }
       switch (w) {
-        case 1: return inv ? k_fused<true, 1> : k_fused<false, 1>;
-        case 8: return inv ? k_fused<true, 8> : k_fused<false, 8>;
-        case 16: return inv ? k_fused<true, 16> : k_fused<false, 16>;
-        case 32: return inv ? k_fused<true, 32> : k_fused<false, 32>;
+        case 1: return inv ? k_fused<true, 1, 1> : k_fused<false, 1, 1>;
+        case 8: return inv ? k_fused<true, 8, 1> : k_fused<false, 8, 1>;
+        case 16: return inv ? k_fused<true, 16, 1> : k_fused<false, 16, 1>;
+        case 32: return inv ? k_fused<true, 32, 1> : k_fused<false, 32, 1>;
+        case 64: return inv ? k_fused<true, 64, 1> : k_fused<false, 64, 1>;
+        case 128: return inv ? k_fused<true, 128, 1> : k_fused<false, 128, 1>;
         default: return nullptr;
       }
     case KIND_REG:
@@ -714,7 +845,11 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
   src.ntasks = 1;
   src.total_tiles = task.tiles;
   src.single = task;
-  const size_t smem = task_smem(task);
+  size_t smem = task_smem(task);
+  if (task.kind == KIND_FUSED) {                 // pipeline stages, 16-byte aligned
+    src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
+    smem = size_t(fused_stages()) * src.stage_doubles * 8;
+  }
   const int64_t cap = resident_ctas(fn, smem);
   const int64_t grid = task.tiles < cap ? task.tiles : cap;
   if (grid <= 0) return cudaSuccess;
@@ -736,6 +871,10 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
   src.prefix = d_prefix;
   src.ntasks = ntasks;
   src.total_tiles = total_tiles;
+  if (kind == KIND_FUSED) {
+    src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
+    smem = size_t(fused_stages()) * src.stage_doubles * 8;
+  }
   const int64_t cap = resident_ctas(fn, smem);
   const int64_t grid = total_tiles < cap ? total_tiles : cap;
   if (grid <= 0) return cudaSuccess;

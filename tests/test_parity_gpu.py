@@ -66,6 +66,8 @@ SHAPES = [
     # multi-axis FUSED groups: contiguous (W=1) and column (W=8/16/32) tiles
     (1, 1, 5, 5), (5, 3, 3), (3, 4, 4, 2), (6, 6, 5, 5), (2, 3, 6, 6), (4, 2, 3, 7), (10, 4, 4, 4), (1, 3, 1, 4, 4),
     (7, 6, 6), (3, 5, 6), (2, 2, 6, 5, 1),
+    # wide FUSED column tiles (W = 64 / 128) with ragged column groups
+    (7, 2, 3), (6, 3, 3), (8, 2, 2, 2), (9, 3, 2), (5, 1, 2, 2),
 ]
 
 
