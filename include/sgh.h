@@ -212,7 +212,7 @@ sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_
  * 1 FLAT_BLOCKS, 2 STRIDED, 3 REG.  bytes = 16 x points transformed. */
 typedef struct {
     int32_t kind;
-    int32_t level;    /* pole level for REG, else the task's l */
+    int32_t level;    /* REG: pole level; STRIDED / FUSED: tile width W; else the task's l */
     int32_t inverse;  /* 1 for dehierarchization */
     int32_t reserved;
     double bytes;     /* algorithmic bytes (one read + one write per point) */

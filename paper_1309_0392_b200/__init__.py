@@ -30,7 +30,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsgh.so")
+# SGH_LIB_PATH selects a tuning variant built with `build.py --out` (experiments only)
+LIB_PATH = os.environ.get("SGH_LIB_PATH") or os.path.join(_HERE, "lib", "libsgh.so")
 
 FLAG_DEHIERARCHIZE = 1
 FLAG_PER_AXIS = 2
@@ -220,7 +221,7 @@ def profile_read():
     n = int(lib.sgh_profile_read(ctypes.cast(buf, ctypes.c_void_p), n))
     out = []
     for r in buf[:n]:
-        name = KIND_NAMES.get(r.kind, str(r.kind)) + (f"<{r.level}>" if r.kind == 3 else "")
+        name = KIND_NAMES.get(r.kind, str(r.kind)) + (f"<{r.level}>" if r.kind in (2, 3, 4) else "")
         out.append({"kernel": name, "level": r.level, "inverse": bool(r.inverse), "bytes": r.bytes, "ms": r.ms})
     return out
 

@@ -49,16 +49,18 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build LIB (or a tuning variant at `out` with extra -D defines)."""
+    target = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
+    os.makedirs(os.path.dirname(target), exist_ok=True)
     inc, libdir = nccl_paths()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-cudart", "static", "-Xptxas", "-v" if verbose else "-O3",
-           f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}",
-           *sources(), "-o", LIB + ".tmp",
+           f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}", *[f"-D{d}" for d in defines],
+           *sources(), "-o", target + ".tmp",
            f"-L{libdir}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={libdir}"]
     if verbose:
         print(" ".join(cmd))
@@ -68,13 +70,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libsgh.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--out", default=None, help="build a tuning variant here instead of lib/libsgh.so")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra preprocessor define")
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, a.out, a.defines))

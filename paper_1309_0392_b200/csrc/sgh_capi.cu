@@ -184,9 +184,15 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
   t.O = O;
   t.l = levels[a];
   if (Sa == 1) {
+    static int t1 = -1;
+    if (t1 < 0) {
+      const char *e = getenv("SGH_FUSED_T1");  // tuning experiment override (contiguous tiles)
+      t1 = e ? atoi(e) : (int)kFusedT;
+      if (t1 < 1024 || t1 > 12288) t1 = (int)kFusedT;
+    }
     if (P > kFusedT) return false;
     t.W = 1;
-    t.R = (int32_t)(kFusedT / P);
+    t.R = (int32_t)(std::max<int64_t>(t1, P) / P);
     t.OS = P;
     t.tiles = (O + t.R - 1) / t.R;
     return true;

@@ -453,6 +453,167 @@ __device__ __forceinline__ void pole_regs(double *p, int STR) {
   }
 }
 
+// Alg. 1 on one longer pole (5 <= L <= 7) in registers, by the block + coarse
+// lattice decomposition of SURVEY 8(a) a3.iii applied inside one thread:
+// points with tz(i) < 3 have both predecessors in their aligned 8-point block
+// [8b, 8b+8], so each block is transformed from 9 registers; the coarse points
+// {8j} form a level-(L-3) pole (stride 8) done by pole_regs.  Hierarchization:
+// blocks first (they read the unmodified coarse ends), then the lattice;
+// dehierarchization: lattice first, then the blocks coarse -> fine.  Same
+// per-point operations as Alg. 1, so bitwise identical.
+template <int L, bool INV>
+__device__ __forceinline__ void pole_blocked(double *p, int STR) {
+  constexpr int T = 3;
+  constexpr int B = 1 << T;
+  constexpr int n = (1 << L) - 1;
+  constexpr int nb = 1 << (L - T);
+  if (INV) pole_regs<L - T, true>(p + (B - 1) * STR, B * STR);
+#pragma unroll
+  for (int b = 0; b < nb; ++b) {
+    double v[B + 1];
+#pragma unroll
+    for (int r = 0; r <= B; ++r) {
+      const int i = b * B + r;
+      v[r] = (i >= 1 && i <= n) ? p[(i - 1) * STR] : 0.0;   // i = 0 / 2^L: boundary, never used
+    }
+    if (!INV) {
+#pragma unroll
+      for (int r = 1; r < B; ++r) {
+        const int i = b * B + r;
+        const int s = r & -r;
+        double x = v[r];
+        if (i - s >= 1) x = x - 0.5 * v[r - s];
+        if (i + s <= n) x = x - 0.5 * v[r + s];
+        p[(i - 1) * STR] = x;
+      }
+    } else {
+#pragma unroll
+      for (int s = B / 2; s >= 1; s >>= 1) {
+#pragma unroll
+        for (int r = s; r < B; r += 2 * s) {
+          const int i = b * B + r;
+          double x = v[r];
+          if (i - s >= 1) x = x + 0.5 * v[r - s];
+          if (i + s <= n) x = x + 0.5 * v[r + s];
+          v[r] = x;
+        }
+      }
+#pragma unroll
+      for (int r = 1; r < B; ++r) p[(b * B + r - 1) * STR] = v[r];
+    }
+  }
+  if (!INV) pole_regs<L - T, false>(p + (B - 1) * STR, B * STR);
+}
+
+// One aligned 8-point block of a (lattice) pole held in 9 registers.  p0 is the
+// address of the virtual point j = 0 of the lattice (never dereferenced), point
+// j at p0[j*STR]; the lattice has nblk blocks, i.e. n = 8*nblk - 1 points.
+// Writes only the block's fine points j = 8b+1 .. 8b+7 (a3.iii).
+template <bool INV>
+__device__ __forceinline__ void block8(double *p0, int STR, int b, int nblk) {
+  double v[9];
+  const int n = 8 * nblk - 1;
+#pragma unroll
+  for (int r = 0; r <= 8; ++r) {
+    const int j = 8 * b + r;
+    v[r] = (j >= 1 && j <= n) ? p0[j * STR] : 0.0;
+  }
+  if (!INV) {
+#pragma unroll
+    for (int r = 1; r < 8; ++r) {
+      const int s = r & -r;
+      const int j = 8 * b + r;
+      double x = v[r];
+      if (j - s >= 1) x = x - 0.5 * v[r - s];    // left predecessor
+      if (j + s <= n) x = x - 0.5 * v[r + s];    // right predecessor
+      p0[j * STR] = x;
+    }
+  } else {
+#pragma unroll
+    for (int s = 4; s >= 1; s >>= 1) {
+#pragma unroll
+      for (int r = s; r < 8; r += 2 * s) {
+        const int j = 8 * b + r;
+        double x = v[r];
+        if (j - s >= 1) x = x + 0.5 * v[r - s];
+        if (j + s <= n) x = x + 0.5 * v[r + s];
+        v[r] = x;
+      }
+    }
+#pragma unroll
+    for (int r = 1; r < 8; ++r) p0[(8 * b + r) * STR] = v[r];
+  }
+}
+
+template <bool INV>
+__device__ __forceinline__ void pole_regs_rt(double *p, int L, int STR) {
+  switch (L) {
+    case 2: pole_regs<2, INV>(p, STR); break;
+    case 3: pole_regs<3, INV>(p, STR); break;
+    case 4: pole_regs<4, INV>(p, STR); break;
+    default: break;                              // L = 1: a single point, no update
+  }
+}
+
+// One axis of a staged tile, all npoles poles of level l (pole p = (oo, rk, c)
+// at sm + (oo*n*R + rk)*RS + c, point stride R*RS), in parallel work items:
+// l <= 4: one register pole per thread; l >= 5: (pole, 8-block) items on the
+// level-l pole, then on its coarse lattice (stride x8, level l-3), ... until
+// the lattice has l' <= 4, done as register poles.  A barrier between lattice
+// levels; hierarchization runs fine -> coarse, dehierarchization the reverse.
+template <bool INV, int W>
+__device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv &fR, int Ok) {
+  constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
+  const int n = (1 << l) - 1;
+  const int npoles = Ok * R * W;
+  const int STR = R * RS;
+  auto pole_base = [&](int p) -> double * {
+    const int c = p & (W - 1);
+    const int rest = p >> LOGW;
+    const int oo = (int)fdiv((uint32_t)rest, fR);
+    const int rk = rest - oo * R;
+    return sm + (oo * n * R + rk) * RS + c;
+  };
+  if (l <= 4) {
+    for (int p = threadIdx.x; p < npoles; p += kThreads) pole_regs_rt<INV>(pole_base(p), l, STR);
+    __syncthreads();
+    return;
+  }
+  // lattice levels visited: l, l-3, l-6, ... (> 4), then the register lattice
+  int levels[8], nlev = 0, lf = l;
+  while (lf > 4) {
+    levels[nlev++] = lf;
+    lf -= 3;
+  }
+  const FDiv fP = device_fdiv((uint32_t)npoles);
+  auto block_phase = [&](int k) {                // k-th lattice level: stride 8^k
+    const int m = 1 << (3 * k);
+    const int nblk = 1 << (levels[k] - 3);
+    const int items = npoles * nblk;
+    for (int it = threadIdx.x; it < items; it += kThreads) {
+      const int b = (int)fdiv((uint32_t)it, fP);
+      const int p = it - b * npoles;             // lanes run over poles: conflict-free SMEM
+      block8<INV>(pole_base(p) - STR, m * STR, b, nblk);
+    }
+    __syncthreads();
+  };
+  auto lattice_phase = [&]() {
+    const int m = 1 << (3 * nlev);
+    for (int p = threadIdx.x; p < npoles; p += kThreads) {
+      double *p0 = pole_base(p) - STR;           // virtual point 0
+      pole_regs_rt<INV>(p0 + m * STR, lf, m * STR);
+    }
+    __syncthreads();
+  };
+  if (!INV) {
+    for (int k = 0; k < nlev; ++k) block_phase(k);
+    lattice_phase();
+  } else {
+    lattice_phase();
+    for (int k = nlev - 1; k >= 0; --k) block_phase(k);
+  }
+}
+
 // Alg. 1 on one pole of n = 2^l - 1 points at p[0], p[STR], ... (serial)
 template <bool INV>
 __device__ __forceinline__ void pole_serial(double *p, int l, int STR) {
@@ -532,65 +693,7 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
       const int R = T.gR[j];
       const FDiv fR = T.fR[j];
       const int Ok = rows_total / (n * R);
-      const int npoles = Ok * R * W;
-      if (npoles >= 2 * kThreads / 3) {
-        // pole owners: a pole = (oo, rk, c); lanes run over c (W > 1) or rk / oo
-        const int STR = R * RS;
-        auto run = [&](auto op) {
-          for (int p = threadIdx.x; p < npoles; p += kThreads) {
-            const int c = p & (W - 1);
-            const int rest = p >> LOGW;
-            const int oo = (int)fdiv((uint32_t)rest, fR);
-            const int rk = rest - oo * R;
-            op(sm + (oo * n * R + rk) * RS + c);
-          }
-        };
-        switch (l) {
-          case 2: run([&](double *pp) { pole_regs<2, INV>(pp, STR); }); break;
-          case 3: run([&](double *pp) { pole_regs<3, INV>(pp, STR); }); break;
-          case 4: run([&](double *pp) { pole_regs<4, INV>(pp, STR); }); break;
-          default: run([&](double *pp) { pole_serial<INV>(pp, l, STR); }); break;
-        }
-        __syncthreads();
-      } else {
-        // few long poles: all threads sweep one level at a time
-        const FDiv fO = device_fdiv((uint32_t)Ok);
-        const bool across = (W == 1) && (R == 1);
-        for (int st = 0; st < l - 1; ++st) {
-          const int lam = INV ? 2 + st : l - st;
-          const int s = 1 << (l - lam);
-          const int lh = lam - 1;
-          const int cnt = (Ok << lh) * R * W;
-          for (int idx = threadIdx.x; idx < cnt; idx += kThreads) {
-            int c = 0, rk, jx, oo;
-            if (across) {
-              jx = (int)fdiv((uint32_t)idx, fO);
-              oo = idx - jx * Ok;
-              rk = 0;
-            } else {
-              c = idx & (W - 1);
-              const int rest = idx >> LOGW;
-              const int q2 = (int)fdiv((uint32_t)rest, fR);
-              rk = rest - q2 * R;
-              jx = q2 & ((1 << lh) - 1);
-              oo = q2 >> lh;
-            }
-            const int i = s * (2 * jx + 1);
-            double *x0 = sm + ((oo * n + (i - 1)) * R + rk) * RS + c;
-            const int sd = s * R * RS;
-            double x = *x0;
-            if (!INV) {
-              if (i - s >= 1) x = x - 0.5 * x0[-sd];      // left predecessor
-              if (i + s <= n) x = x - 0.5 * x0[sd];       // right predecessor
-            } else {
-              if (i - s >= 1) x = x + 0.5 * x0[-sd];
-              if (i + s <= n) x = x + 0.5 * x0[sd];
-            }
-            *x0 = x;
-          }
-          __syncthreads();
-        }
-      }
+      fused_axis<INV, W>(sm, RS, l, R, fR, Ok);
     }
     if (W == 1) {
       for (int e = threadIdx.x; e < rows_total; e += kThreads) __stcg(gbase + e, sm[e]);
@@ -618,8 +721,11 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
 // Persistent, double-buffered: while a CTA transforms tile k in one SMEM stage,
 // the cp.async copies of tile k+1 fill the other, so HBM reads overlap the
 // SMEM work instead of alternating with it.
+#ifndef FUSED_MINB
+#define FUSED_MINB 3   // resident CTAs per SM the FUSED register budget is sized for
+#endif
 template <bool INV, int W, int STAGES>
-__global__ void __launch_bounds__(kThreads, (STAGES == 1 ? 3 : 2)) k_fused(const __grid_constant__ Src src) {
+__global__ void __launch_bounds__(kThreads, (STAGES == 1 ? FUSED_MINB : 2)) k_fused(const __grid_constant__ Src src) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Task s_task[2];                      // descriptors of the two in-flight tiles
   int64_t q = blockIdx.x;
@@ -856,7 +962,8 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
   ProfToken tok = prof_begin(stream);
   fn<<<(unsigned)grid, kThreads, smem, stream>>>(src);
   cudaError_t e = cudaGetLastError();
-  prof_end(tok, task.kind, task.l, inv, 16.0 * task_points(task), stream);
+  prof_end(tok, task.kind, task.kind == KIND_FUSED || task.kind == KIND_STRIDED ? task.W : task.l, inv,
+           16.0 * task_points(task), stream);
   return e;
 }
 
@@ -881,7 +988,7 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
   ProfToken tok = prof_begin(stream);
   fn<<<(unsigned)grid, kThreads, smem, stream>>>(src);
   cudaError_t e = cudaGetLastError();
-  prof_end(tok, kind, l, inv, 16.0 * points, stream);
+  prof_end(tok, kind, kind == KIND_FUSED || kind == KIND_STRIDED ? w : l, inv, 16.0 * points, stream);
   return e;
 }
 
