@@ -119,14 +119,31 @@ void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64
   static int wpref = -1;
   if (wpref < 0) {
     const char *e = getenv("SGH_STRIDED_W");  // tuning experiment override
-    wpref = e ? atoi(e) : 128;
-    if (wpref != 32 && wpref != 64 && wpref != 128) wpref = 128;
+    wpref = e ? atoi(e) : 256;
+    if (wpref != 32 && wpref != 64 && wpref != 128 && wpref != 256) wpref = 128;
   }
+  static int64_t tile_budget = -1;
+  if (tile_budget < 0) {
+    const char *e = getenv("SGH_STRIDED_TILE");  // tuning experiment override (doubles)
+    tile_budget = e ? atoll(e) : kStridedTileDoubles;
+    if (tile_budget < 1024 || tile_budget > 13000) tile_budget = kStridedTileDoubles;
+  }
+  auto tmax_of = [&](int w) {
+    int tm = 0;
+    while (((int64_t(1) << (tm + 1)) + 1) * (w + 2) <= tile_budget) ++tm;
+    return tm;
+  };
   int W = wpref;
   while (W > 32 && S <= W / 2 + W / 4) W >>= 1;
-  int tmax = 0;
-  while (((int64_t(1) << (tmax + 1)) + 1) * (W + 2) <= kStridedTileDoubles) ++tmax;
-  const int tb = std::min(l, tmax);
+  // Prefer a width whose tile holds the whole pole (no coarse-lattice phase;
+  // l - t == 1 leaves only the root, which has no update) as long as rows stay
+  // >= 512 B; otherwise the widest tile and a lattice phase.
+  for (int w = W; w >= 64; w >>= 1)
+    if (tmax_of(w) >= l - 1) {
+      W = w;
+      break;
+    }
+  const int tb = std::min(l, tmax_of(W));   // l - tb == 1: the lattice is the root alone (no phase)
   t.kind = KIND_STRIDED;
   t.W = W;
   t.t = tb;

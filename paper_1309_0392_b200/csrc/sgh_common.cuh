@@ -27,7 +27,7 @@ constexpr int kFlatT = 4096;       // FLAT tile: 2^12 elements (32 KB)
 constexpr int kFlatMaxS = 64;      // FLAT handles views with S < 64 columns
 constexpr int kFlatCap = kFlatT + kFlatMaxS + 2;
 constexpr int kStridedWMax = 128;  // STRIDED tile width W in {32, 64, 128} columns
-constexpr int kStridedTileDoubles = 4480;  // STRIDED tile budget: (2^t + 1) * (W + 2) doubles (35 KB)
+constexpr int kStridedTileDoubles = 8960;  // STRIDED tile budget: (2^t + 1) * (W + 2) doubles (70 KB)
 constexpr int kRegMaxL = 4;        // REG kernel: poles of up to 15 points in registers
 constexpr int kFusedT = 8192;      // FUSED tile budget per pipeline stage (doubles, excl. row padding)
 
