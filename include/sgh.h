@@ -69,6 +69,10 @@ typedef enum {
 #define SGH_FLAG_DEHIERARCHIZE 1u /* run the inverse transform instead  */
 #define SGH_FLAG_PER_AXIS 2u      /* one HBM round trip per axis: disable the multi-axis
                                      FUSED kernel (a4); results are bitwise identical */
+#define SGH_FLAG_WHOLE_POLES 4u   /* fused groups hold whole poles only: no BLOCKED
+                                     groups (an axis split into aligned 2^t blocks +
+                                     end points, its coarse lattice a later phase;
+                                     SURVEY 8(a) a3.iii/a4); results are bitwise identical */
 
 /* ------------------------------------------------------------ geometry */
 
@@ -209,17 +213,24 @@ sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_
  * sgh_profile_enable(0) stops (and clears).  sgh_profile_read fills up to
  * `capacity` records (waiting for their events) and returns the number of
  * records; out may be NULL to query the count.  kind: 0 FLAT_SLABS,
- * 1 FLAT_BLOCKS, 2 STRIDED, 3 REG.  bytes = 16 x points transformed. */
+ * 1 FLAT_BLOCKS, 2 STRIDED, 3 REG, 4 FUSED.  bytes = 16 x points transformed. */
 typedef struct {
     int32_t kind;
     int32_t level;    /* REG: pole level; STRIDED / FUSED: tile width W; else the task's l */
     int32_t inverse;  /* 1 for dehierarchization */
-    int32_t reserved;
+    int32_t variant;  /* FUSED: 0 dense, 1 BLOCKED tiles, 2 coarse-lattice views, 3 both */
     double bytes;     /* algorithmic bytes (one read + one write per point) */
     double ms;        /* event-timed duration, -1 if unavailable */
 } sgh_launch_record;
 sgh_status sgh_profile_enable(int32_t on);
 int64_t sgh_profile_read(sgh_launch_record *out, int64_t capacity);
+
+/* Host-only description of the plan the library would run for one grid with
+ * these flags (no CUDA call): one line per pass ("pass k:"), then one line per
+ * phase with its kernel kind, tile width, special axis / block level and the
+ * points it writes.  Writes at most cap bytes (NUL-terminated) into buf (may be
+ * NULL) and returns the full length, or -1 on invalid levels / flags. */
+int64_t sgh_plan_describe(const int32_t *levels, int32_t d, uint32_t flags, char *buf, size_t cap);
 
 /* Number of kernels this library has launched in this process (all calls).
  * Used by bench.py to report gpu_launches. */

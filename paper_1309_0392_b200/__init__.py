@@ -35,6 +35,7 @@ LIB_PATH = os.environ.get("SGH_LIB_PATH") or os.path.join(_HERE, "lib", "libsgh.
 
 FLAG_DEHIERARCHIZE = 1
 FLAG_PER_AXIS = 2
+FLAG_WHOLE_POLES = 4
 STATUS = {0: "SGH_OK", 1: "SGH_ERR_INVALID_ARGUMENT", 2: "SGH_ERR_CAPACITY", 3: "SGH_ERR_CUDA",
           4: "SGH_ERR_NCCL", 5: "SGH_ERR_WORKSPACE"}
 
@@ -81,6 +82,7 @@ def _load():
         "sgh_digest": (st, [vp, ctypes.c_int64, ctypes.c_int64, u64p, vp]),
         "sgh_digest_batched": (st, [vpp, i64p, ctypes.c_int64, u64p, vp, sz, vp]),
         "sgh_launch_count": (ctypes.c_uint64, []),
+        "sgh_plan_describe": (ctypes.c_int64, [i32p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_char_p, sz]),
         "sgh_profile_enable": (st, [ctypes.c_int32]),
         "sgh_profile_read": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int64]),
         "sgh_status_string": (ctypes.c_char_p, [st]),
@@ -101,7 +103,7 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_comm_unique_id", "sgh_sharded_workspace_bytes", "sgh_hierarchize_sharded",
             "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
-            "sgh_profile_enable", "sgh_profile_read",
+            "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe",
             "sgh_status_string", "sgh_last_error", "sgh_version")
 
 
@@ -139,8 +141,30 @@ def num_points(levels: Sequence[int]) -> int:
     return int(lib.sgh_num_points(a, d))
 
 
-def _flags(inverse: bool, fuse: bool = True) -> int:
-    return (FLAG_DEHIERARCHIZE if inverse else 0) | (0 if fuse else FLAG_PER_AXIS)
+def _flags(inverse: bool, fuse=True) -> int:
+    """fuse: True (planner's choice, blocked groups allowed), "whole" (fused
+    groups of whole poles only) or False (one HBM round trip per axis)."""
+    if fuse == "whole":
+        f = FLAG_WHOLE_POLES
+    elif fuse is True:
+        f = 0
+    elif fuse is False:
+        f = FLAG_PER_AXIS
+    else:
+        raise ValueError(f"fuse must be True, False or 'whole', not {fuse!r}")
+    return (FLAG_DEHIERARCHIZE if inverse else 0) | f
+
+
+def plan_describe(levels: Sequence[int], inverse: bool = False, fuse=True) -> str:
+    """The library's plan for one grid (host-only, no CUDA call)."""
+    a, d = _levels_arr(levels)
+    fl = ctypes.c_uint32(_flags(inverse, fuse))
+    n = int(lib.sgh_plan_describe(a, d, fl, None, 0))
+    if n < 0:
+        raise ValueError(f"invalid levels {tuple(levels)}")
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.sgh_plan_describe(a, d, fl, buf, n + 1)
+    return buf.value.decode()
 
 
 def transform(grid: torch.Tensor, levels: Sequence[int], *, inverse: bool = False, axis_order=None,
@@ -202,7 +226,7 @@ def launch_count() -> int:
 
 class _LaunchRecord(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("level", ctypes.c_int32), ("inverse", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("bytes", ctypes.c_double), ("ms", ctypes.c_double)]
+                ("variant", ctypes.c_int32), ("bytes", ctypes.c_double), ("ms", ctypes.c_double)]
 
 
 KIND_NAMES = {0: "flat_slabs", 1: "flat_blocks", 2: "strided", 3: "reg", 4: "fused"}
@@ -222,7 +246,9 @@ def profile_read():
     out = []
     for r in buf[:n]:
         name = KIND_NAMES.get(r.kind, str(r.kind)) + (f"<{r.level}>" if r.kind in (2, 3, 4) else "")
-        out.append({"kernel": name, "level": r.level, "inverse": bool(r.inverse), "bytes": r.bytes, "ms": r.ms})
+        name += {1: "B", 2: "L", 3: "BL"}.get(r.variant, "")   # blocked tiles / lattice views
+        out.append({"kernel": name, "level": r.level, "inverse": bool(r.inverse), "bytes": r.bytes, "ms": r.ms,
+                    "variant": r.variant})
     return out
 
 

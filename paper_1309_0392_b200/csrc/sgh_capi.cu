@@ -173,6 +173,16 @@ static int fused_budget() {
   return T;
 }
 
+static int fused_wmax() {
+  static int wmax = -1;
+  if (wmax < 0) {
+    const char *e = getenv("SGH_FUSED_W");  // tuning experiment override (8..128)
+    wmax = e ? atoi(e) : 128;
+    if (wmax != 8 && wmax != 16 && wmax != 32 && wmax != 64 && wmax != 128) wmax = 128;
+  }
+  return wmax;
+}
+
 static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, int b, Task &t) {
   const int64_t kFusedT = fused_budget();
   int64_t Sa = 1, P = 1, O = 1;
@@ -187,6 +197,7 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
   std::memset(&t, 0, sizeof t);
   t.grid = grid;
   t.kind = KIND_FUSED;
+  t.bj = -1;
   t.m = b - a;
   t.P = (int32_t)std::min<int64_t>(P, INT32_MAX);
   int64_t R = 1;
@@ -214,15 +225,9 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
     t.tiles = (O + t.R - 1) / t.R;
     return true;
   }
-  static int wmax = -1;
-  if (wmax < 0) {
-    const char *e = getenv("SGH_FUSED_W");  // tuning experiment override (8..128)
-    wmax = e ? atoi(e) : 128;
-    if (wmax != 8 && wmax != 16 && wmax != 32 && wmax != 64 && wmax != 128) wmax = 128;
-  }
   // widest tile that fits: long contiguous row segments keep DRAM efficient
   int W = 8;
-  while (W < wmax && W < Sa) W <<= 1;
+  while (W < fused_wmax() && W < Sa) W <<= 1;
   while (W > 8 && P * (W + 1) > kFusedT + kFusedT / 16) W >>= 1;
   if (P * (W + 1) > kFusedT + kFusedT / 16) return false;
   t.W = W;
@@ -233,67 +238,215 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
   return true;
 }
 
-// Estimated time per byte (1 / TB/s) of a pass, from the kernels' measured
+// BLOCKED group [a, b) with special axis j (a <= j < b), column width W (1: the
+// group starts at a unit-stride axis).  The other axes of the group hold whole
+// poles; axis j is viewed as a pole of level lj at global stride Gj from
+// `base`.  While its whole poles do not fit a tile, the tile holds aligned
+// blocks of 2^bt points + their end points (the largest bt that fits) and
+// writes the blocks' fine points; the coarse lattice {i : 2^bt | i} of axis j
+// (level lj - bt, stride 2^bt Gj) is the next view.
+// Phases come out in hierarchization order (block tiles, then the lattice
+// views); dehierarchization runs them reversed, which requires that no axis
+// after j in the group is transformed (the block ends must be final values
+// when a block tile reads them).  Returns false if no block of >= 4 points fits.
+static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a, int b, int j, int W,
+                               std::vector<Task> &phases) {
+  const int64_t budget = fused_budget() + fused_budget() / 16;
+  if (b - a > 16 || b - a < 2 || levels[j] < 3) return false;
+  int64_t Sa = 1, O = 1, Prest = 1, A = 1;
+  for (int k = 0; k < a; ++k) Sa *= (int64_t(1) << levels[k]) - 1;
+  for (int k = b; k < d; ++k) O *= (int64_t(1) << levels[k]) - 1;
+  int busy = 0;
+  for (int k = a; k < b; ++k) {
+    const int64_t nk = (int64_t(1) << levels[k]) - 1;
+    busy += levels[k] > 1;
+    if (k == j) continue;
+    Prest *= nk;
+    if (k < j) A *= nk;
+  }
+  if (busy < 2) return false;
+  if ((W == 1) != (Sa == 1)) return false;
+  if (W > 1 && W > 2 * Sa && W > 8) return false;
+  const int64_t Wf = (W == 1) ? 1 : W + 1;
+  const int64_t nj = (int64_t(1) << levels[j]) - 1;
+  int64_t G = Sa;                                   // dense global stride of axis j
+  for (int k = a; k < j; ++k) G *= (int64_t(1) << levels[k]) - 1;
+  const int64_t Gnext = (j + 1 < b) ? G * nj : 0;
+  int lj = levels[j];
+  int64_t Gj = G, base = 0;
+  const size_t first = phases.size();
+  for (int step = 0;; ++step) {
+    const int64_t nlj = (int64_t(1) << lj) - 1;
+    int bt = lj;                                      // whole poles?
+    if (Prest * nlj * Wf > budget) {
+      bt = 0;
+      while (bt + 1 < lj && Prest * ((int64_t(1) << (bt + 1)) + 1) * Wf <= budget) ++bt;
+      if (bt < 2) {
+        phases.resize(first);
+        return false;
+      }
+    }
+    const bool blocked = bt < lj;
+    const int64_t ej = blocked ? (int64_t(1) << bt) + 1 : nlj;
+    Task t;
+    std::memset(&t, 0, sizeof t);
+    t.grid = grid;
+    t.kind = KIND_FUSED;
+    t.m = b - a;
+    int64_t R = 1;
+    for (int k = a; k < b; ++k) {
+      t.gl[k - a] = (int8_t)(k == j ? lj : levels[k]);
+      t.gR[k - a] = (int32_t)R;
+      t.fR[k - a] = make_fdiv((uint32_t)R);
+      R *= (k == j) ? ej : (int64_t(1) << levels[k]) - 1;
+    }
+    t.P = (int32_t)R;
+    t.S = Sa;
+    t.O = O;
+    t.OS = Prest * nj * Sa;                           // the group's dense extent
+    t.base = base;
+    t.l = levels[a];
+    t.W = W;
+    t.R = 1;
+    t.bj = j - a;
+    t.bt = blocked ? bt : lj;
+    t.nb_log = blocked ? lj - bt : 0;
+    t.A = (int32_t)A;
+    t.ej = (int32_t)ej;
+    t.fA = make_fdiv((uint32_t)A);
+    t.fE = make_fdiv((uint32_t)ej);
+    t.Gj = Gj;
+    t.Gnext = Gnext;
+    // 16-byte copies need the global 8-byte phase of every tile row (element)
+    // to follow the SMEM one: rows x + A (y + ej z) at x S + y Gj + z Gnext with
+    // S, A odd (products of odd extents) -> Gj odd and Gnext = ej (mod 2).
+    t.aligned = ((Gj & 1) == (A & 1)) && (Gnext == 0 || (Gnext & 1) == ((A * ej) & 1));
+    t.ncb = (W > 1) ? (Sa + W - 1) / W : 1;
+    t.tiles = (O << t.nb_log) * t.ncb;
+    if (lj <= 1 && busy - (levels[j] > 1) == 0) break;   // nothing left to transform
+    phases.push_back(t);
+    if (!blocked) break;
+    base += ((int64_t(1) << bt) - 1) * Gj;            // first lattice point i = 2^bt
+    Gj <<= bt;
+    lj -= bt;
+  }
+  return phases.size() > first;
+}
+
+// Estimated time per point (1 / TB/s) of a pass, from the kernels' measured
 // B200 throughput (profiles/r01): wide contiguous tiles stream best, narrow
 // column tiles lose DRAM efficiency.
+static double kind_bw(const Task &t) {
+  switch (t.kind) {
+    case KIND_FLAT_SLABS:
+    case KIND_FLAT_BLOCKS: return 5.6;
+    case KIND_REG: return 5.0;
+    case KIND_STRIDED: return t.W >= 128 ? 4.8 : (t.W >= 64 ? 4.6 : 3.9);
+    case KIND_FUSED: {
+      // contiguous run length of the tile's global segments (doubles)
+      int64_t run = t.W;
+      if (t.W == 1) {
+        run = 1 << 20;
+        if (t.bj >= 0) run = (t.Gj == t.A) ? int64_t(t.A) * t.ej : t.A;
+      }
+      double bw = run >= 256 ? 5.2 : run >= 128 ? 4.6 : run >= 64 ? 4.3 : run >= 32 ? 4.0 : run >= 16 ? 3.3 : 2.2;
+      // lattice views: 8-byte copies; single-element runs (a lattice of the
+      // contiguous axis) touch one 32-byte sector per point and write partial
+      // sectors (measured ~0.3 TB/s algorithmic on C3's (5,4,4) lattice)
+      if (t.bj >= 0 && !t.aligned) bw = std::min(bw, run <= 1 ? 0.35 : 1.5);
+      return bw;
+    }
+    default: return 4.0;
+  }
+}
+
 static double pass_cost(const std::vector<Task> &phases) {
   double c = 0;
   for (size_t i = 0; i < phases.size(); ++i) {
     const Task &t = phases[i];
-    double bw;
-    switch (t.kind) {
-      case KIND_FLAT_SLABS:
-      case KIND_FLAT_BLOCKS: bw = 5.6; break;
-      case KIND_REG: bw = 5.0; break;
-      case KIND_STRIDED: bw = t.W >= 128 ? 4.8 : (t.W >= 64 ? 4.6 : 3.9); break;
-      case KIND_FUSED:
-        bw = t.W == 1 ? 5.2 : t.W >= 128 ? 4.6 : t.W >= 64 ? 4.3 : t.W >= 32 ? 4.0 : t.W >= 16 ? 3.3 : 2.2;
-        break;
-      default: bw = 4.0;
+    const double bw = kind_bw(t);
+    if (i == 0) {
+      c += 1.0 / bw;
+    } else if (t.kind == KIND_FUSED) {
+      // a lattice view of a blocked group: its share of the points, plus a
+      // fixed per-phase cost (a few % of a pass: launch tail, small tiles)
+      c += task_points(t) / std::max(1.0, task_points(phases[0])) / (0.7 * bw) + 0.01;
+    } else {
+      // later phases are coarse lattices: a small fraction of the points, latency bound
+      c += 2.0 * task_points(t) / std::max(1.0, task_points(phases[0])) / 1.0;
     }
-    // later phases are coarse lattices: a small fraction of the points, latency bound
-    c += (i == 0) ? 1.0 / bw : 2.0 * task_points(t) / std::max(1.0, task_points(phases[0])) / 1.0;
   }
   return c;
 }
 
-// Passes of a whole grid (hierarchization order inside each pass).  With
-// `fuse`, a DP over consecutive axis groups picks the plan of least estimated
-// time: a group is either one axis (per-axis kernels) or a run of axes whose
-// whole poles fit one FUSED tile.  The axis order stays 1..d, so the
-// results are bitwise equal to the per-axis path.
-void plan_grid(double *grid, const int32_t *levels, int d, bool fuse, std::vector<std::vector<Task>> &passes) {
+// Passes of a whole grid (hierarchization order inside each pass).  Unless
+// SGH_FLAG_PER_AXIS, a DP over consecutive axis groups picks the plan of least
+// estimated time: a group is either one axis (per-axis kernels), a run of axes
+// whose whole poles fit one FUSED tile, or (unless SGH_FLAG_WHOLE_POLES) a run
+// with one BLOCKED axis.  The axis order stays 1..d, so the results are
+// bitwise equal to the per-axis path.
+void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::vector<std::vector<Task>> &passes) {
   passes.clear();
+  const bool fuse = (flags & SGH_FLAG_PER_AXIS) == 0;
+  const bool blocked_ok = fuse && (flags & SGH_FLAG_WHOLE_POLES) == 0 && getenv("SGH_NO_BLOCKED") == nullptr;
+  const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   const double kInf = 1e30;
   std::vector<double> cost(d + 1, kInf);
   std::vector<int> from(d + 1, -1);
+  std::vector<std::vector<Task>> best(d + 1);      // phases of the group ending at j (fused groups)
   cost[0] = 0;
   for (int i = 0; i < d; ++i) {
     if (cost[i] >= kInf) continue;
     std::vector<Task> ph;
     plan_axis(grid, levels, d, i, ph);
     const double c1 = cost[i] + (ph.empty() ? 0.0 : pass_cost(ph));
-    if (c1 < cost[i + 1]) { cost[i + 1] = c1; from[i + 1] = i; }
+    if (c1 < cost[i + 1]) {
+      cost[i + 1] = c1;
+      from[i + 1] = i;
+      best[i + 1].clear();
+    }
     if (!fuse) continue;
+    int64_t Sa = 1;
+    for (int k = 0; k < i; ++k) Sa *= (int64_t(1) << levels[k]) - 1;
     Task t;
     for (int j = i + 2; j <= d; ++j) {
-      if (!plan_fused_group(grid, levels, d, i, j, t)) continue;
-      const double cj = cost[i] + pass_cost(std::vector<Task>{t});
-      if (cj < cost[j] - 1e-12) { cost[j] = cj; from[j] = i; }
+      if (plan_fused_group(grid, levels, d, i, j, t)) {
+        const double cj = cost[i] + pass_cost(std::vector<Task>{t});
+        if (cj < cost[j] - 1e-12) {
+          cost[j] = cj;
+          from[j] = i;
+          best[j] = std::vector<Task>{t};
+        }
+        continue;                                  // whole poles fit: no blocking needed
+      }
+      if (!blocked_ok) continue;
+      for (int s = i; s < j; ++s) {
+        if (inv) {                                 // no transformed axis after the blocked one
+          bool later = false;
+          for (int k = s + 1; k < j; ++k) later |= levels[k] > 1;
+          if (later) continue;
+        }
+        for (int W = (Sa == 1 ? 1 : fused_wmax()); W >= (Sa == 1 ? 1 : 8); W >>= 1) {
+          std::vector<Task> bp;
+          if (!plan_blocked_group(grid, levels, d, i, j, s, W, bp)) continue;
+          const double cj = cost[i] + pass_cost(bp);
+          if (cj < cost[j] - 1e-12) {
+            cost[j] = cj;
+            from[j] = i;
+            best[j] = bp;
+          }
+        }
+      }
     }
   }
-  std::vector<std::pair<int, int>> groups;
-  for (int j = d; j > 0; j = from[j]) groups.push_back({from[j], j});
-  std::reverse(groups.begin(), groups.end());
-  for (auto &g : groups) {
+  std::vector<int> ends;
+  for (int j = d; j > 0; j = from[j]) ends.push_back(j);
+  std::reverse(ends.begin(), ends.end());
+  for (int j : ends) {
+    const int i = from[j];
     std::vector<Task> phases;
-    if (g.second - g.first == 1) {
-      plan_axis(grid, levels, d, g.first, phases);
-    } else {
-      Task t;
-      plan_fused_group(grid, levels, d, g.first, g.second, t);
-      phases.push_back(t);
-    }
+    if (j - i == 1 && best[j].empty()) plan_axis(grid, levels, d, i, phases);
+    else phases = best[j];
     if (!phases.empty()) passes.push_back(std::move(phases));
   }
 }
@@ -382,12 +535,12 @@ static sgh_status transform_single(double *grid, const int32_t *levels, int32_t 
   const bool all_axes = (axis_mask == 0) || ((axis_mask & ((d >= 32) ? 0xffffffffu : ((1u << d) - 1))) ==
                                              ((d >= 32) ? 0xffffffffu : ((1u << d) - 1)));
   if (axis_mask == 0) axis_mask = 0xffffffffu;
-  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS)) return invalid("unknown flags");
+  if (flags & ~kKnownFlags) return invalid("unknown flags");
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!axis_order && all_axes) {
     std::vector<std::vector<Task>> passes;
-    plan_grid(grid, levels, d, (flags & SGH_FLAG_PER_AXIS) == 0, passes);
+    plan_grid(grid, levels, d, flags, passes);
     for (auto &phases : passes) {
       if (inv) std::reverse(phases.begin(), phases.end());   // coarse lattice first (H2)
       for (const Task &t : phases) {
@@ -423,6 +576,7 @@ struct Segment {
   int64_t tiles;
   size_t smem;        // max dynamic shared memory over the segment's tasks
   double points;      // points the segment transforms (profiling)
+  int variant;        // task_variant of its tasks (3: mixed blocked / lattice)
 };
 
 struct BatchedPlan {
@@ -434,12 +588,13 @@ struct BatchedPlan {
   }
 };
 
-static void build_batched_plan(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv,
-                               BatchedPlan &P, bool fuse = true) {
+static void build_batched_plan(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
+                               uint32_t flags, BatchedPlan &P) {
+  const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   std::vector<std::vector<std::vector<Task>>> all(num_grids);
   size_t rounds = 0;
   for (int64_t g = 0; g < num_grids; ++g) {
-    plan_grid(grids ? grids[g] : nullptr, levels + g * d, d, fuse, all[g]);
+    plan_grid(grids ? grids[g] : nullptr, levels + g * d, d, flags, all[g]);
     rounds = std::max(rounds, all[g].size());
   }
   std::vector<std::vector<Task>> per(num_grids);
@@ -471,7 +626,10 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
         int64_t acc = 0;
         sg.smem = 0;
         sg.points = 0;
+        sg.variant = -1;
         for (const Task *t : kv.second) {
+          const int v = task_variant(*t);
+          sg.variant = (sg.variant < 0 || sg.variant == v) ? v : 3;
           sg.smem = std::max(sg.smem, task_smem(*t));
           sg.points += task_points(*t);
           P.tasks.push_back(*t);
@@ -486,10 +644,10 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
   }
 }
 
-size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv,
-                           bool fuse) {
+size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
+                           uint32_t flags) {
   BatchedPlan P;
-  build_batched_plan(grids, levels, d, num_grids, inv, P, fuse);
+  build_batched_plan(grids, levels, d, num_grids, flags, P);
   return P.segs.empty() ? 0 : P.table_bytes();
 }
 
@@ -509,13 +667,13 @@ static sgh_status validate_batch(double *const *grids, const int32_t *levels, in
 
 sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
                               uint32_t flags, void *workspace, size_t ws_bytes, cudaStream_t s) {
-  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS)) return invalid("unknown flags");
+  if (flags & ~kKnownFlags) return invalid("unknown flags");
   sgh_status st = validate_batch(grids, levels, d, num_grids, true);
   if (st != SGH_OK) return st;
   if (num_grids == 0) return SGH_OK;
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   BatchedPlan P;
-  build_batched_plan(grids, levels, d, num_grids, inv, P, (flags & SGH_FLAG_PER_AXIS) == 0);
+  build_batched_plan(grids, levels, d, num_grids, flags, P);
   if (P.segs.empty()) return SGH_OK;
   const size_t bytes = P.table_bytes();
   if (!workspace || ws_bytes < bytes || (reinterpret_cast<uintptr_t>(workspace) & 15)) {
@@ -532,7 +690,7 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
   const int64_t *d_prefix = reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + prefix_base);
   for (const Segment &sg : P.segs) {
     cudaError_t e = launch_table(sg.kind, sg.l, sg.w, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off, sg.ntasks,
-                                 sg.tiles, sg.smem, sg.points, s);
+                                 sg.tiles, sg.smem, sg.points, s, sg.variant);
     if (e != cudaSuccess) return cuda_fail(e, "grouped kernel launch");
     count_launch();
   }
@@ -571,8 +729,7 @@ sgh_status sgh_transform_ex(double *grid, const int32_t *levels, int32_t d, cons
 size_t sgh_batched_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
   if (validate_batch(nullptr, levels, d, num_grids, false) != SGH_OK || num_grids == 0) return 0;
   BatchedPlan P;
-  build_batched_plan(nullptr, levels, d, num_grids, (flags & SGH_FLAG_DEHIERARCHIZE) != 0, P,
-                     (flags & SGH_FLAG_PER_AXIS) == 0);
+  build_batched_plan(nullptr, levels, d, num_grids, flags, P);
   return P.table_bytes();
 }
 
@@ -709,6 +866,37 @@ sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize(digests)");
   return SGH_OK;
+}
+
+int64_t sgh_plan_describe(const int32_t *levels, int32_t d, uint32_t flags, char *buf, size_t cap) {
+  if (validate_levels(levels, d, nullptr) != SGH_OK || (flags & ~kKnownFlags)) return -1;
+  std::vector<std::vector<Task>> passes;
+  plan_grid(nullptr, levels, d, flags, passes);
+  static const char *names[] = {"FLAT_SLABS", "FLAT_BLOCKS", "STRIDED", "REG", "FUSED"};
+  std::string out;
+  char line[256];
+  for (size_t k = 0; k < passes.size(); ++k) {
+    std::snprintf(line, sizeof line, "pass %zu:\n", k);
+    out += line;
+    for (const Task &t : passes[k]) {
+      if (t.kind == KIND_FUSED) {
+        std::string lv;
+        for (int j = 0; j < t.m; ++j) lv += (j ? "," : "") + std::to_string(int(t.gl[j]));
+        std::snprintf(line, sizeof line, "  FUSED W=%d levels=(%s) special=%d bt=%d aligned=%d points=%.0f\n", t.W,
+                      lv.c_str(), t.bj, t.bj >= 0 ? t.bt : -1, t.bj >= 0 ? t.aligned : 1, task_points(t));
+      } else {
+        std::snprintf(line, sizeof line, "  %s l=%d t=%d W=%d points=%.0f\n", names[t.kind], t.l, t.t, t.W,
+                      task_points(t));
+      }
+      out += line;
+    }
+  }
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, out.size());
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)out.size();
 }
 
 uint64_t sgh_launch_count(void) { return g_launches.load(); }

@@ -81,10 +81,27 @@ struct Task {
   //           base + o*OS + row*S + cb*W + c, ncb column groups.
   // Inside a unit, axis j of the group has row stride gR[j] = prod_{i<j} n_i.
   int32_t m;          // axes in the group
-  int32_t P;          // rows per unit = prod of the group's n_k
+  int32_t P;          // rows per unit = prod of the group's local extents
   int8_t gl[16];      // the group's levels
   int32_t gR[16];     // row strides
   FDiv fR[16];        // division by gR[j]
+  // FUSED with a SPECIAL axis bj (bj < 0: none, the group is dense).  The
+  // special axis either is BLOCKED (bt < gl[bj]: the tile holds an aligned
+  // block of 2^bt points plus its two end points, local y = 0..2^bt at
+  // 0-based pole index b 2^bt - 1 + y, and writes only the block's fine points
+  // y = 1..2^bt-1) or is a coarse LATTICE (bt >= gl[bj]:
+  // whole poles, but with a global stride Gj other than the dense one).  The
+  // group axes before bj are dense (row stride S), the ones after it are dense
+  // among themselves (the first at stride Gnext).  A tile row r_local =
+  // x + A (y + ej z) sits at global offset x S + y Gj + z Gnext.
+  int32_t bj;         // special axis (index in the group), -1: none
+  int32_t bt;         // its block level (>= gl[bj]: not blocked)
+  int32_t nb_log;     // log2(blocks per pole) (0 if not blocked)
+  int32_t A;          // tile rows before the special axis (= gR[bj])
+  int32_t ej;         // local extent of the special axis (2^bt + 1, or n)
+  int32_t aligned;    // 1: global and SMEM 8-byte phases agree row by row (16-byte copies)
+  int64_t Gj, Gnext;  // global strides (elements) of the special axis and of the next group axis
+  FDiv fA, fE;        // division by A, by ej
 };
 
 static_assert(sizeof(Task) % 8 == 0, "Task must stay 8-byte aligned");

@@ -27,7 +27,7 @@ struct HostLayout {
   size_t total = 0;
 };
 
-static sgh_status host_layout(const int32_t *levels, int32_t d, int64_t num_grids, bool inv, bool fuse, HostLayout &L) {
+static sgh_status host_layout(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags, HostLayout &L) {
   L.grid_off.resize(num_grids);
   size_t off = 0;
   size_t acc = 0;
@@ -48,7 +48,7 @@ static sgh_status host_layout(const int32_t *levels, int32_t d, int64_t num_grid
   }
   for (auto &c : L.chunks) {
     L.table_off.push_back(off);
-    const size_t tb = batched_table_bytes(nullptr, levels + c.first * d, d, c.second - c.first, inv, fuse);
+    const size_t tb = batched_table_bytes(nullptr, levels + c.first * d, d, c.second - c.first, flags);
     off += (tb + 255) / 256 * 256;
   }
   L.total = off;
@@ -84,8 +84,7 @@ extern "C" {
 size_t sgh_batched_host_buffer_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
   if (!levels || num_grids <= 0) return 0;
   HostLayout L;
-  if (host_layout(levels, d, num_grids, (flags & SGH_FLAG_DEHIERARCHIZE) != 0, (flags & SGH_FLAG_PER_AXIS) == 0,
-                  L) != SGH_OK)
+  if (host_layout(levels, d, num_grids, flags, L) != SGH_OK)
     return 0;
   return L.total;
 }
@@ -93,7 +92,7 @@ size_t sgh_batched_host_buffer_bytes(const int32_t *levels, int32_t d, int64_t n
 sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *levels, int32_t d,
                                       int64_t num_grids, uint32_t flags, void *device_buffer,
                                       size_t device_buffer_bytes, void *stream) {
-  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS)) return invalid("unknown flags");
+  if (flags & ~kKnownFlags) return invalid("unknown flags");
   if (num_grids < 0) return invalid("num_grids < 0");
   if (num_grids == 0) return SGH_OK;
   if (!host_grids || !levels) return invalid("NULL argument");
@@ -101,7 +100,7 @@ sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *
     if (!host_grids[g]) return invalid("host_grids[g] is NULL");
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   HostLayout L;
-  sgh_status st = host_layout(levels, d, num_grids, inv, (flags & SGH_FLAG_PER_AXIS) == 0, L);
+  sgh_status st = host_layout(levels, d, num_grids, flags, L);
   if (st != SGH_OK) return st;
   if (!device_buffer || device_buffer_bytes < L.total || (reinterpret_cast<uintptr_t>(device_buffer) & 255)) {
     set_error("device_buffer missing, misaligned or smaller than sgh_batched_host_buffer_bytes()");

@@ -78,10 +78,25 @@ __device__ __forceinline__ void copy_range_async(double *sdst, const double *gsr
 }
 
 // Task index owning tile q.  `idx` is the cursor from the previous tile of this
-// CTA (tiles only increase), so the scan is amortised O(1).
+// CTA (tiles only increase).  A CTA's tiles are gridDim.x apart, which can skip
+// hundreds of small tasks (the C5 set: thousands of grids with a few tiles
+// each), so the search gallops from the cursor (1, 2, 4, .. tasks ahead) and
+// then bisects: O(log gap) dependent loads instead of O(gap).
 __device__ __forceinline__ int advance_task(const Src &src, int idx, int64_t q) {
-  while (idx + 1 < src.ntasks && __ldg(&src.prefix[idx + 1]) <= q) ++idx;
-  return idx;
+  if (idx + 1 >= src.ntasks || __ldg(&src.prefix[idx + 1]) > q) return idx;
+  int lo = idx + 1, step = 1;                      // prefix[lo] <= q
+  int hi = lo + 1;
+  while (hi < src.ntasks && __ldg(&src.prefix[hi]) <= q) {
+    lo = hi;
+    step <<= 1;
+    hi = lo + step;
+  }
+  if (hi > src.ntasks) hi = src.ntasks;            // answer in [lo, hi): prefix[hi] > q or hi == ntasks
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(&src.prefix[mid]) <= q) lo = mid; else hi = mid;
+  }
+  return lo;
 }
 
 __device__ __forceinline__ int first_task(const Src &src, int64_t q) {
@@ -373,15 +388,6 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
 // Per axis, when the tile holds enough poles, each thread owns whole poles and
 // runs the levels serially in SMEM (no division per point, no barrier inside
 // the axis); otherwise all threads sweep one level at a time (barrier per level).
-__device__ __forceinline__ FDiv device_fdiv(uint32_t d) {
-  FDiv f;
-  f.d = d;
-  uint32_t s = 0;
-  while (s < 32 && (1ull << s) < d) ++s;
-  f.s = s;
-  f.m = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
-  return f;
-}
 
 // rows 0..P-1 of W columns (wc valid), global row r at g + r*S (S odd), SMEM row r at sb + r*(W+1).
 // Lane = (sub-row, 16-byte slot): one warp instruction covers 32/(W/2) rows.
@@ -467,96 +473,54 @@ __device__ __forceinline__ void pole_regs(double *p, int STR) {
   }
 }
 
-// Alg. 1 on one longer pole (5 <= L <= 7) in registers, by the block + coarse
-// lattice decomposition of SURVEY 8(a) a3.iii applied inside one thread:
-// points with tz(i) < 3 have both predecessors in their aligned 8-point block
-// [8b, 8b+8], so each block is transformed from 9 registers; the coarse points
-// {8j} form a level-(L-3) pole (stride 8) done by pole_regs.  Hierarchization:
-// blocks first (they read the unmodified coarse ends), then the lattice;
-// dehierarchization: lattice first, then the blocks coarse -> fine.  Same
-// per-point operations as Alg. 1, so bitwise identical.
-template <int L, bool INV>
-__device__ __forceinline__ void pole_blocked(double *p, int STR) {
-  constexpr int T = 3;
+// Fine part of one aligned block of 2^T points of a pole together with its two
+// end points: local point r = 0..2^T at p0[r*STR].  Every
+// r = 1..2^T-1 has both predecessors r -+ 2^{tz(r)} inside [0, 2^T], so the
+// block is transformed from 2^T + 1 registers: hierarchization from the values
+// entering the pass (one-pass stencil), dehierarchization coarse -> fine with
+// nodal ends.  An end with !lo_ok / !hi_ok is the zero boundary: it is
+// never read and the update that would use it is skipped -- the same
+// operations as Alg. 1 on the whole pole, hence bitwise identical.
+template <int T, bool INV>
+__device__ __forceinline__ void block_fine(double *p0, int STR, bool lo_ok, bool hi_ok) {
   constexpr int B = 1 << T;
-  constexpr int n = (1 << L) - 1;
-  constexpr int nb = 1 << (L - T);
-  if (INV) pole_regs<L - T, true>(p + (B - 1) * STR, B * STR);
+  double v[B + 1];
+  v[0] = lo_ok ? p0[0] : 0.0;
 #pragma unroll
-  for (int b = 0; b < nb; ++b) {
-    double v[B + 1];
-#pragma unroll
-    for (int r = 0; r <= B; ++r) {
-      const int i = b * B + r;
-      v[r] = (i >= 1 && i <= n) ? p[(i - 1) * STR] : 0.0;   // i = 0 / 2^L: boundary, never used
-    }
-    if (!INV) {
-#pragma unroll
-      for (int r = 1; r < B; ++r) {
-        const int i = b * B + r;
-        const int s = r & -r;
-        double x = v[r];
-        if (i - s >= 1) x = x - 0.5 * v[r - s];
-        if (i + s <= n) x = x - 0.5 * v[r + s];
-        p[(i - 1) * STR] = x;
-      }
-    } else {
-#pragma unroll
-      for (int s = B / 2; s >= 1; s >>= 1) {
-#pragma unroll
-        for (int r = s; r < B; r += 2 * s) {
-          const int i = b * B + r;
-          double x = v[r];
-          if (i - s >= 1) x = x + 0.5 * v[r - s];
-          if (i + s <= n) x = x + 0.5 * v[r + s];
-          v[r] = x;
-        }
-      }
-#pragma unroll
-      for (int r = 1; r < B; ++r) p[(b * B + r - 1) * STR] = v[r];
-    }
-  }
-  if (!INV) pole_regs<L - T, false>(p + (B - 1) * STR, B * STR);
-}
-
-// One aligned 8-point block of a (lattice) pole held in 9 registers.  p0 is the
-// address of the virtual point j = 0 of the lattice (never dereferenced), point
-// j at p0[j*STR]; the lattice has nblk blocks, i.e. n = 8*nblk - 1 points.
-// Writes only the block's fine points j = 8b+1 .. 8b+7 (a3.iii).
-template <bool INV>
-__device__ __forceinline__ void block8(double *p0, int STR, int b, int nblk) {
-  double v[9];
-  const int n = 8 * nblk - 1;
-#pragma unroll
-  for (int r = 0; r <= 8; ++r) {
-    const int j = 8 * b + r;
-    v[r] = (j >= 1 && j <= n) ? p0[j * STR] : 0.0;
-  }
+  for (int r = 1; r < B; ++r) v[r] = p0[r * STR];
+  v[B] = hi_ok ? p0[B * STR] : 0.0;
   if (!INV) {
 #pragma unroll
-    for (int r = 1; r < 8; ++r) {
+    for (int r = 1; r < B; ++r) {
       const int s = r & -r;
-      const int j = 8 * b + r;
       double x = v[r];
-      if (j - s >= 1) x = x - 0.5 * v[r - s];    // left predecessor
-      if (j + s <= n) x = x - 0.5 * v[r + s];    // right predecessor
-      p0[j * STR] = x;
+      if (r - s > 0 || lo_ok) x = x - 0.5 * v[r - s];   // left predecessor
+      if (r + s < B || hi_ok) x = x - 0.5 * v[r + s];   // right predecessor
+      p0[r * STR] = x;
     }
   } else {
 #pragma unroll
-    for (int s = 4; s >= 1; s >>= 1) {
+    for (int s = B / 2; s >= 1; s >>= 1) {               // coarse -> fine (reading R9)
 #pragma unroll
-      for (int r = s; r < 8; r += 2 * s) {
-        const int j = 8 * b + r;
+      for (int r = s; r < B; r += 2 * s) {
         double x = v[r];
-        if (j - s >= 1) x = x + 0.5 * v[r - s];
-        if (j + s <= n) x = x + 0.5 * v[r + s];
+        if (r - s > 0 || lo_ok) x = x + 0.5 * v[r - s];
+        if (r + s < B || hi_ok) x = x + 0.5 * v[r + s];
         v[r] = x;
       }
     }
 #pragma unroll
-    for (int r = 1; r < 8; ++r) p0[(8 * b + r) * STR] = v[r];
+    for (int r = 1; r < B; ++r) p0[r * STR] = v[r];
   }
+}
+
+// One aligned 8-point block b of a (lattice) pole of nblk blocks: p0 is the
+// address of the virtual point j = 0 of the lattice (never dereferenced), point
+// j at p0[j*STR], n = 8*nblk - 1 points; its ends are the boundary only for the
+// first / last block.  Writes only the block's fine points j = 8b+1 .. 8b+7.
+template <bool INV>
+__device__ __forceinline__ void block8(double *p0, int STR, int b, int nblk) {
+  block_fine<3, INV>(p0 + 8 * b * STR, STR, b > 0, b < nblk - 1);
 }
 
 template <bool INV>
@@ -569,6 +533,43 @@ __device__ __forceinline__ void pole_regs_rt(double *p, int L, int STR) {
   }
 }
 
+// Thread-strided walk over work items it = b * npoles + p (p fastest) without a
+// division per item: (b, p) advance by (kThreads / npoles, kThreads % npoles).
+struct ItemWalk {
+  int np, db, dp, b0, p0;
+  __device__ __forceinline__ explicit ItemWalk(int npoles, int start = (int)threadIdx.x, int step = kThreads)
+      : np(npoles) {
+    db = step / npoles;
+    dp = step - db * npoles;
+    b0 = start / npoles;
+    p0 = start - b0 * npoles;
+  }
+  __device__ __forceinline__ void next(int &b, int &p) const {
+    b += db;
+    p += dp;
+    if (p >= np) {
+      p -= np;
+      ++b;
+    }
+  }
+};
+
+// Dehierarchization of a tile with a BLOCKED axis: a pole of an axis before the
+// blocked one lies in one local row y of the blocked axis.  The end rows
+// y = 0 and y = 2^bt hold values that are already final (their coarse lattice
+// ran first) and must not be transformed again.
+struct HaloSkip {
+  bool on;
+  FDiv fA, fE;  // division by A (tile rows before the blocked axis), by ej
+  int ej;
+  __device__ __forceinline__ bool skip(int row) const {  // row: the pole's first local row
+    if (!on) return false;
+    const uint32_t q = fdiv((uint32_t)row, fA);
+    const int y = (int)(q - fdiv(q, fE) * (uint32_t)ej);
+    return y == 0 || y == ej - 1;
+  }
+};
+
 // One axis of a staged tile, all npoles poles of level l (pole p = (oo, rk, c)
 // at sm + (oo*n*R + rk)*RS + c, point stride R*RS), in parallel work items:
 // l <= 4: one register pole per thread; l >= 5: (pole, 8-block) items on the
@@ -576,20 +577,24 @@ __device__ __forceinline__ void pole_regs_rt(double *p, int L, int STR) {
 // the lattice has l' <= 4, done as register poles.  A barrier between lattice
 // levels; hierarchization runs fine -> coarse, dehierarchization the reverse.
 template <bool INV, int W>
-__device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv &fR, int Ok) {
+__device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv fR, int Ok,
+                                           const HaloSkip hs) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   const int n = (1 << l) - 1;
   const int npoles = Ok * R * W;
   const int STR = R * RS;
-  auto pole_base = [&](int p) -> double * {
-    const int c = p & (W - 1);
+  auto pole_row = [&](int p) -> int {
     const int rest = p >> LOGW;
     const int oo = (int)fdiv((uint32_t)rest, fR);
     const int rk = rest - oo * R;
-    return sm + (oo * n * R + rk) * RS + c;
+    return oo * n * R + rk;
   };
+  auto pole_base = [&](int p) -> double * { return sm + pole_row(p) * RS + (p & (W - 1)); };
   if (l <= 4) {
-    for (int p = threadIdx.x; p < npoles; p += kThreads) pole_regs_rt<INV>(pole_base(p), l, STR);
+    for (int p = threadIdx.x; p < npoles; p += kThreads) {
+      if (hs.on && hs.skip(pole_row(p))) continue;
+      pole_regs_rt<INV>(pole_base(p), l, STR);
+    }
     __syncthreads();
     return;
   }
@@ -599,14 +604,13 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
     levels[nlev++] = lf;
     lf -= 3;
   }
-  const FDiv fP = device_fdiv((uint32_t)npoles);
+  const ItemWalk walk(npoles);
   auto block_phase = [&](int k) {                // k-th lattice level: stride 8^k
     const int m = 1 << (3 * k);
     const int nblk = 1 << (levels[k] - 3);
-    const int items = npoles * nblk;
-    for (int it = threadIdx.x; it < items; it += kThreads) {
-      const int b = (int)fdiv((uint32_t)it, fP);
-      const int p = it - b * npoles;             // lanes run over poles: conflict-free SMEM
+    // items (b, p), p fastest: lanes run over poles (conflict-free SMEM)
+    for (int b = walk.b0, p = walk.p0; b < nblk; walk.next(b, p)) {
+      if (hs.on && hs.skip(pole_row(p))) continue;
       block8<INV>(pole_base(p) - STR, m * STR, b, nblk);
     }
     __syncthreads();
@@ -614,6 +618,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   auto lattice_phase = [&]() {
     const int m = 1 << (3 * nlev);
     for (int p = threadIdx.x; p < npoles; p += kThreads) {
+      if (hs.on && hs.skip(pole_row(p))) continue;
       double *p0 = pole_base(p) - STR;           // virtual point 0
       pole_regs_rt<INV>(p0 + m * STR, lf, m * STR);
     }
@@ -628,63 +633,265 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   }
 }
 
-// Alg. 1 on one pole of n = 2^l - 1 points at p[0], p[STR], ... (serial)
-template <bool INV>
-__device__ __forceinline__ void pole_serial(double *p, int l, int STR) {
-  const int n = (1 << l) - 1;
+// The BLOCKED axis of a tile: every pole holds one aligned block of 2^t points
+// plus its two ends (local y = 0..2^t, point stride R*RS); only the fine points
+// y = 1..2^t-1 are transformed.  Inside the block the same
+// lattice recursion as fused_axis: 8-point sub-blocks at strides 1, 8, ..,
+// 8^{K-1} (K = t/3), then the top lattice of 2^{t-3K} + 1 points at stride 8^K.
+// lo_ok / hi_ok: the block's ends are grid points (false: the zero boundary).
+template <bool INV, int W>
+__device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int R, const FDiv fR, int Ok,
+                                                 bool lo_ok, bool hi_ok) {
+  constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
+  const int ej = (1 << t) + 1;
+  const int npoles = Ok * R * W;
+  const int STR = R * RS;
+  auto pole_base = [&](int p) -> double * {
+    const int c = p & (W - 1);
+    const int rest = p >> LOGW;
+    const int oo = (int)fdiv((uint32_t)rest, fR);
+    const int rk = rest - oo * R;
+    return sm + (oo * ej * R + rk) * RS + c;     // local point y = 0
+  };
+  const int K = t / 3;
+  const int tr = t - 3 * K;
+  const ItemWalk walk(npoles);
+  auto sub_phase = [&](int k) {
+    const int m = 1 << (3 * k);
+    const int nblk = 1 << (t - 3 * k - 3);
+    for (int b = walk.b0, p = walk.p0; b < nblk; walk.next(b, p))
+      block_fine<3, INV>(pole_base(p) + 8 * b * m * STR, m * STR, lo_ok || b > 0, hi_ok || b < nblk - 1);
+    __syncthreads();
+  };
+  auto top_phase = [&]() {
+    if (tr == 0) return;                         // the top lattice is just the two ends
+    const int m = 1 << (3 * K);
+    for (int p = threadIdx.x; p < npoles; p += kThreads) {
+      if (tr == 1) block_fine<1, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
+      else block_fine<2, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
+    }
+    __syncthreads();
+  };
   if (!INV) {
-    for (int s = 1; s < (1 << (l - 1)); s <<= 1) {        // levels l .. 2, finest first
-#pragma unroll 2
-      for (int i = s; i <= n; i += 2 * s) {
-        double x = p[(i - 1) * STR];
-        if (i - s >= 1) x = x - 0.5 * p[(i - s - 1) * STR];
-        if (i + s <= n) x = x - 0.5 * p[(i + s - 1) * STR];
-        p[(i - 1) * STR] = x;
-      }
-    }
+    for (int k = 0; k < K; ++k) sub_phase(k);
+    top_phase();
   } else {
-    for (int s = 1 << (l - 2); s >= 1; s >>= 1) {           // levels 2 .. l (reading R9)
-#pragma unroll 2
-      for (int i = s; i <= n; i += 2 * s) {
-        double x = p[(i - 1) * STR];
-        if (i - s >= 1) x = x + 0.5 * p[(i - s - 1) * STR];
-        if (i + s <= n) x = x + 0.5 * p[(i + s - 1) * STR];
-        p[(i - 1) * STR] = x;
-      }
-    }
+    top_phase();
+    for (int k = K - 1; k >= 0; --k) sub_phase(k);
   }
 }
 
 // geometry of one FUSED tile
 struct FusedTile {
-  double *g;   // global base: W == 1 start of the range; W > 1 row 0 at column c0
-  int units;   // W == 1: units in this tile
-  int wc;      // W > 1: valid columns
-  int par;     // 8-byte phase of g (SMEM data starts at stage + par)
+  double *g;      // global address of local row 0 (W > 1: at column c0); with a
+                  // blocked axis, local y = 0 of block 0 is virtual (never accessed)
+  int units;      // W == 1 dense: units in this tile
+  int wc;         // W > 1: valid columns
+  int par;        // 8-byte phase of the SMEM data start
+  int ylo, yhi;   // special axis: local rows that exist in the grid
+  bool lo_ok, hi_ok;  // blocked axis: the block's end points are grid points
 };
 
 template <int W>
 __device__ __forceinline__ FusedTile fused_tile(const Task &T, int64_t q) {
   FusedTile f;
-  if (W == 1) {
-    const int64_t u0 = q * T.R;
-    f.units = (int)min((int64_t)T.R, T.O - u0);
-    f.g = T.grid + T.base + u0 * T.P;
-    f.wc = 1;
-  } else {
-    const int64_t cb = q % T.ncb;
-    const int64_t o = q / T.ncb;
-    const int64_t c0 = cb * W;
-    f.units = 1;
-    f.wc = (int)min((int64_t)W, T.S - c0);
-    f.g = T.grid + T.base + o * T.OS + c0;        // (row r, col c) at g[r*S + c]
+  f.ylo = 0;
+  f.yhi = 0;
+  f.lo_ok = f.hi_ok = true;
+  if (T.bj < 0) {
+    if (W == 1) {
+      const int64_t u0 = q * T.R;
+      f.units = (int)min((int64_t)T.R, T.O - u0);
+      f.g = T.grid + T.base + u0 * T.P;
+      f.wc = 1;
+    } else {
+      const int64_t cb = q % T.ncb;
+      const int64_t o = q / T.ncb;
+      const int64_t c0 = cb * W;
+      f.units = 1;
+      f.wc = (int)min((int64_t)W, T.S - c0);
+      f.g = T.grid + T.base + o * T.OS + c0;        // (row r, col c) at g[r*S + c]
+    }
+    f.par = phase8(f.g);
+    return f;
   }
-  f.par = phase8(f.g);
+  const bool blocked = T.bt < T.gl[T.bj];
+  int64_t rest = q, c0 = 0;
+  if (W > 1) {
+    c0 = (q % T.ncb) * W;
+    rest = q / T.ncb;
+  }
+  const int b = (int)(rest & ((int64_t(1) << T.nb_log) - 1));
+  const int64_t o = rest >> T.nb_log;
+  const int64_t y0 = blocked ? (int64_t(b) << T.bt) - 1 : 0;   // 0-based pole index of local y = 0
+  f.g = T.grid + T.base + o * T.OS + c0 + y0 * T.Gj;
+  f.units = 1;
+  f.wc = (W > 1) ? (int)min((int64_t)W, T.S - c0) : 1;
+  f.lo_ok = !blocked || b > 0;
+  f.hi_ok = !blocked || b < (1 << T.nb_log) - 1;
+  f.ylo = f.lo_ok ? 0 : 1;
+  f.yhi = f.hi_ok ? T.ej - 1 : T.ej - 2;
+  f.par = T.aligned ? phase8(f.g) : 0;
   return f;
+}
+
+// W == 1 tile with a special axis: contiguous global runs (segments).  With a
+// dense special axis (Gj == A) a segment is rows y0..y1 of one z; otherwise one
+// row y of A elements.  Loads issue cp.async (16-byte pairs when the task's
+// phases agree), stores write the fine rows only.
+template <bool STORE>
+__device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f, double *sm) {
+  const int A = T.A, ej = T.ej;
+  const int nz = T.P / (A * ej);
+  const bool blocked = T.bt < T.gl[T.bj];
+  const int y0 = (STORE && blocked) ? 1 : f.ylo;
+  const int y1 = (STORE && blocked) ? ej - 2 : f.yhi;
+  const int ny = y1 - y0 + 1;
+  const int64_t Gj = T.Gj, Gn = T.Gnext;         // registers: the cp.async "memory" clobbers
+  const bool aligned = T.aligned != 0;              // would otherwise reload Task fields per run
+  double *const g0 = f.g;
+  const bool dense_y = (Gj == (int64_t)A);
+  const int len = dense_y ? ny * A : A;
+  const int nseg = dense_y ? nz : nz * ny;
+  const int nyw = dense_y ? 1 : ny;                // segment s = z * nyw + (y - y0)
+  auto seg_lo = [=](int z, int yy) { return (z * ej + y0 + yy) * A; };
+  auto seg_g = [=](int z, int yy) { return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)z * Gn; };
+  if (nseg < 16 && len >= 128) {                  // few long runs: the whole CTA on each
+    for (int z = 0; z < nseg / nyw; ++z)
+      for (int yy = 0; yy < nyw; ++yy) {
+        const int lo = seg_lo(z, yy);
+        double *gp = seg_g(z, yy);
+        if (STORE) {
+          for (int e = threadIdx.x; e < len; e += kThreads) __stcg(gp + e, sm[lo + e]);
+        } else if (aligned) {
+          copy_range_async(sm + lo, gp, len);
+        } else {
+          for (int e = threadIdx.x; e < len; e += kThreads) cp_async8(sm + lo + e, gp + e);
+        }
+      }
+    return;
+  }
+  // many runs: a group of L lanes per run (16-byte pairs + 8-byte head / tail),
+  // runs walked as (z, yy) without divisions
+  // L = lanes per run: enough for one 16-byte pair each (len/2 pairs at most);
+  // stores and 8-byte copies then take 2 elements per lane
+  const int half = len >> 1;
+  const int logL = half > 16 ? 5 : half > 8 ? 4 : half > 4 ? 3 : half > 2 ? 2 : len > 1 ? 1 : 0;
+  const int L = 1 << logL;
+  const int lane = threadIdx.x & (L - 1);
+  const ItemWalk walk(nyw, (int)threadIdx.x >> logL, kThreads >> logL);
+  if (!STORE && aligned && len > 1 && len <= 2 * L + 1) {   // straight-line: one 16-byte pair per lane
+    const int c0 = 2 * lane;
+    for (int z = walk.b0, yy = walk.p0; z < nz; walk.next(z, yy)) {
+      double *sp = sm + seg_lo(z, yy);
+      double *gp = seg_g(z, yy);
+      const int par = phase8(gp);
+      const int npairs = (len - par) >> 1;
+      const int last = par + 2 * npairs;
+      if (lane < npairs) cp_async16(sp + par + c0, gp + par + c0);
+      if (lane == L - 1 && par) cp_async8(sp, gp);
+      if (lane == L - 2 && last < len) cp_async8(sp + last, gp + last);
+    }
+    return;
+  }
+  for (int z = walk.b0, yy = walk.p0; z < nz; walk.next(z, yy)) {
+    double *sp = sm + seg_lo(z, yy);
+    double *gp = seg_g(z, yy);
+    if (STORE) {
+      for (int c = lane; c < len; c += L) __stcg(gp + c, sp[c]);
+    } else if (aligned) {
+      const int par = phase8(gp);
+      const int npairs = (len - par) >> 1;
+      const int last = par + 2 * npairs;
+      for (int k = lane; k < npairs; k += L) cp_async16(sp + par + 2 * k, gp + par + 2 * k);
+      if (lane == L - 1 && par) cp_async8(sp, gp);
+      if (lane == L - 2 && last < len) cp_async8(sp + last, gp + last);
+    } else {
+      for (int c = lane; c < len; c += L) cp_async8(sp + c, gp + c);
+    }
+  }
+}
+
+// W > 1 tile with a special axis: row r_local = x + A (y + ej z) of W columns at
+// global g + x S + y Gj + z Gnext; rows whose y lies outside the grid (load) or
+// on the block ends (store) are skipped.
+template <int W, bool STORE>
+__device__ __forceinline__ void fused_rows_special(const Task &T, const FusedTile &f, double *sm) {
+  constexpr int RS = W + 1;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const bool blocked = T.bt < T.gl[T.bj];
+  const int y0 = (STORE && blocked) ? 1 : f.ylo;
+  const int y1 = (STORE && blocked) ? T.ej - 2 : f.yhi;
+  const int P = T.P, A = T.A, ej = T.ej, wc = f.wc;
+  const int64_t S = T.S, Gj = T.Gj, Gn = T.Gnext;
+  const FDiv fA = T.fA, fE = T.fE;
+  const bool aligned = T.aligned != 0;
+  double *const g0 = f.g;
+  auto row_ptr = [=](int r, double *&gr) -> bool {
+    const uint32_t q = fdiv((uint32_t)r, fA);
+    const int x = r - (int)q * A;
+    const uint32_t z = fdiv(q, fE);
+    const int y = (int)(q - z * (uint32_t)ej);
+    gr = g0 + (int64_t)x * S + (int64_t)y * Gj + (int64_t)z * Gn;
+    return y >= y0 && y <= y1;
+  };
+  if (STORE) {
+    constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
+    constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
+    constexpr int STEP = RPI * (kThreads / 32);
+    const int c0 = (W >= 32) ? lane : lane % W;
+    for (int r = warp * RPI + ((W >= 32) ? 0 : lane / W); r < P; r += STEP) {
+      double *gr;
+      if (!row_ptr(r, gr)) continue;
+      const double *sr = sm + r * RS;
+#pragma unroll
+      for (int u = 0; u < CPL; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < wc) __stcg(gr + c, sr[c]);
+      }
+    }
+    return;
+  }
+  constexpr int NP = W / 2;                        // 16-byte slots per row
+  constexpr int RPI = (NP >= 32) ? 1 : 32 / NP;
+  constexpr int SPL = (NP >= 32) ? NP / 32 : 1;    // slots per lane
+  constexpr int STEP = RPI * (kThreads / 32);
+  const int k0 = (NP >= 32) ? lane : lane % NP;
+  for (int r = warp * RPI + ((NP >= 32) ? 0 : lane / NP); r < P; r += STEP) {
+    double *gr;
+    if (!row_ptr(r, gr)) continue;
+    double *sr = sm + r * RS;
+    if (aligned) {
+      const int par = phase8(gr);
+      const int npairs = (wc - par) >> 1;
+      const int last = par + 2 * npairs;
+#pragma unroll
+      for (int u = 0; u < SPL; ++u) {
+        const int k = k0 + 32 * u;
+        const int c = par + 2 * k;
+        if (k < npairs) cp_async16(sr + c, gr + c);
+        if (k == NP - 1 && par) cp_async8(sr, gr);
+        if (k == NP - 2 && last < wc) cp_async8(sr + last, gr + last);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < SPL; ++u) {
+        const int c = 2 * (k0 + 32 * u);
+        if (c < wc) cp_async8(sr + c, gr + c);
+        if (c + 1 < wc) cp_async8(sr + c + 1, gr + c + 1);
+      }
+    }
+  }
 }
 
 template <int W>
 __device__ __forceinline__ void fused_issue(const Task &T, const FusedTile &f, double *stage) {
+  if (T.bj >= 0) {
+    if (W == 1) fused_segments<false>(T, f, stage + f.par);
+    else fused_rows_special<(W == 1 ? 8 : W), false>(T, f, stage + f.par);
+    return;
+  }
   if (W == 1) copy_range_async(stage + f.par, f.g, f.units * T.P);
   else if (W >= 64) fused_load_rows_wide<(W >= 64 ? W : 64)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
   else fused_load_rows<(W == 1 || W >= 64 ? 8 : W)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
@@ -694,42 +901,58 @@ __device__ __forceinline__ void fused_issue(const Task &T, const FusedTile &f, d
 template <bool INV, int W>
 __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTile &f, double *sm) {
   constexpr int RS = (W == 1) ? 1 : W + 1;
-  constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   const int P = T.P;
   const int units = f.units, wc = f.wc;
   const int64_t S = T.S;
   double *gbase = f.g;
-    const int rows_total = units * P;
-    for (int j = 0; j < T.m; ++j) {                   // axes ascending
-      const int l = T.gl[j];
-      if (l <= 1) continue;
-      const int n = (1 << l) - 1;
-      const int R = T.gR[j];
-      const FDiv fR = T.fR[j];
-      const int Ok = rows_total / (n * R);
-      fused_axis<INV, W>(sm, RS, l, R, fR, Ok);
+  const int rows_total = units * P;
+  const bool blocked = T.bj >= 0 && T.bt < T.gl[T.bj];
+  HaloSkip hs;
+  hs.on = false;
+  if (blocked) {
+    hs.fA = T.fA;
+    hs.fE = T.fE;
+    hs.ej = T.ej;
+  }
+  for (int j = 0; j < T.m; ++j) {                   // axes ascending
+    const int l = T.gl[j];
+    if (l <= 1) continue;
+    const int R = T.gR[j];
+    const FDiv fR = T.fR[j];
+    if (blocked && j == T.bj) {
+      fused_axis_block<INV, W>(sm, RS, T.bt, R, fR, rows_total / (T.ej * R), f.lo_ok, f.hi_ok);
+      continue;
     }
-    if (W == 1) {
-      for (int e = threadIdx.x; e < rows_total; e += kThreads) __stcg(gbase + e, sm[e]);
-    } else {
-      constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
-      constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
-      constexpr int STEP = RPI * (kThreads / 32);
-      const int lane = threadIdx.x & 31;
-      const int c0 = (W >= 32) ? lane : lane % W;
-      int row = (threadIdx.x >> 5) * RPI + ((W >= 32) ? 0 : lane / W);
-      double *gr = gbase + (int64_t)row * S;
-      const double *sr = sm + row * RS;
-      const int64_t gstep = (int64_t)STEP * S;
+    const int n = (T.bj == j) ? T.ej : (1 << l) - 1;
+    hs.on = blocked && INV && j < T.bj;             // nodal block ends stay as loaded
+    fused_axis<INV, W>(sm, RS, l, R, fR, rows_total / (n * R), hs);
+  }
+  if (T.bj >= 0) {
+    if (W == 1) fused_segments<true>(T, f, sm);
+    else fused_rows_special<(W == 1 ? 8 : W), true>(T, f, sm);
+    return;
+  }
+  if (W == 1) {
+    for (int e = threadIdx.x; e < rows_total; e += kThreads) __stcg(gbase + e, sm[e]);
+  } else {
+    constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
+    constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
+    constexpr int STEP = RPI * (kThreads / 32);
+    const int lane = threadIdx.x & 31;
+    const int c0 = (W >= 32) ? lane : lane % W;
+    int row = (threadIdx.x >> 5) * RPI + ((W >= 32) ? 0 : lane / W);
+    double *gr = gbase + (int64_t)row * S;
+    const double *sr = sm + row * RS;
+    const int64_t gstep = (int64_t)STEP * S;
 #pragma unroll 2
-      for (; row < P; row += STEP, gr += gstep, sr += STEP * RS) {
+    for (; row < P; row += STEP, gr += gstep, sr += STEP * RS) {
 #pragma unroll
-        for (int u = 0; u < CPL; ++u) {
-          const int c = c0 + 32 * u;
-          if (c < wc) __stcg(gr + c, sr[c]);
-        }
+      for (int u = 0; u < CPL; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < wc) __stcg(gr + c, sr[c]);
       }
     }
+  }
 }
 
 // Persistent, double-buffered: while a CTA transforms tile k in one SMEM stage,
@@ -978,14 +1201,15 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
   fn<<<(unsigned)grid, kThreads, smem, stream>>>(src);
   cudaError_t e = cudaGetLastError();
   prof_end(tok, task.kind, task.kind == KIND_FUSED || task.kind == KIND_STRIDED ? task.W : task.l, inv,
-           16.0 * task_points(task), stream);
+           16.0 * task_points(task), stream, task_variant(task));
   return e;
 }
 
 // Launch a group of tasks of one kernel instance from a device task table;
 // smem = max task_smem over the group.
 cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
-                         int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream) {
+                         int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream,
+                         int variant) {
   KernelFn fn = kernel_for(kind, l, w, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
@@ -1003,7 +1227,7 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
   ProfToken tok = prof_begin(stream);
   fn<<<(unsigned)grid, kThreads, smem, stream>>>(src);
   cudaError_t e = cudaGetLastError();
-  prof_end(tok, kind, kind == KIND_FUSED || kind == KIND_STRIDED ? w : l, inv, 16.0 * points, stream);
+  prof_end(tok, kind, kind == KIND_FUSED || kind == KIND_STRIDED ? w : l, inv, 16.0 * points, stream, variant);
   return e;
 }
 

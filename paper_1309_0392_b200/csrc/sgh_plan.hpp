@@ -14,7 +14,8 @@ namespace sgh {
 // launchers (sgh_kernels.cu)
 cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream);
 cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
-                         int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream);
+                         int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream,
+                         int variant = 0);
 size_t task_smem(const Task &t);
 
 // per-launch profiling (sgh_profile.cu); a no-op unless sgh_profile_enable(1)
@@ -22,11 +23,24 @@ struct ProfToken {
   cudaEvent_t start;
 };
 ProfToken prof_begin(cudaStream_t s);
-void prof_end(ProfToken tok, int kind, int l, bool inv, double bytes, cudaStream_t s);
+// variant: 0 dense / per-axis, 1 BLOCKED fused tiles, 2 coarse-lattice views of a
+// blocked group, 3 a grouped launch mixing 1 and 2
+void prof_end(ProfToken tok, int kind, int l, bool inv, double bytes, cudaStream_t s, int variant = 0);
+inline int task_variant(const Task &t) {
+  if (t.kind != KIND_FUSED || t.bj < 0) return 0;
+  return t.bt < t.gl[t.bj] ? 1 : 2;
+}
 
 // points a task transforms (= writes): 16 B each is its algorithmic traffic
 inline double task_points(const Task &t) {
-  if (t.kind == KIND_FUSED) return double(t.O) * double(t.P) * double(t.S);   // every point, once
+  if (t.kind == KIND_FUSED) {
+    if (t.bj >= 0 && t.bt < t.gl[t.bj]) {           // blocked: the fine points of every block
+      const int lj = t.gl[t.bj];
+      const double fine = double((int64_t(1) << lj) - 1) - double((int64_t(1) << (lj - t.bt)) - 1);
+      return double(t.O) * double(t.S) * double(t.P / t.ej) * fine;
+    }
+    return double(t.O) * double(t.P) * double(t.S);   // every point, once
+  }
   const int64_t n = (int64_t(1) << t.l) - 1;
   const int64_t coarse = (t.t < t.l) ? (int64_t(1) << (t.l - t.t)) - 1 : 0;
   return double(t.O) * double(t.S) * double(n - coarse);
@@ -55,8 +69,10 @@ sgh_status staged_upload(void *dst, const void *src, size_t bytes, cudaStream_t 
 // batched driver: transform num_grids grids whose task tables go to `workspace`
 sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
                        uint32_t flags, void *workspace, size_t ws_bytes, cudaStream_t s);
-size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, bool inv,
-                           bool fuse = true);
-void plan_grid(double *grid, const int32_t *levels, int d, bool fuse, std::vector<std::vector<Task>> &passes);
+size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
+                           uint32_t flags);
+// flags: SGH_FLAG_DEHIERARCHIZE / SGH_FLAG_PER_AXIS / SGH_FLAG_WHOLE_POLES (sgh.h)
+void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::vector<std::vector<Task>> &passes);
+constexpr uint32_t kKnownFlags = SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS | SGH_FLAG_WHOLE_POLES;
 
 }  // namespace sgh

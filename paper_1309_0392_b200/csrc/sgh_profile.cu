@@ -16,7 +16,7 @@
 namespace sgh {
 
 struct ProfRec {
-  int kind, l, inv;
+  int kind, l, inv, variant;
   double bytes;
   cudaEvent_t a, b;
 };
@@ -45,12 +45,12 @@ ProfToken prof_begin(cudaStream_t s) {
   return ProfToken{a};
 }
 
-void prof_end(ProfToken tok, int kind, int l, bool inv, double bytes, cudaStream_t s) {
+void prof_end(ProfToken tok, int kind, int l, bool inv, double bytes, cudaStream_t s, int variant) {
   if (!tok.start) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t b = take_event();
   cudaEventRecord(b, s);
-  g_recs.push_back(ProfRec{kind, l, inv ? 1 : 0, bytes, tok.start, b});
+  g_recs.push_back(ProfRec{kind, l, inv ? 1 : 0, variant, bytes, tok.start, b});
 }
 
 }  // namespace sgh
@@ -81,7 +81,7 @@ int64_t sgh_profile_read(sgh_launch_record *out, int64_t capacity) {
     out[i].kind = r.kind;
     out[i].level = r.l;
     out[i].inverse = r.inv;
-    out[i].reserved = 0;
+    out[i].variant = r.variant;
     out[i].bytes = r.bytes;
     out[i].ms = ms;
   }

@@ -102,3 +102,47 @@ def test_no_cpu_fallback():
     import torch
     with pytest.raises(TypeError):
         sgh.hierarchize(torch.zeros(961, dtype=torch.float64), [5, 5])
+
+
+def _plan_passes(levels, **kw):
+    """Parse sgh_plan_describe: list of passes, each a list of (kind, attrs, points)."""
+    passes = []
+    for line in sgh.plan_describe(levels, **kw).splitlines():
+        if line.startswith("pass"):
+            passes.append([])
+            continue
+        kind = line.split()[0]
+        attrs = dict(kv.split("=", 1) for kv in line.split()[1:])
+        passes[-1].append((kind, attrs, float(attrs["points"])))
+    return passes
+
+
+@pytest.mark.parametrize("levels", [(8, 8, 8), (10, 4, 4, 4, 4), (16, 2, 2, 1), (2, 7, 11, 2), (9, 2, 8, 2),
+                                    (1, 3, 12), (14, 1, 3, 4), (5, 3, 3, 3)], ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_plan_blocked_groups_cover_each_point_once(levels, inverse):
+    """A fused pass (whole poles, or a BLOCKED group: block tiles + coarse-lattice
+    views) writes every point of the grid exactly once; a dehierarchization plan
+    never transforms a group axis after its blocked axis (the block ends must be
+    final values when a tile reads them)."""
+    N = si.num_points(levels)
+    for ph in _plan_passes(levels, inverse=inverse):
+        if ph[0][0] != "FUSED":
+            continue
+        assert sum(p for _, _, p in ph) == N
+        a = ph[0][1]
+        gl = [int(x) for x in a["levels"].strip("()").split(",")]
+        j, bt = int(a["special"]), int(a["bt"])
+        if j >= 0 and bt < gl[j] and inverse:
+            assert all(l == 1 for l in gl[j + 1:])
+
+
+def test_plan_c2_c3_use_blocked_fusion():
+    """C2 (8,8,8): x_1 whole rows x 2^5-row x_2 blocks in one round trip (+ its
+    7-row coarse lattice), then x_3 -- 2.03 HBM passes instead of 3."""
+    p = _plan_passes((8, 8, 8))
+    assert len(p) == 2 and p[0][0][0] == "FUSED" and p[0][0][1]["special"] == "1" and p[0][0][1]["bt"] == "5"
+    assert len(_plan_passes((8, 8, 8), fuse="whole")) == 3
+    assert len(_plan_passes((10, 4, 4, 4, 4))) == 2
+    assert all(len(ph) == 1 for ph in _plan_passes((8, 8, 8), fuse=False)[:1])
+    assert sgh.plan_describe((8, 8, 8), fuse=False).count("FUSED") == 0

@@ -70,10 +70,26 @@ SHAPES = [
     (7, 2, 3), (6, 3, 3), (8, 2, 2, 2), (9, 3, 2), (5, 1, 2, 2),
 ]
 
+# BLOCKED fused groups (one axis split into aligned 2^t blocks + end points, its
+# coarse lattice a later phase): chosen by scripts/blocked_cover.py so that the
+# planner's choices cover, for hierarchization and dehierarchization, contiguous
+# (W=1) and column (W>1) tiles, the blocked axis first / in the middle / last in
+# its group, block levels t = 0, 1, 2 (mod 3) (every top-lattice variant), the
+# coarse-lattice views with 16- and 8-byte copies, and multi-step lattice chains.
+BLOCKED_SHAPES = [
+    (1, 2, 14, 1), (1, 3, 12), (1, 6, 2, 10), (1, 7, 13, 1), (1, 10, 8, 3), (1, 11, 2, 6), (2, 1, 11, 7),
+    (2, 2, 4, 6), (2, 7, 11, 2), (2, 9, 4, 7), (3, 1, 6, 12), (3, 7, 7, 4), (4, 4, 1, 12), (4, 6, 2, 2),
+    (5, 1, 2, 14), (5, 3, 3, 3), (7, 3, 5, 1), (7, 3, 5, 5), (8, 11, 1, 2), (9, 1, 2, 9), (9, 1, 9, 3),
+    (9, 2, 8, 2), (9, 2, 10, 1), (9, 10, 1, 1), (10, 2, 5, 4), (11, 4, 2, 5), (11, 6, 2), (12, 4, 5),
+    (14, 1, 3, 4), (8, 8, 8),
+]
+FUSE_MODES = [True, "whole", False]
+FUSE_IDS = ["fused", "whole", "per_axis"]
 
-@pytest.mark.parametrize("levels", SHAPES, ids=str)
+
+@pytest.mark.parametrize("levels", SHAPES + BLOCKED_SHAPES, ids=str)
 @pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
-@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "per_axis"])
+@pytest.mark.parametrize("fuse", FUSE_MODES, ids=FUSE_IDS)
 def test_shape_sweep_bitwise(sgh, levels, inverse, fuse):
     N = si.num_points(levels)
     u = si.fill_uniform(N, grid_id=(N * 7 + len(levels)) % 9973)
@@ -183,15 +199,16 @@ def _batch_check(sgh, members, ids, inverse=False, fuse=True):
 
 
 @pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
-@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "per_axis"])
+@pytest.mark.parametrize("fuse", FUSE_MODES, ids=FUSE_IDS)
 def test_batched_mixed_bitwise(sgh, inverse, fuse):
     rng = np.random.default_rng(11)
     members = [tuple(int(x) for x in rng.integers(1, 8, size=3)) for _ in range(60)]
     members += [(1, 1, 1), (13, 1, 2), (1, 12, 1), (2, 2, 11), (7, 7, 3)]
+    members += [lv[:3] for lv in BLOCKED_SHAPES if len(lv) == 3 or lv[3] == 1]
     _batch_check(sgh, members, list(range(len(members))), inverse, fuse)
 
 
-@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "per_axis"])
+@pytest.mark.parametrize("fuse", FUSE_MODES, ids=FUSE_IDS)
 @pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
 def test_batched_c5_sample_vs_oracle(sgh, fuse, inverse):
     """A sample of the C5 set (every 97th member plus the extremes), each compared
