@@ -98,7 +98,6 @@ sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *
   if (!host_grids || !levels) return invalid("NULL argument");
   for (int64_t g = 0; g < num_grids; ++g)
     if (!host_grids[g]) return invalid("host_grids[g] is NULL");
-  const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   HostLayout L;
   sgh_status st = host_layout(levels, d, num_grids, flags, L);
   if (st != SGH_OK) return st;

@@ -62,6 +62,39 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // 8-byte phase of a global address (0: 16-byte aligned, 1: 8 mod 16)
 __device__ __forceinline__ int phase8(const double *p) { return (int)((reinterpret_cast<uintptr_t>(p) >> 3) & 1); }
 
+// TMA bulk store (cp.async.bulk shared -> global, SASS UBLKCP): the FUSED W == 1
+// tiles write their contiguous ranges back through the async copy engine
+// instead of an LDS + STG per element.  SMEM element e sits at the same 16-byte
+// phase as its global address (the stage is offset by the tile's phase), so the
+// 16-byte aligned interior of a range is one bulk copy; its 8-byte ends are
+// stored by the issuing thread.  Issued by ONE thread, after
+// fence.proxy.async + a barrier (the tile's SMEM writes come from the generic
+// proxy); the stage is reused only after cp.async.bulk.wait_group.read.
+#ifndef SGH_BULK_STORE
+#define SGH_BULK_STORE 1
+#endif
+__device__ __forceinline__ void bulk_store_range(double *g, const double *s, int len) {
+  if (len <= 0) return;
+  const int head = phase8(g);
+  const int pairs = (len - head) >> 1;
+  const int last = head + 2 * pairs;
+  if (head) __stcg(g, s[0]);
+  if (last < len) __stcg(g + last, s[last]);
+  if (pairs > 0) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s + head);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g + head), "r"(sa),
+                 "r"(pairs * 16)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_fence_barrier() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
 // Copy len doubles gsrc[0..len) -> sdst[0..len) where sdst and gsrc have the
 // same 16-byte phase: 8-byte head/tail, 16-byte body.  Issue only.
 __device__ __forceinline__ void copy_range_async(double *sdst, const double *gsrc, int len) {
@@ -514,13 +547,22 @@ __device__ __forceinline__ void block_fine(double *p0, int STR, bool lo_ok, bool
   }
 }
 
-// One aligned 8-point block b of a (lattice) pole of nblk blocks: p0 is the
-// address of the virtual point j = 0 of the lattice (never dereferenced), point
-// j at p0[j*STR], n = 8*nblk - 1 points; its ends are the boundary only for the
-// first / last block.  Writes only the block's fine points j = 8b+1 .. 8b+7.
+// Work items of the in-SMEM pole transforms are aligned blocks of 2^kTB points
+// (kTB + 1 ... fine levels in 2^kTB + 1 registers per item); a pole of level l
+// is done as blocks at stride 1, then its coarse lattice (stride 2^kTB, level
+// l - kTB) the same way, until the lattice fits one register pole.
+#ifndef SGH_TB
+#define SGH_TB 3
+#endif
+constexpr int kTB = SGH_TB;
+
+// One aligned block b of 2^kTB points of a (lattice) pole of nblk blocks: p0 is
+// the address of the virtual point j = 0 of the lattice (never dereferenced),
+// point j at p0[j*STR], n = 2^kTB nblk - 1 points; its ends are the boundary
+// only for the first / last block.  Writes only the block's fine points.
 template <bool INV>
-__device__ __forceinline__ void block8(double *p0, int STR, int b, int nblk) {
-  block_fine<3, INV>(p0 + 8 * b * STR, STR, b > 0, b < nblk - 1);
+__device__ __forceinline__ void block_item(double *p0, int STR, int b, int nblk) {
+  block_fine<kTB, INV>(p0 + (b << kTB) * STR, STR, b > 0, b < nblk - 1);
 }
 
 template <bool INV>
@@ -572,9 +614,9 @@ struct HaloSkip {
 
 // One axis of a staged tile, all npoles poles of level l (pole p = (oo, rk, c)
 // at sm + (oo*n*R + rk)*RS + c, point stride R*RS), in parallel work items:
-// l <= 4: one register pole per thread; l >= 5: (pole, 8-block) items on the
-// level-l pole, then on its coarse lattice (stride x8, level l-3), ... until
-// the lattice has l' <= 4, done as register poles.  A barrier between lattice
+// l <= 4: one register pole per thread; l >= 5: (pole, 2^kTB-block) items on
+// the level-l pole, then on its coarse lattice (stride x2^kTB, level l-kTB),
+// ... until the lattice has l' <= 4, done as register poles.  A barrier between lattice
 // levels; hierarchization runs fine -> coarse, dehierarchization the reverse.
 template <bool INV, int W>
 __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv fR, int Ok,
@@ -598,25 +640,26 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
     __syncthreads();
     return;
   }
-  // lattice levels visited: l, l-3, l-6, ... (> 4), then the register lattice
+  // lattice levels visited: l, l-kTB, l-2kTB, ... (> 4), then the register lattice
   int levels[8], nlev = 0, lf = l;
   while (lf > 4) {
     levels[nlev++] = lf;
-    lf -= 3;
+    lf -= kTB;
   }
   const ItemWalk walk(npoles);
-  auto block_phase = [&](int k) {                // k-th lattice level: stride 8^k
-    const int m = 1 << (3 * k);
-    const int nblk = 1 << (levels[k] - 3);
+  auto block_phase = [&](int k) {                // k-th lattice level: stride 2^{kTB k}
+    const int m = 1 << (kTB * k);
+    const int nblk = 1 << (levels[k] - kTB);
     // items (b, p), p fastest: lanes run over poles (conflict-free SMEM)
     for (int b = walk.b0, p = walk.p0; b < nblk; walk.next(b, p)) {
       if (hs.on && hs.skip(pole_row(p))) continue;
-      block8<INV>(pole_base(p) - STR, m * STR, b, nblk);
+      block_item<INV>(pole_base(p) - STR, m * STR, b, nblk);
     }
     __syncthreads();
   };
   auto lattice_phase = [&]() {
-    const int m = 1 << (3 * nlev);
+    if (lf <= 1) return;                         // a single point: no update
+    const int m = 1 << (kTB * nlev);
     for (int p = threadIdx.x; p < npoles; p += kThreads) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       double *p0 = pole_base(p) - STR;           // virtual point 0
@@ -636,8 +679,8 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
 // The BLOCKED axis of a tile: every pole holds one aligned block of 2^t points
 // plus its two ends (local y = 0..2^t, point stride R*RS); only the fine points
 // y = 1..2^t-1 are transformed.  Inside the block the same
-// lattice recursion as fused_axis: 8-point sub-blocks at strides 1, 8, ..,
-// 8^{K-1} (K = t/3), then the top lattice of 2^{t-3K} + 1 points at stride 8^K.
+// lattice recursion as fused_axis: 2^kTB-point sub-blocks at strides 1, 2^kTB,
+// .. (K = t / kTB levels), then the top lattice of 2^{t - kTB K} + 1 points.
 // lo_ok / hi_ok: the block's ends are grid points (false: the zero boundary).
 template <bool INV, int W>
 __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int R, const FDiv fR, int Ok,
@@ -653,22 +696,23 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
     const int rk = rest - oo * R;
     return sm + (oo * ej * R + rk) * RS + c;     // local point y = 0
   };
-  const int K = t / 3;
-  const int tr = t - 3 * K;
+  const int K = t / kTB;
+  const int tr = t - kTB * K;
   const ItemWalk walk(npoles);
   auto sub_phase = [&](int k) {
-    const int m = 1 << (3 * k);
-    const int nblk = 1 << (t - 3 * k - 3);
+    const int m = 1 << (kTB * k);
+    const int nblk = 1 << (t - kTB * k - kTB);
     for (int b = walk.b0, p = walk.p0; b < nblk; walk.next(b, p))
-      block_fine<3, INV>(pole_base(p) + 8 * b * m * STR, m * STR, lo_ok || b > 0, hi_ok || b < nblk - 1);
+      block_fine<kTB, INV>(pole_base(p) + (b << kTB) * m * STR, m * STR, lo_ok || b > 0, hi_ok || b < nblk - 1);
     __syncthreads();
   };
   auto top_phase = [&]() {
     if (tr == 0) return;                         // the top lattice is just the two ends
-    const int m = 1 << (3 * K);
+    const int m = 1 << (kTB * K);
     for (int p = threadIdx.x; p < npoles; p += kThreads) {
       if (tr == 1) block_fine<1, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
-      else block_fine<2, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
+      else if (tr == 2 || kTB <= 3) block_fine<2, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
+      else block_fine<(kTB > 3 ? 3 : 2), INV>(pole_base(p), m * STR, lo_ok, hi_ok);
     }
     __syncthreads();
   };
@@ -756,6 +800,15 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
   const int nyw = dense_y ? 1 : ny;                // segment s = z * nyw + (y - y0)
   auto seg_lo = [=](int z, int yy) { return (z * ej + y0 + yy) * A; };
   auto seg_g = [=](int z, int yy) { return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)z * Gn; };
+  if (STORE && SGH_BULK_STORE && aligned && nseg <= 64 && len >= 64) {   // bulk stores by one thread
+    bulk_fence_barrier();
+    if (threadIdx.x == 0) {
+      for (int z = 0; z < nseg / nyw; ++z)
+        for (int yy = 0; yy < nyw; ++yy) bulk_store_range(seg_g(z, yy), sm + seg_lo(z, yy), len);
+      bulk_commit();
+    }
+    return;
+  }
   if (nseg < 16 && len >= 128) {                  // few long runs: the whole CTA on each
     for (int z = 0; z < nseg / nyw; ++z)
       for (int yy = 0; yy < nyw; ++yy) {
@@ -914,7 +967,11 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     hs.fE = T.fE;
     hs.ej = T.ej;
   }
+#ifdef SGH_DEBUG_NOCOMPUTE
+  for (int j = 0; j < 0; ++j) {                     // timing experiment: load + store only
+#else
   for (int j = 0; j < T.m; ++j) {                   // axes ascending
+#endif
     const int l = T.gl[j];
     if (l <= 1) continue;
     const int R = T.gR[j];
@@ -933,7 +990,15 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     return;
   }
   if (W == 1) {
-    for (int e = threadIdx.x; e < rows_total; e += kThreads) __stcg(gbase + e, sm[e]);
+    if (SGH_BULK_STORE) {
+      bulk_fence_barrier();
+      if (threadIdx.x == 0) {
+        bulk_store_range(gbase, sm, rows_total);
+        bulk_commit();
+      }
+    } else {
+      for (int e = threadIdx.x; e < rows_total; e += kThreads) __stcg(gbase + e, sm[e]);
+    }
   } else {
     constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
     constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
@@ -961,8 +1026,11 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
 #ifndef FUSED_MINB
 #define FUSED_MINB 3   // resident CTAs per SM the FUSED register budget is sized for
 #endif
+#ifndef FUSED_MINB2
+#define FUSED_MINB2 2  // the same for the two-stage (double-buffered) variant
+#endif
 template <bool INV, int W, int STAGES>
-__global__ void __launch_bounds__(kThreads, (STAGES == 1 ? FUSED_MINB : 2)) k_fused(const __grid_constant__ Src src) {
+__global__ void __launch_bounds__(kThreads, (STAGES == 1 ? FUSED_MINB : FUSED_MINB2)) k_fused(const __grid_constant__ Src src) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Task s_task[2];                      // descriptors of the two in-flight tiles
   int64_t q = blockIdx.x;
@@ -1007,6 +1075,7 @@ __global__ void __launch_bounds__(kThreads, (STAGES == 1 ? FUSED_MINB : 2)) k_fu
     }
     __syncthreads();
     fused_compute_store<INV, W>(s_task[STAGES == 2 ? (k & 1) : 0], fc, cur + fc.par);
+    if (W == 1 && SGH_BULK_STORE && threadIdx.x == 0) bulk_wait_read();   // bulk stores have read the stage
     __syncthreads();                              // the stage is free for the next load
     if (!more) break;
     q = qn;
@@ -1021,6 +1090,7 @@ __global__ void __launch_bounds__(kThreads, (STAGES == 1 ? FUSED_MINB : 2)) k_fu
     Tc = Tn;
     fc = fn;
   }
+  if (W == 1 && SGH_BULK_STORE && threadIdx.x == 0) bulk_wait_all();
 }
 
 // ----------------------------------------------------------------------- REG
