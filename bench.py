@@ -188,6 +188,10 @@ def main():
                     help="time dehierarchization (P:77) instead (reported under a 'dehierarchized' metric)")
     ap.add_argument("--per-axis", action="store_true",
                     help="one HBM round trip per axis (disable the multi-axis FUSED kernel)")
+    ap.add_argument("--dump-launch-keys", default=None,
+                    help="write the kernel keys of one timed step's launches (in order) to this JSON file "
+                         "(pairs the launches of an ncu launch list with the bench's kernel keys: "
+                         "scripts/ncu_traffic.py)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -282,6 +286,12 @@ def sgh_arm(args, rank, world, local_rank):
     barrier()
     launches = sgh.launch_count() - n0
     recs = sgh.profile_read()
+    if args.dump_launch_keys and rank == 0:
+        per_step = len(recs) // max(1, args.steps)
+        with open(args.dump_launch_keys, "w") as f:
+            json.dump({"workload": args.workload, "launches_per_step": per_step,
+                       "warmup": args.warmup, "keys": [r["kernel"] for r in recs[:per_step]],
+                       "algorithmic_bytes": [r["bytes"] for r in recs[:per_step]]}, f)
     sgh.profile_enable(False)
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1)
@@ -314,7 +324,8 @@ def sgh_arm(args, rank, world, local_rank):
         tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tf):
             try:
-                traffic = json.load(open(tf)).get(args.workload, {}).get(dom)
+                t = json.load(open(tf)).get(args.workload, {}).get(dom)
+                traffic = t["traffic_bytes_per_launch"] if isinstance(t, dict) else t
             except Exception:
                 traffic = None
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -79,6 +79,7 @@ void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64
   const int64_t n = (int64_t(1) << l) - 1;
   Task t;
   std::memset(&t, 0, sizeof t);
+  t.bt2 = -1;
   t.grid = grid;
   t.O = O;
   t.OS = OS;
@@ -195,6 +196,7 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
   for (int k = b; k < d; ++k) O *= (int64_t(1) << levels[k]) - 1;
   if (busy < 2 || b - a > 16) return false;
   std::memset(&t, 0, sizeof t);
+  t.bt2 = -1;
   t.grid = grid;
   t.kind = KIND_FUSED;
   t.bj = -1;
@@ -290,6 +292,7 @@ static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a
     const int64_t ej = blocked ? (int64_t(1) << bt) + 1 : nlj;
     Task t;
     std::memset(&t, 0, sizeof t);
+    t.bt2 = -1;
     t.grid = grid;
     t.kind = KIND_FUSED;
     t.m = b - a;
@@ -333,6 +336,133 @@ static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a
   return phases.size() > first;
 }
 
+// Only the FINE part of a pole view w.r.t. block level tb (the points with
+// tz(i) < tb, each written from its aligned 2^tb block + end points): one
+// FLAT_BLOCKS or STRIDED phase, no lattice.  Returns false if no tile fits.
+static bool plan_view_fine(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64_t base, int l, int tb,
+                           std::vector<Task> &phases) {
+  if (l <= 1 || O <= 0 || S <= 0 || tb < 1 || tb >= l) return false;
+  Task t;
+  std::memset(&t, 0, sizeof t);
+  t.bt2 = -1;
+  t.grid = grid;
+  t.O = O;
+  t.OS = OS;
+  t.PS = PS;
+  t.S = S;
+  t.base = base;
+  t.l = l;
+  t.t = tb;
+  if (PS == S && S < kFlatMaxS && (int64_t(1) << tb) * S <= kFlatT) {
+    t.kind = KIND_FLAT_BLOCKS;
+    t.fS = make_fdiv((uint32_t)S);
+    t.tiles = O << (l - tb);
+    phases.push_back(t);
+    return true;
+  }
+  int W = 256;
+  while (W > 32 && S <= W / 2 + W / 4) W >>= 1;
+  while (W > 32 && ((int64_t(1) << tb) + 1) * (W + 2) > kStridedTileDoubles) W >>= 1;
+  if (((int64_t(1) << tb) + 1) * (W + 2) > kStridedTileDoubles) return false;
+  t.kind = KIND_STRIDED;
+  t.W = W;
+  t.ncb = (S + W - 1) / W;
+  t.tiles = (O << (l - tb)) * t.ncb;
+  phases.push_back(t);
+  return true;
+}
+
+// TWO-BLOCKED group (the block scheme for C4): a grid whose only
+// non-trivial axes are a and a + 1 (a the unit-stride one).  Hierarchization
+// only.  Phases, in order (no phase reads a value an earlier one wrote unless
+// it needs exactly that value):
+//   0  FUSED tiles of (2^t1 + 1) x (2^t2 + 1) points: the fine-a & fine-b points
+//      (axis a fine part, then axis b fine part, both in SMEM);
+//   1  fine-a part on the coarse-b rows (reads original coarse-a ends);
+//   2  FUSED tiles over the coarse-a columns x one b-block (+ end rows): the
+//      whole a-lattice of each row, then the fine-b part; writes the fine-b
+//      rows (the end rows are only a halo here);
+//   3  the a-lattice on the coarse-b rows (points coarse along both axes),
+//      after phases 1 and 2 have read their original values;
+//   4  the coarse-b lattice over all columns (level l_b - t2, stride 2^t2 n_a).
+// Phases 1-4 move ~2^-t1 + 2^-t2 of the points.  Bitwise equal to Alg. 1: every
+// point receives the same operations in the same order (axis a, then b).
+static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, int t1, int t2,
+                             std::vector<Task> &phases) {
+  if (a + 1 >= d) return false;
+  for (int k = 0; k < d; ++k)
+    if (k != a && k != a + 1 && levels[k] != 1) return false;
+  const int la = levels[a], lb = levels[a + 1];
+  if (t1 < 2 || t2 < 2 || t1 >= la || t2 >= lb) return false;
+  const int64_t na = (int64_t(1) << la) - 1, nb = (int64_t(1) << lb) - 1;
+  const int64_t e1 = (int64_t(1) << t1) + 1, e2 = (int64_t(1) << t2) + 1;
+  if (e1 * e2 > fused_budget() + fused_budget() / 16) return false;
+  const size_t first = phases.size();
+  Task t;
+  std::memset(&t, 0, sizeof t);
+  t.grid = grid;
+  t.kind = KIND_FUSED;
+  t.m = 2;
+  t.gl[0] = (int8_t)la;
+  t.gl[1] = (int8_t)lb;
+  t.gR[0] = 1;
+  t.gR[1] = (int32_t)e1;
+  t.fR[0] = make_fdiv(1);
+  t.fR[1] = make_fdiv((uint32_t)e1);
+  t.P = (int32_t)(e1 * e2);
+  t.S = 1;
+  t.O = 1;
+  t.OS = na * nb;
+  t.l = la;
+  t.W = 1;
+  t.R = 1;
+  t.bj = 0;
+  t.bt = t1;
+  t.nb_log = la - t1;
+  t.A = 1;
+  t.ej = (int32_t)e1;
+  t.fA = make_fdiv(1);
+  t.fE = make_fdiv((uint32_t)e1);
+  t.Gj = 1;
+  t.Gnext = na;
+  t.aligned = 1;                                     // Gj = 1, Gnext = n_a and e1 odd
+  t.bt2 = t2;
+  t.nb2_log = lb - t2;
+  t.ncb = 1;
+  t.tiles = int64_t(1) << (t.nb_log + t.nb2_log);
+  phases.push_back(t);
+  const int64_t s1 = int64_t(1) << t1, s2 = int64_t(1) << t2;
+  const int64_t nla = (int64_t(1) << (la - t1)) - 1;   // coarse-a columns
+  if (nla * e2 > fused_budget() + fused_budget() / 16) {
+    phases.resize(first);
+    return false;
+  }
+  // 1: fine-a part on the coarse-b rows
+  bool ok = plan_view_fine(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, 1, 1, (s2 - 1) * na, la, t1, phases);
+  // 2: the coarse-a columns in b-blocks: the whole a-lattice of every row of the
+  //    block (its end rows only as halo, not written), then the fine-b part
+  Task c = t;
+  c.gl[0] = (int8_t)(la - t1);
+  c.gR[1] = (int32_t)nla;
+  c.fR[1] = make_fdiv((uint32_t)nla);
+  c.P = (int32_t)(nla * e2);
+  c.base = s1 - 1;
+  c.bt = la - t1;                                    // whole lattice poles (not blocked)
+  c.nb_log = 0;
+  c.ej = (int32_t)nla;
+  c.fE = make_fdiv((uint32_t)nla);
+  c.Gj = s1;
+  c.aligned = 0;
+  c.tiles = int64_t(1) << c.nb2_log;
+  phases.push_back(c);
+  // 3: the a-lattice on the coarse-b rows (the points coarse along both axes)
+  plan_view(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, s1, 1, (s2 - 1) * na + s1 - 1, la - t1, phases);
+  // 4: the coarse-b lattice over all columns
+  plan_view(grid, 1, 0, s2 * na, na, (s2 - 1) * na, lb - t2, phases);
+  if (!ok) phases.resize(first);
+  return ok;
+}
+
 // Estimated time per point (1 / TB/s) of a pass, from the kernels' measured
 // B200 throughput (profiles/r01): wide contiguous tiles stream best, narrow
 // column tiles lose DRAM efficiency.
@@ -350,6 +480,10 @@ static double kind_bw(const Task &t) {
         if (t.bj >= 0) run = (t.Gj == t.A) ? int64_t(t.A) * t.ej : t.A;
       }
       double bw = run >= 256 ? 5.2 : run >= 128 ? 4.6 : run >= 64 ? 4.3 : run >= 32 ? 4.0 : run >= 16 ? 3.3 : 2.2;
+      // two blocked axes: two block transforms per tile, compute-bound on
+      // B200 (measured 2.84 TB/s on C4 (14,13) tiles 129 x 65; below the
+      // per-axis pair FLAT_BLOCKS + STRIDED, so the planner keeps that)
+      if (t.bt2 >= 0 && t.bt < t.gl[t.bj]) bw = std::min(bw, 2.6);
       // lattice views: 8-byte copies; single-element runs (a lattice of the
       // contiguous axis) touch one 32-byte sector per point and write partial
       // sectors (measured ~0.3 TB/s algorithmic on C3's (5,4,4) lattice)
@@ -371,6 +505,10 @@ static double pass_cost(const std::vector<Task> &phases) {
       // a lattice view of a blocked group: its share of the points, plus a
       // fixed per-phase cost (a few % of a pass: launch tail, small tiles)
       c += task_points(t) / std::max(1.0, task_points(phases[0])) / (0.7 * bw) + 0.01;
+    } else if (t.S < 8 && t.PS != t.S) {
+      // a view whose elements are isolated (one per 32-byte sector, no two in
+      // a row): measured ~0.13 TB/s algorithmic (STRIDED, C4 cross phases)
+      c += task_points(t) / std::max(1.0, task_points(phases[0])) / 0.15;
     } else {
       // later phases are coarse lattices: a small fraction of the points, latency bound
       c += 2.0 * task_points(t) / std::max(1.0, task_points(phases[0])) / 1.0;
@@ -437,6 +575,28 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
           }
         }
       }
+    }
+  }
+  // two-blocked plan (grids with exactly two adjacent non-trivial axes)
+  if (blocked_ok && !inv) {
+    std::vector<Task> bestp;
+    // SGH_TWO_BLOCKED=force: take a two-blocked plan whenever one exists (tests)
+    const char *tb = getenv("SGH_TWO_BLOCKED");
+    double bc = (tb && std::strcmp(tb, "force") == 0) ? 1e30 : cost[d];
+    for (int a = 0; a + 1 < d; ++a)
+      for (int t1 = 2; t1 < levels[a]; ++t1)
+        for (int t2 = 2; t2 < levels[a + 1]; ++t2) {
+          std::vector<Task> ph;
+          if (!plan_two_blocked(grid, levels, d, a, t1, t2, ph)) continue;
+          const double c = pass_cost(ph);
+          if (c < bc - 1e-12) {
+            bc = c;
+            bestp = ph;
+          }
+        }
+    if (!bestp.empty()) {
+      passes.push_back(std::move(bestp));
+      return;
     }
   }
   std::vector<int> ends;
@@ -882,8 +1042,9 @@ int64_t sgh_plan_describe(const int32_t *levels, int32_t d, uint32_t flags, char
       if (t.kind == KIND_FUSED) {
         std::string lv;
         for (int j = 0; j < t.m; ++j) lv += (j ? "," : "") + std::to_string(int(t.gl[j]));
-        std::snprintf(line, sizeof line, "  FUSED W=%d levels=(%s) special=%d bt=%d aligned=%d points=%.0f\n", t.W,
-                      lv.c_str(), t.bj, t.bj >= 0 ? t.bt : -1, t.bj >= 0 ? t.aligned : 1, task_points(t));
+        std::snprintf(line, sizeof line, "  FUSED W=%d levels=(%s) special=%d bt=%d bt2=%d aligned=%d points=%.0f\n",
+                      t.W, lv.c_str(), t.bj, t.bj >= 0 ? t.bt : -1, t.bj >= 0 ? t.bt2 : -1, t.bj >= 0 ? t.aligned : 1,
+                      task_points(t));
       } else {
         std::snprintf(line, sizeof line, "  %s l=%d t=%d W=%d points=%.0f\n", names[t.kind], t.l, t.t, t.W,
                       task_points(t));

@@ -102,6 +102,19 @@ struct Task {
   int32_t aligned;    // 1: global and SMEM 8-byte phases agree row by row (16-byte copies)
   int64_t Gj, Gnext;  // global strides (elements) of the special axis and of the next group axis
   FDiv fA, fE;        // division by A, by ej
+  // TWO blocked axes (W == 1 only, SURVEY 8(a) a4 block scheme for C4): the
+  // group axis bj + 1 (the last one of the group) is blocked too, with block
+  // level bt2 (< 0: not).  The tile holds (2^bt + 1) x (2^bt2 + 1) points and
+  // writes the points that are fine along both axes; the rest (the "cross") is
+  // done by later phases (planner).
+  int32_t bt2;
+  int32_t nb2_log;    // log2(blocks of axis bj + 1)
+  // Cross phases of a two-blocked group: group axes in skipmask are laid out
+  // in the tile but NOT transformed (a pass along the other axis only), and
+  // the tile index o may be split into o1 + O1 o2 at o1 OS + o2 OS2 (O1 > 0).
+  uint32_t skipmask;
+  int32_t O1;
+  int64_t OS2;
 };
 
 static_assert(sizeof(Task) % 8 == 0, "Task must stay 8-byte aligned");

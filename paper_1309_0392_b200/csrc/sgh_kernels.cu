@@ -733,7 +733,9 @@ struct FusedTile {
   int wc;         // W > 1: valid columns
   int par;        // 8-byte phase of the SMEM data start
   int ylo, yhi;   // special axis: local rows that exist in the grid
-  bool lo_ok, hi_ok;  // blocked axis: the block's end points are grid points
+  int zlo, zhi;   // second blocked axis: local rows that exist in the grid
+  bool lo_ok, hi_ok;    // blocked axis: the block's end points are grid points
+  bool lo2_ok, hi2_ok;  // second blocked axis: the same
 };
 
 template <int W>
@@ -766,9 +768,27 @@ __device__ __forceinline__ FusedTile fused_tile(const Task &T, int64_t q) {
     rest = q / T.ncb;
   }
   const int b = (int)(rest & ((int64_t(1) << T.nb_log) - 1));
-  const int64_t o = rest >> T.nb_log;
+  rest >>= T.nb_log;
+  f.zlo = 0;
+  f.zhi = 0;
+  f.lo2_ok = f.hi2_ok = true;
+  int64_t z0 = 0;
+  if (T.bt2 >= 0) {                                // second blocked axis (bj + 1)
+    const int b2 = (int)(rest & ((int64_t(1) << T.nb2_log) - 1));
+    rest >>= T.nb2_log;
+    z0 = (int64_t(b2) << T.bt2) - 1;
+    f.lo2_ok = b2 > 0;
+    f.hi2_ok = b2 < (1 << T.nb2_log) - 1;
+    f.zlo = f.lo2_ok ? 0 : 1;
+    f.zhi = f.hi2_ok ? (1 << T.bt2) : (1 << T.bt2) - 1;
+  }
+  int64_t ooff = rest * T.OS;
+  if (T.O1 > 0) {                                  // two-level outer index
+    const int64_t o2 = rest / T.O1;
+    ooff = (rest - o2 * T.O1) * T.OS + o2 * T.OS2;
+  }
   const int64_t y0 = blocked ? (int64_t(b) << T.bt) - 1 : 0;   // 0-based pole index of local y = 0
-  f.g = T.grid + T.base + o * T.OS + c0 + y0 * T.Gj;
+  f.g = T.grid + T.base + ooff + c0 + y0 * T.Gj + z0 * T.Gnext;
   f.units = 1;
   f.wc = (W > 1) ? (int)min((int64_t)W, T.S - c0) : 1;
   f.lo_ok = !blocked || b > 0;
@@ -786,11 +806,17 @@ __device__ __forceinline__ FusedTile fused_tile(const Task &T, int64_t q) {
 template <bool STORE>
 __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f, double *sm) {
   const int A = T.A, ej = T.ej;
-  const int nz = T.P / (A * ej);
   const bool blocked = T.bt < T.gl[T.bj];
   const int y0 = (STORE && blocked) ? 1 : f.ylo;
   const int y1 = (STORE && blocked) ? ej - 2 : f.yhi;
   const int ny = y1 - y0 + 1;
+  // rows z of the axes after the special one: all of them, or the existing /
+  // fine rows of a second blocked axis
+  int z0 = 0, nz = T.P / (A * ej);
+  if (T.bt2 >= 0) {
+    z0 = STORE ? 1 : f.zlo;
+    nz = (STORE ? nz - 2 : f.zhi) - z0 + 1;
+  }
   const int64_t Gj = T.Gj, Gn = T.Gnext;         // registers: the cp.async "memory" clobbers
   const bool aligned = T.aligned != 0;              // would otherwise reload Task fields per run
   double *const g0 = f.g;
@@ -798,8 +824,8 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
   const int len = dense_y ? ny * A : A;
   const int nseg = dense_y ? nz : nz * ny;
   const int nyw = dense_y ? 1 : ny;                // segment s = z * nyw + (y - y0)
-  auto seg_lo = [=](int z, int yy) { return (z * ej + y0 + yy) * A; };
-  auto seg_g = [=](int z, int yy) { return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)z * Gn; };
+  auto seg_lo = [=](int z, int yy) { return ((z0 + z) * ej + y0 + yy) * A; };
+  auto seg_g = [=](int z, int yy) { return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)(z0 + z) * Gn; };
   if (STORE && SGH_BULK_STORE && aligned && nseg <= 64 && len >= 64) {   // bulk stores by one thread
     bulk_fence_barrier();
     if (threadIdx.x == 0) {
@@ -973,11 +999,15 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
   for (int j = 0; j < T.m; ++j) {                   // axes ascending
 #endif
     const int l = T.gl[j];
-    if (l <= 1) continue;
+    if (l <= 1 || ((T.skipmask >> j) & 1u)) continue;
     const int R = T.gR[j];
     const FDiv fR = T.fR[j];
     if (blocked && j == T.bj) {
       fused_axis_block<INV, W>(sm, RS, T.bt, R, fR, rows_total / (T.ej * R), f.lo_ok, f.hi_ok);
+      continue;
+    }
+    if (T.bt2 >= 0 && j == T.bj + 1) {              // second blocked axis (hierarchization only)
+      fused_axis_block<INV, W>(sm, RS, T.bt2, R, fR, rows_total / (((1 << T.bt2) + 1) * R), f.lo2_ok, f.hi2_ok);
       continue;
     }
     const int n = (T.bj == j) ? T.ej : (1 << l) - 1;

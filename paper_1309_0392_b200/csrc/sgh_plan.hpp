@@ -37,7 +37,17 @@ inline double task_points(const Task &t) {
     if (t.bj >= 0 && t.bt < t.gl[t.bj]) {           // blocked: the fine points of every block
       const int lj = t.gl[t.bj];
       const double fine = double((int64_t(1) << lj) - 1) - double((int64_t(1) << (lj - t.bt)) - 1);
+      if (t.bt2 >= 0) {                             // two blocked axes: fine along both
+        const int l2 = t.gl[t.bj + 1];
+        const double fine2 = double((int64_t(1) << l2) - 1) - double((int64_t(1) << (l2 - t.bt2)) - 1);
+        return double(t.O) * double(t.S) * double(t.P / t.ej / ((1 << t.bt2) + 1)) * fine * fine2;
+      }
       return double(t.O) * double(t.S) * double(t.P / t.ej) * fine;
+    }
+    if (t.bj >= 0 && t.bt2 >= 0) {                 // lattice axis x blocked axis: fine rows of the latter
+      const int l2 = t.gl[t.bj + 1];
+      const double fine2 = double((int64_t(1) << l2) - 1) - double((int64_t(1) << (l2 - t.bt2)) - 1);
+      return double(t.O) * double(t.S) * double(t.P / ((1 << t.bt2) + 1)) * fine2;
     }
     return double(t.O) * double(t.P) * double(t.S);   // every point, once
   }

@@ -118,7 +118,7 @@ def _plan_passes(levels, **kw):
 
 
 @pytest.mark.parametrize("levels", [(8, 8, 8), (10, 4, 4, 4, 4), (16, 2, 2, 1), (2, 7, 11, 2), (9, 2, 8, 2),
-                                    (1, 3, 12), (14, 1, 3, 4), (5, 3, 3, 3)], ids=str)
+                                    (1, 3, 12), (14, 1, 3, 4), (5, 3, 3, 3), (14, 13), (1, 10, 10, 1)], ids=str)
 @pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
 def test_plan_blocked_groups_cover_each_point_once(levels, inverse):
     """A fused pass (whole poles, or a BLOCKED group: block tiles + coarse-lattice
@@ -128,6 +128,12 @@ def test_plan_blocked_groups_cover_each_point_once(levels, inverse):
     N = si.num_points(levels)
     for ph in _plan_passes(levels, inverse=inverse):
         if ph[0][0] != "FUSED":
+            continue
+        if int(ph[0][1]["bt2"]) >= 0:
+            # two-blocked: the tiles write the points fine along both axes; the
+            # cross phases pass over every other point (some once per axis)
+            assert not inverse
+            assert ph[0][2] < N <= sum(p for _, _, p in ph)
             continue
         assert sum(p for _, _, p in ph) == N
         a = ph[0][1]
@@ -146,3 +152,23 @@ def test_plan_c2_c3_use_blocked_fusion():
     assert len(_plan_passes((10, 4, 4, 4, 4))) == 2
     assert all(len(ph) == 1 for ph in _plan_passes((8, 8, 8), fuse=False)[:1])
     assert sgh.plan_describe((8, 8, 8), fuse=False).count("FUSED") == 0
+
+
+def test_plan_two_blocked_available():
+    """Two-blocked plans (SURVEY 8(a) a4 block scheme: both axes of a 2-D grid
+    in aligned blocks, one round trip + cross phases) exist for hierarchization;
+    the cost model (measured 2.84 TB/s tiles) keeps C4 on its per-axis pair."""
+    p = _plan_passes((14, 13))
+    assert len(p) == 2
+    assert len(_plan_passes((14, 13), inverse=True)) == 2
+
+def test_plan_two_blocked_forced(monkeypatch):
+    """SGH_TWO_BLOCKED=force selects the two-blocked plan wherever one exists
+    (how the GPU parity tests exercise it)."""
+    monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
+    for lv in [(14, 13), (10, 10), (11, 8), (1, 1, 11, 9)]:
+        p = _plan_passes(lv)
+        assert len(p) == 1 and int(p[0][0][1]["bt2"]) >= 2, lv
+        N = si.num_points(lv)
+        assert p[0][0][2] < N <= sum(x for _, _, x in p[0])
+    assert len(_plan_passes((14, 13), inverse=True)) == 2       # hierarchization only

@@ -174,6 +174,29 @@ def test_config_golden_and_oracle(sgh, name):
         assert sgh.digest(g) == int(c["dehierarchized_fill"], 16)
 
 
+TWO_BLOCKED_SHAPES = [(10, 10), (11, 8), (13, 6), (12, 7), (1, 1, 11, 9), (12, 12), (7, 7), (5, 9), (9, 5), (3, 3)]
+
+
+@pytest.mark.parametrize("levels", TWO_BLOCKED_SHAPES, ids=str)
+def test_two_blocked_bitwise(sgh, levels, monkeypatch):
+    """The two-blocked plan (SURVEY 8(a) a4 block scheme: tiles fine along both
+    axes, then the cross phases) forced on 2-D grids: bitwise vs the oracle."""
+    monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
+    N = si.num_points(levels)
+    u = si.fill_uniform(N, grid_id=N % 977)
+    want = oracle.hierarchize(u.copy(), levels)
+    assert_bitwise(gpu_transform(sgh, u, levels), want)
+
+
+def test_two_blocked_c4_golden(sgh, monkeypatch):
+    monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
+    c = SD["configs"]["C4"]
+    g = torch.empty(si.num_points(c["levels"]), dtype=torch.float64, device="cuda")
+    sgh.fill_uniform(g, SD["seed"], c["grid_id"])
+    sgh.hierarchize(g, c["levels"])
+    assert sgh.digest(g) == int(c["hierarchized"], 16)
+
+
 @pytest.mark.parametrize("levels", [(8, 8, 8), (14, 13), (10, 4, 4, 4, 4)], ids=["C2", "C4", "C3"])
 def test_round_trip_device(sgh, levels):
     N = si.num_points(levels)
@@ -204,7 +227,7 @@ def test_batched_mixed_bitwise(sgh, inverse, fuse):
     rng = np.random.default_rng(11)
     members = [tuple(int(x) for x in rng.integers(1, 8, size=3)) for _ in range(60)]
     members += [(1, 1, 1), (13, 1, 2), (1, 12, 1), (2, 2, 11), (7, 7, 3)]
-    members += [lv[:3] for lv in BLOCKED_SHAPES if len(lv) == 3 or lv[3] == 1]
+    members += [tuple(lv[:3]) + (1,) * (3 - len(lv)) for lv in BLOCKED_SHAPES if len(lv) <= 3 or lv[3:] == (1,)]
     _batch_check(sgh, members, list(range(len(members))), inverse, fuse)
 
 
