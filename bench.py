@@ -62,7 +62,7 @@ def workload(name):
         desc = (f"C5: combination set d={cfg.d} n={cfg.n}, |l|_1 in {{{cfg.n},{cfg.n-1},{cfg.n-2},{cfg.n-3}}}, "
                 f"{len(members)} grids")
         return members, list(range(len(members))), desc
-    lv = si.CONFIGS[name].levels
+    lv = (si.CONFIGS.get(name) or si.SWEEPS[name]).levels
     return [tuple(lv)], [0], f"{name}: single grid level {tuple(lv)}"
 
 
@@ -179,7 +179,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="C5", choices=["C5", "C2", "C3", "C4"])
+    ap.add_argument("--workload", default="C5", choices=["C5", "C2", "C3", "C4", "S1", "S10"],
+                    help="BASELINE.json configs C2..C5 (default C5, the metric's config); S1 / S10 are the "
+                         "paper's 1-D l=27 and 10-D (9,2,..,2) sweep tops (SURVEY 8(f))")
     ap.add_argument("--impl", default="sgh", choices=["sgh", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -126,6 +126,26 @@ CONFIGS = {
     "C5": Config("C5", None, d=4, n=22),
 }
 
+# Paper-shaped sweeps (not BASELINE.json configs):
+#   S1  -- the 1-D grid of Fig. fig:1DLayouts at its largest size, l = 27
+#          ("1 GB when the levelsum |l|_1 = 27"): 134,217,727 points;
+#   S10 -- the 10-D anisotropic grid of Fig. fig:10D, level (l_1, 2, ..., 2)
+#          ("all other dimensions are fixed to 3 grid points") at the
+#          largest l_1 with |l|_1 <= 27: l_1 = 9, 511 x 3^9 = 10,057,813 points.
+SWEEPS = {
+    "S1": Config("S1", (27,)),
+    "S10": Config("S10", (9,) + (2,) * 9),
+}
+
+
+def sweep_levels(name: str, top: int):
+    """Level vectors of a paper sweep up to `top` (1-D: l = 1..top; 10-D: l_1 = 1..top)."""
+    if name == "S1":
+        return [(l,) for l in range(1, top + 1)]
+    if name == "S10":
+        return [(l,) + (2,) * 9 for l in range(1, top + 1)]
+    raise KeyError(name)
+
 
 def lpt_partition(sizes, nparts: int):
     """Longest-processing-time-first assignment of items (by size) to parts.

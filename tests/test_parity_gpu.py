@@ -174,6 +174,38 @@ def test_config_golden_and_oracle(sgh, name):
         assert sgh.digest(g) == int(c["dehierarchized_fill"], 16)
 
 
+@pytest.mark.parametrize("name", ["S1", "S10"])
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_paper_sweep_tops_bitwise(sgh, name, inverse):
+    """The paper's sweep shapes at their largest sizes: the 1-D
+    l = 27 grid (134 M points, 1.07 GB; long-pole blocks + 2-level lattice) and
+    the 10-D (9,2,...,2) grid, element-wise bitwise vs the oracle."""
+    levels = si.SWEEPS[name].levels
+    N = si.num_points(levels)
+    g = torch.empty(N, dtype=torch.float64, device="cuda")
+    sgh.fill_uniform(g, si.SEED, 7)
+    (sgh.dehierarchize if inverse else sgh.hierarchize)(g, levels)
+    want = oracle.fill_uniform(N, si.SEED, 7)
+    (oracle.dehierarchize if inverse else oracle.hierarchize)(want, levels)
+    assert_bitwise(g.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name,top", [("S1", 26), ("S10", 9)])
+def test_paper_sweeps_small_levels(sgh, name, top):
+    """Every level of the sweeps (1-D l = 1..26 step 5 + the tops' neighbours;
+    10-D l_1 = 1..9), bitwise, hierarchize then dehierarchize."""
+    lvs = si.sweep_levels(name, top)
+    if name == "S1":
+        lvs = [lv for lv in lvs if lv[0] % 5 == 1 or lv[0] >= 24]
+    for lv in lvs:
+        N = si.num_points(lv)
+        u = si.fill_uniform(N, grid_id=lv[0])
+        want = oracle.hierarchize(u.copy(), lv)
+        got = gpu_transform(sgh, u, lv, guard=64)
+        assert_bitwise(got, want)
+        assert_bitwise(gpu_transform(sgh, want, lv, inverse=True, guard=64), oracle.dehierarchize(want.copy(), lv))
+
+
 TWO_BLOCKED_SHAPES = [(10, 10), (11, 8), (13, 6), (12, 7), (1, 1, 11, 9), (12, 12), (7, 7), (5, 9), (9, 5), (3, 3)]
 
 
