@@ -13,7 +13,9 @@ scaling: the set is fixed), no data-path collective; the elapsed time is the
 max over ranks.  Inputs (41 GB) are far larger than L2, so no flush is needed.
 
 Single-grid workloads C2/C3/C4 run the same way with one grid (replicated per
-rank; C4 with N > 1 runs the sharded path with its NCCL all-to-all).
+rank; C4 with N > 1 runs the sharded path: by default the halo + coarse-lattice
+exchange -- one all-gather of a row per rank -- or, with --sharded a2a, the NCCL
+all-to-all re-shard).
 
 --impl reference times the CPU oracle (oracle/, the plain Alg. 1) on this box's
 host cores on a bounded sample of the same workload (the paper has no GPU
@@ -190,6 +192,9 @@ def main():
                     help="time dehierarchization (P:77) instead (reported under a 'dehierarchized' metric)")
     ap.add_argument("--per-axis", action="store_true",
                     help="one HBM round trip per axis (disable the multi-axis FUSED kernel)")
+    ap.add_argument("--sharded", default="halo", choices=["halo", "a2a"],
+                    help="C4 with N > 1 ranks: halo + coarse-lattice exchange (one all-gather of a row per rank, "
+                         "SURVEY 8(f) 1; default) or the all-to-all re-shard (SURVEY 8(a) a7)")
     ap.add_argument("--dump-launch-keys", default=None,
                     help="write the kernel keys of one timed step's launches (in order) to this JSON file "
                          "(pairs the launches of an ncu launch list with the bench's kernel keys: "
@@ -253,11 +258,18 @@ def sgh_arm(args, rank, world, local_rank):
         levels = members[0]
         b, e = sgh.shard_rows(levels, world, rank)
         C = sizes[0] // ((1 << levels[-1]) - 1)
-        shard = torch.empty((e - b) * C, dtype=torch.float64, device=dev)
-        sgh.fill_uniform(shard, si.SEED, 0, b * C)
         comm = sgh.ShardComm()
-        ws = torch.empty(sgh.sharded_workspace_bytes(levels, world) // 8 + 1, dtype=torch.float64, device=dev)
-        step = lambda: comm.transform(shard, levels, ws, inverse=args.inverse)  # noqa: E731
+        if args.sharded == "halo":
+            buf = torch.empty((e - b + 1) * C, dtype=torch.float64, device=dev)   # + the halo slot
+            shard = buf[:(e - b) * C]
+            ws = torch.empty(sgh.sharded_halo_workspace_bytes(levels, world) // 8 + 1, dtype=torch.float64,
+                             device=dev)
+            step = lambda: comm.transform_halo(buf, levels, ws, inverse=args.inverse)  # noqa: E731
+        else:
+            shard = torch.empty((e - b) * C, dtype=torch.float64, device=dev)
+            ws = torch.empty(sgh.sharded_workspace_bytes(levels, world) // 8 + 1, dtype=torch.float64, device=dev)
+            step = lambda: comm.transform(shard, levels, ws, inverse=args.inverse)  # noqa: E731
+        sgh.fill_uniform(shard, si.SEED, 0, b * C)
         my_points = shard.numel()
         deff_pts = d_eff(levels) * my_points
     else:
@@ -360,7 +372,8 @@ def sgh_arm(args, rank, world, local_rank):
                           "l2": "inputs larger than L2 (no flush needed)" if 8 * total_points > 2 * 126e6
                           else "L2 not flushed; input < 2x L2",
                           "parallelism": (f"grids LPT-balanced over {world} ranks" if args.workload == "C5"
-                                          else ("sharded along x_d, NCCL all-to-all" if sharded else "replicas")),
+                                          else ((f"sharded along x_d, {'halo + coarse-lattice all-gather' if args.sharded == 'halo' else 'NCCL all-to-all'}")
+                                                if sharded else "replicas")),
                           "seed": si.SEED},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                "gpu_launches": launches, "kernels": kern_tab, "model": model}

@@ -186,6 +186,33 @@ sgh_status sgh_dehierarchize_sharded(double *shard, const int32_t *levels, int32
 sgh_status sgh_transform_sharded_loopback(double *const *shards, const int32_t *levels, int32_t d, int32_t nranks,
                                           uint32_t flags, void *workspace, size_t ws_bytes, void *stream);
 
+/* ---- halo + coarse-lattice sharded pass ----
+ * The same row sharding of x_d over nranks = 2^p ranks (sgh_shard_rows), but
+ * the axis-d pass needs no re-shard: rank r's rows are the aligned
+ * super-block [r 2^T, (r+1) 2^T) of every x_d pole (T = l_d - p), whose
+ * interior depends only on the shard plus ONE halo row (the next shard's first
+ * row), by Alg. 1's finest-first order and predecessor rule;
+ * the shards' first rows form the coarse lattice, a level-p pole per column.
+ * One ncclAllGather of prod_{k<d} n_k doubles per rank gathers the first rows
+ * (halo and coarse lattice at once); every rank transforms the P - 1 coarse
+ * rows redundantly and keeps its own.  Bitwise equal to the single-GPU result.
+ *  shard:     this rank's rows (row_end - row_begin) * C doubles followed by ONE
+ *             spare row of C doubles (the halo slot; unspecified on return),
+ *             C = prod_{k<d} n_k.
+ *  workspace: >= sgh_sharded_halo_workspace_bytes() bytes (nranks * C doubles).
+ *  flags:     SGH_FLAG_DEHIERARCHIZE for the inverse (coarse lattice first).
+ * Errors: INVALID_ARGUMENT if nranks is not a power of two >= 2 or
+ * nranks > 2^{l_d - 1}.  Collective: every rank calls it. */
+size_t sgh_sharded_halo_workspace_bytes(const int32_t *levels, int32_t d, int32_t nranks);
+sgh_status sgh_transform_sharded_halo(double *shard, const int32_t *levels, int32_t d, void *comm, uint32_t flags,
+                                      void *workspace, size_t ws_bytes, void *stream);
+/* Test utility: the halo path for `nranks` VIRTUAL ranks on the current device
+ * (the all-gather becomes device copies).  shards[r]: rank r's rows + spare
+ * row; workspace: nranks * sgh_sharded_halo_workspace_bytes() bytes. */
+sgh_status sgh_transform_sharded_halo_loopback(double *const *shards, const int32_t *levels, int32_t d,
+                                               int32_t nranks, uint32_t flags, void *workspace, size_t ws_bytes,
+                                               void *stream);
+
 /* ----------------------------------------- harness utilities (not the method) */
 
 /* Seeded counter-based fill: value of global flat

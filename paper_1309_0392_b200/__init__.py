@@ -77,6 +77,10 @@ def _load():
         "sgh_hierarchize_sharded": (st, [vp, i32p, ctypes.c_int32, vp, vp, sz, vp]),
         "sgh_dehierarchize_sharded": (st, [vp, i32p, ctypes.c_int32, vp, vp, sz, vp]),
         "sgh_transform_sharded_loopback": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, vp, sz, vp]),
+        "sgh_sharded_halo_workspace_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int32]),
+        "sgh_transform_sharded_halo": (st, [vp, i32p, ctypes.c_int32, vp, ctypes.c_uint32, vp, sz, vp]),
+        "sgh_transform_sharded_halo_loopback": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+                                                     vp, sz, vp]),
         "sgh_fill_uniform": (st, [vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, vp]),
         "sgh_fill_uniform_batched": (st, [vpp, i64p, u64p, ctypes.c_int64, ctypes.c_uint64, vp, sz, vp]),
         "sgh_digest": (st, [vp, ctypes.c_int64, ctypes.c_int64, u64p, vp]),
@@ -101,7 +105,8 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_batched_workspace_bytes", "sgh_hierarchize_batched", "sgh_batched_host_buffer_bytes",
             "sgh_transform_batched_host", "sgh_shard_rows", "sgh_shard_layout", "sgh_comm_create", "sgh_comm_destroy",
             "sgh_comm_unique_id", "sgh_sharded_workspace_bytes", "sgh_hierarchize_sharded",
-            "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_fill_uniform",
+            "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_sharded_halo_workspace_bytes",
+            "sgh_transform_sharded_halo", "sgh_transform_sharded_halo_loopback", "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
             "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe",
             "sgh_status_string", "sgh_last_error", "sgh_version")
@@ -434,6 +439,17 @@ class ShardComm:
                      workspace.numel() * workspace.element_size(), _stream(stream)))
         return shard
 
+    def transform_halo(self, shard: torch.Tensor, levels, workspace: torch.Tensor, inverse=False, stream=None):
+        """Halo + coarse-lattice sharded pass: ``shard`` = this rank's rows plus
+        one spare row (sgh_transform_sharded_halo)."""
+        a, d = _levels_arr(levels)
+        with torch.cuda.device(shard.device):
+            _check(lib.sgh_transform_sharded_halo(_grid_ptr(shard, None), a, d, self.handle,
+                                                  ctypes.c_uint32(FLAG_DEHIERARCHIZE if inverse else 0),
+                                                  ctypes.c_void_p(workspace.data_ptr()),
+                                                  workspace.numel() * workspace.element_size(), _stream(stream)))
+        return shard
+
     def close(self):
         if self.handle:
             lib.sgh_comm_destroy(self.handle)
@@ -455,3 +471,21 @@ def transform_sharded_loopback(shards, levels, workspace: torch.Tensor, inverse=
         _check(lib.sgh_transform_sharded_loopback(ptrs, a, d, P, FLAG_DEHIERARCHIZE if inverse else 0,
                                                   ctypes.c_void_p(workspace.data_ptr()),
                                                   workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def sharded_halo_workspace_bytes(levels, nranks: int) -> int:
+    a, d = _levels_arr(levels)
+    return int(lib.sgh_sharded_halo_workspace_bytes(a, d, int(nranks)))
+
+
+def transform_sharded_halo_loopback(shards, levels, workspace: torch.Tensor, inverse=False, stream=None):
+    """Halo path for len(shards) virtual ranks on one device (test utility);
+    shards[r] = rank r's rows + one spare row."""
+    P = len(shards)
+    a, d = _levels_arr(levels)
+    ptrs = (ctypes.c_void_p * P)(*[s.data_ptr() for s in shards])
+    with torch.cuda.device(workspace.device):
+        _check(lib.sgh_transform_sharded_halo_loopback(ptrs, a, d, P, FLAG_DEHIERARCHIZE if inverse else 0,
+                                                       ctypes.c_void_p(workspace.data_ptr()),
+                                                       workspace.numel() * workspace.element_size(),
+                                                       _stream(stream)))

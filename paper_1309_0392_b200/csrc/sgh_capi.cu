@@ -102,6 +102,7 @@ void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64
     const int tb = floor_log2(kFlatT / S);               // 2^tb * S <= kFlatT < 2^l * S
     t.kind = KIND_FLAT_BLOCKS;
     t.t = tb;
+    t.rlog = l - tb;
     t.tiles = O << (l - tb);
     phases.push_back(t);
     plan_view(grid, O, OS, PS << tb, S, base + ((int64_t(1) << tb) - 1) * PS, l - tb, phases);
@@ -148,6 +149,7 @@ void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64
   t.kind = KIND_STRIDED;
   t.W = W;
   t.t = tb;
+  t.rlog = l - tb;
   t.ncb = (S + W - 1) / W;
   t.tiles = (O << (l - tb)) * t.ncb;
   phases.push_back(t);
@@ -339,8 +341,8 @@ static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a
 // Only the FINE part of a pole view w.r.t. block level tb (the points with
 // tz(i) < tb, each written from its aligned 2^tb block + end points): one
 // FLAT_BLOCKS or STRIDED phase, no lattice.  Returns false if no tile fits.
-static bool plan_view_fine(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64_t base, int l, int tb,
-                           std::vector<Task> &phases) {
+bool plan_view_fine(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64_t base, int l, int tb,
+                    std::vector<Task> &phases) {
   if (l <= 1 || O <= 0 || S <= 0 || tb < 1 || tb >= l) return false;
   Task t;
   std::memset(&t, 0, sizeof t);
@@ -353,6 +355,7 @@ static bool plan_view_fine(double *grid, int64_t O, int64_t OS, int64_t PS, int6
   t.base = base;
   t.l = l;
   t.t = tb;
+  t.rlog = l - tb;
   if (PS == S && S < kFlatMaxS && (int64_t(1) << tb) * S <= kFlatT) {
     t.kind = KIND_FLAT_BLOCKS;
     t.fS = make_fdiv((uint32_t)S);

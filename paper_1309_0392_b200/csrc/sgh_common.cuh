@@ -71,7 +71,9 @@ struct Task {
   int32_t kind;
   int32_t R;          // FLAT_SLABS: slabs per tile
   int32_t W;          // STRIDED: tile width (columns)
-  int32_t pad_;
+  int32_t rlog;       // FLAT_BLOCKS / STRIDED: the tiles cover 2^rlog consecutive blocks (of level t)
+  int64_t blk0;       //   starting at block blk0 (all blocks: rlog = l - t, blk0 = 0; a shard's
+                      //   super-block only in the halo-sharded pass)
   FDiv fS;            // division by S   (FLAT kinds, S < 2^31)
   FDiv fNS;           // division by n*S (FLAT_SLABS)
   // FUSED: axes a..a+m-1 of the grid transformed together, whole poles.

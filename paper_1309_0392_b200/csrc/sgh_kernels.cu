@@ -238,9 +238,9 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
   for_each_tile(src, [&](const Task &T, int64_t q) {
     const int t = T.t;
     const int B = 1 << t;
-    const int nb_log = T.l - t;
-    const int64_t o = q >> nb_log;
-    const int b = (int)(q & ((1 << nb_log) - 1));
+    const int nb_log = T.l - t;                            // global blocks per pole
+    const int64_t o = q >> T.rlog;
+    const int b = (int)(T.blk0 + (q & ((int64_t(1) << T.rlog) - 1)));
     const int S = (int)T.S;
     const int n = (1 << T.l) - 1;
     const int i0 = b * B;                                  // pole index of local row 0
@@ -333,11 +333,10 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
   for_each_tile(src, [&](const Task &T, int64_t q) {
     const int t = T.t;
     const int B = 1 << t;
-    const int nb_log = T.l - t;
     const int64_t cb = q % T.ncb;
     const int64_t rest = q / T.ncb;
-    const int b = (int)(rest & ((1 << nb_log) - 1));
-    const int64_t o = rest >> nb_log;
+    const int b = (int)(T.blk0 + (rest & ((int64_t(1) << T.rlog) - 1)));
+    const int64_t o = rest >> T.rlog;
     const int64_t c0 = cb * W;
     const int wc = (int)min((int64_t)W, T.S - c0);
     const int n = (1 << T.l) - 1;

@@ -71,6 +71,11 @@ void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64
 void plan_axis(double *grid, const int32_t *levels, int d, int k, std::vector<Task> &phases,
                int64_t rows_last = -1);
 
+// Only the fine part (tz(i) < tb) of a pole view: one FLAT_BLOCKS / STRIDED
+// phase over all 2^{l-tb} blocks (rlog = l - tb, blk0 = 0).  False if no tile fits.
+bool plan_view_fine(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64_t base, int l, int tb,
+                    std::vector<Task> &phases);
+
 // helpers shared by the drivers (sgh_capi.cu)
 sgh_status cuda_fail(cudaError_t e, const char *where);
 sgh_status invalid(const char *msg);

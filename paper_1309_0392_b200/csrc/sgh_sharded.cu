@@ -273,6 +273,181 @@ static sgh_status sharded_loopback(double *const *shards, const int32_t *levels,
   return SGH_OK;
 }
 
+// ================================================ halo + coarse-lattice path
+// SURVEY 8(f) 1, derived from Alg. 1's finest-first order and the
+// predecessor rule exactly like a3.iii: with dyadic shards, rank r's
+// rows are the aligned super-block [r 2^T, (r+1) 2^T) of the x_d poles
+// (T = l_d - p).  Every point of it except its first row has both predecessors
+// in [r 2^T, (r+1) 2^T]: the shard plus ONE halo row, the next shard's first
+// row.  The first rows {q 2^T : q = 1..P-1} form the coarse lattice, a level-p
+// pole per column.  Hierarchization: gather the first rows of all ranks
+// (ncclAllGather of C doubles per rank), take the halo from them, transform the
+// super-block's interior (block tiles + the super-block's own lattice, all
+// restricted to block range r), then hierarchize the gathered coarse rows
+// (every rank, redundantly: P - 1 rows) and write back the own first row.
+// Dehierarchization: coarse first (gather, dehierarchize, write back own row,
+// take the NODAL halo), then the interior coarse -> fine.  Communication per
+// rank: C doubles out, P C in, instead of two all-to-alls of ~N/P each.
+//
+// The shard buffer holds rows [b, e) of x_d and ONE spare row after them (the
+// halo slot; its content on return is unspecified).
+
+// Block-restricted plan of the interior of super-block r (block level T) of a
+// pole view (global pole indexing through `base`): aligned sub-blocks of the
+// largest level a tile holds, then the super-block's own coarse lattice the
+// same way, until the lattice inside the super-block is empty.
+static bool plan_view_range(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64_t base, int l, int T,
+                            int64_t r, std::vector<Task> &phases) {
+  while (T > 0) {
+    int t = T;
+    std::vector<Task> one;
+    while (t > 0 && !(one.clear(), plan_view_fine(grid, O, OS, PS, S, base, l, t, one))) --t;
+    if (t == 0) return false;
+    Task &k = one.back();
+    k.rlog = T - t;                                   // the 2^{T-t} blocks of super-block r
+    k.blk0 = r << (T - t);
+    k.tiles = (O << k.rlog) * (k.kind == KIND_STRIDED ? k.ncb : 1);
+    phases.push_back(k);
+    base += ((int64_t(1) << t) - 1) * PS;             // the lattice {i : 2^t | i}
+    PS <<= t;
+    l -= t;
+    T -= t;
+  }
+  return true;
+}
+
+struct HaloGeom {
+  int P = 1, p = 0, d = 0, T = 0;
+  int32_t levels[SGH_MAX_D];
+  int64_t C = 1;
+  std::vector<int64_t> rows;
+};
+
+static sgh_status make_halo_geom(const int32_t *levels, int32_t d, int P, HaloGeom &H) {
+  if (d < 1) return invalid("d < 1");
+  sgh_status st = validate_levels(levels, d, nullptr);
+  if (st != SGH_OK) return st;
+  if (P < 2 || (P & (P - 1))) return invalid("the halo-sharded path needs nranks = 2^p >= 2");
+  H.P = P;
+  H.d = d;
+  while ((1 << H.p) < P) ++H.p;
+  if (H.p > levels[d - 1] - 1) return invalid("nranks must be <= 2^{l_d - 1}");
+  H.T = levels[d - 1] - H.p;
+  for (int k = 0; k < d; ++k) H.levels[k] = levels[k];
+  H.C = 1;
+  for (int k = 0; k < d - 1; ++k) H.C *= (int64_t(1) << levels[k]) - 1;
+  H.rows.resize(P);
+  for (int q = 0; q < P; ++q) {
+    int64_t b, e;
+    if ((st = shard_rows_impl(levels, d, P, q, &b, &e)) != SGH_OK) return st;
+    H.rows[q] = e - b;
+  }
+  return SGH_OK;
+}
+
+// axes 0..d-2 of rank r's shard (rows of x_d as the outer index)
+static sgh_status halo_local_axes(double *shard, const HaloGeom &H, int r, bool inv, cudaStream_t s) {
+  std::vector<Task> phases;
+  for (int k = 0; k < H.d - 1; ++k) {
+    phases.clear();
+    plan_axis(shard, H.levels, H.d, k, phases, H.rows[r]);
+    sgh_status st = launch_phases(phases, inv, s);
+    if (st != SGH_OK) return st;
+  }
+  return SGH_OK;
+}
+
+// the interior of rank r's super-block along x_d
+static sgh_status halo_interior(double *shard, const HaloGeom &H, int r, bool inv, cudaStream_t s) {
+  std::vector<Task> phases;
+  const int64_t first = (int64_t(r) << H.T);          // global 1-based index of shard row 0 (r >= 1)
+  const int64_t base = (r == 0) ? 0 : -(first - 1) * H.C;
+  if (!plan_view_range(shard, 1, 0, H.C, H.C, base, H.levels[H.d - 1], H.T, r, phases))
+    return invalid("no tile fits the sharded interior pass");
+  return launch_phases(phases, inv, s);
+}
+
+// the coarse lattice: gathered first rows G[q] (q = 1..P-1) as level-p poles
+static sgh_status halo_coarse(double *G, const HaloGeom &H, bool inv, cudaStream_t s) {
+  std::vector<Task> phases;
+  plan_view(G, 1, 0, H.C, H.C, H.C, H.p, phases);
+  return launch_phases(phases, inv, s);
+}
+
+static sgh_status d2d(double *dst, const double *src, int64_t n, cudaStream_t s, const char *what) {
+  if (n <= 0) return SGH_OK;
+  cudaError_t e = cudaMemcpyAsync(dst, src, size_t(n) * 8, cudaMemcpyDeviceToDevice, s);
+  return e == cudaSuccess ? SGH_OK : cuda_fail(e, what);
+}
+
+// one rank's steps around the gather; `gather` fills G from every rank's row 0
+static sgh_status halo_rank_steps(double *shard, double *G, const HaloGeom &H, int r, bool inv, cudaStream_t s,
+                                  const std::function<sgh_status()> &gather, bool do_local, bool do_gather) {
+  sgh_status st;
+  const int64_t C = H.C, R = H.rows[r];
+  if (do_local && (st = halo_local_axes(shard, H, r, inv, s)) != SGH_OK) return st;
+  if (do_gather && (st = gather()) != SGH_OK) return st;
+  if (!inv) {
+    if (r + 1 < H.P && (st = d2d(shard + R * C, G + (r + 1) * C, C, s, "halo row")) != SGH_OK) return st;
+    if ((st = halo_interior(shard, H, r, false, s)) != SGH_OK) return st;
+    if ((st = halo_coarse(G, H, false, s)) != SGH_OK) return st;   // redundant on every rank
+    if (r >= 1 && (st = d2d(shard, G + r * C, C, s, "coarse row back")) != SGH_OK) return st;
+  } else {
+    if ((st = halo_coarse(G, H, true, s)) != SGH_OK) return st;
+    if (r >= 1 && (st = d2d(shard, G + r * C, C, s, "coarse row back")) != SGH_OK) return st;
+    if (r + 1 < H.P && (st = d2d(shard + R * C, G + (r + 1) * C, C, s, "halo row")) != SGH_OK) return st;
+    if ((st = halo_interior(shard, H, r, true, s)) != SGH_OK) return st;
+  }
+  return SGH_OK;
+}
+
+static sgh_status sharded_halo_nccl(double *shard, const int32_t *levels, int32_t d, void *comm, void *workspace,
+                                    size_t ws_bytes, void *stream, bool inv) {
+  if (!comm) return invalid("comm is NULL");
+  Comm *c = static_cast<Comm *>(comm);
+  HaloGeom H;
+  sgh_status st = make_halo_geom(levels, d, c->nranks, H);
+  if (st != SGH_OK) return st;
+  if (!shard) return invalid("shard is NULL");
+  if (!workspace || ws_bytes < size_t(H.P * H.C * 8)) {
+    set_error("workspace smaller than sgh_sharded_halo_workspace_bytes()");
+    return SGH_ERR_WORKSPACE;
+  }
+  double *G = static_cast<double *>(workspace);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto gather = [&]() -> sgh_status {
+    ncclResult_t nr = ncclAllGather(shard, G, size_t(H.C), ncclDouble, c->nccl, s);
+    return nr == ncclSuccess ? SGH_OK : nccl_fail(nr, "ncclAllGather (coarse rows)");
+  };
+  return halo_rank_steps(shard, G, H, c->rank, inv, s, gather, true, true);
+}
+
+// P virtual ranks on one device (test): the gather is P device copies.
+static sgh_status sharded_halo_loopback(double *const *shards, const int32_t *levels, int32_t d, int32_t P,
+                                        void *workspace, size_t ws_bytes, void *stream, bool inv) {
+  HaloGeom H;
+  sgh_status st = make_halo_geom(levels, d, P, H);
+  if (st != SGH_OK) return st;
+  if (!shards) return invalid("shards is NULL");
+  for (int r = 0; r < P; ++r)
+    if (!shards[r]) return invalid("shards[r] is NULL");
+  if (!workspace || ws_bytes < size_t(H.P * H.C * 8) * size_t(P)) {
+    set_error("workspace smaller than nranks * sgh_sharded_halo_workspace_bytes()");
+    return SGH_ERR_WORKSPACE;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double *ws = static_cast<double *>(workspace);
+  const int64_t GC = H.P * H.C;
+  for (int r = 0; r < P; ++r)
+    if ((st = halo_local_axes(shards[r], H, r, inv, s)) != SGH_OK) return st;
+  for (int r = 0; r < P; ++r)                          // every rank's G = all first rows
+    for (int q = 0; q < P; ++q)
+      if ((st = d2d(ws + r * GC + q * H.C, shards[q], H.C, s, "loopback gather")) != SGH_OK) return st;
+  for (int r = 0; r < P; ++r)
+    if ((st = halo_rank_steps(shards[r], ws + r * GC, H, r, inv, s, nullptr, false, false)) != SGH_OK) return st;
+  return SGH_OK;
+}
+
 }  // namespace sgh
 
 using namespace sgh;
@@ -354,6 +529,26 @@ sgh_status sgh_hierarchize_sharded(double *shard, const int32_t *levels, int32_t
 sgh_status sgh_dehierarchize_sharded(double *shard, const int32_t *levels, int32_t d, void *comm, void *workspace,
                                      size_t ws_bytes, void *stream) {
   return sharded_nccl(shard, levels, d, comm, workspace, ws_bytes, stream, true);
+}
+
+size_t sgh_sharded_halo_workspace_bytes(const int32_t *levels, int32_t d, int32_t nranks) {
+  HaloGeom H;
+  if (make_halo_geom(levels, d, nranks, H) != SGH_OK) return 0;
+  return size_t(H.P * H.C * 8);
+}
+
+sgh_status sgh_transform_sharded_halo(double *shard, const int32_t *levels, int32_t d, void *comm, uint32_t flags,
+                                      void *workspace, size_t ws_bytes, void *stream) {
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
+  return sharded_halo_nccl(shard, levels, d, comm, workspace, ws_bytes, stream, (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
+}
+
+sgh_status sgh_transform_sharded_halo_loopback(double *const *shards, const int32_t *levels, int32_t d,
+                                               int32_t nranks, uint32_t flags, void *workspace, size_t ws_bytes,
+                                               void *stream) {
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
+  return sharded_halo_loopback(shards, levels, d, nranks, workspace, ws_bytes, stream,
+                               (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
 }
 
 sgh_status sgh_transform_sharded_loopback(double *const *shards, const int32_t *levels, int32_t d, int32_t nranks,

@@ -149,3 +149,106 @@ def _c5_worker(rank, world, port):
 
 def test_c5_partition_gloo():
     mp.spawn(_c5_worker, args=(2, _free_port()), nprocs=2, join=True)
+
+
+def _halo_worker(rank, world, port, levels, inverse):
+    """Halo + coarse-lattice sharded pass (sgh_transform_sharded_halo):
+    local axes, ONE all-gather of the shards' first rows (halo + coarse lattice),
+    the super-block interior along x_d from shard + halo, the coarse lattice as
+    level-p poles -- the oracle for the local / coarse pieces, a plain loop of
+    Alg. 1's update for the interior.  Equals the single-process oracle bitwise."""
+    _init(rank, world, port)
+    import oracle
+    import paper_1309_0392_b200 as sgh
+    import sgh_inputs as si
+    ld = levels[-1]
+    p = world.bit_length() - 1
+    T = ld - p
+    nd = (1 << ld) - 1
+    C = si.num_points(levels) // nd
+    rb, re = sgh.shard_rows(levels, world, rank)
+    R = re - rb
+    x = si.fill_uniform(R * C, si.SEED, 5, rb * C).reshape(R, C)
+    sign = 1.0 if inverse else -1.0
+    op = oracle.dehierarchize if inverse else oracle.hierarchize
+    for r in range(R if len(levels) > 1 else 0):          # local axes 1..d-1
+        plane = np.ascontiguousarray(x[r])
+        op(plane, levels[:-1])
+        x[r] = plane
+    first = torch.from_numpy(np.ascontiguousarray(x[0]))
+    rows = [torch.zeros(C, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(rows, first)                          # the only exchange
+    G = np.stack([t.numpy() for t in rows])               # G[q] = rank q's first row
+    lo = rank << T                                        # global index of the super-block start
+    # view: global 1-based index i in [lo, lo + 2^T] -> local row (i - lo); row 0 = own first
+    # row (rank >= 1) or the zero boundary (rank 0); row 2^T = the halo (next rank's first row)
+    def coarse():
+        if world > 2:
+            Gc = np.ascontiguousarray(G[1:]).ravel()
+            (oracle.dehierarchize_axis if inverse else oracle.hierarchize_axis)(
+                Gc, tuple(levels[:-1]) + (p,), len(levels) - 1)
+            G[1:] = Gc.reshape(world - 1, C)
+
+    def interior():
+        off = 0 if rank else 1                            # local row of shard row 0
+        v = np.zeros((1 + (1 << T), C))
+        v[off:off + R] = x
+        if rank + 1 < world:
+            v[1 << T] = G[rank + 1]                       # the halo row
+        if not inverse:                                   # one-pass: values entering the pass
+            out = v.copy()
+            for k in range(1, 1 << T):
+                i = lo + k
+                s = i & -i
+                y = v[k].copy()
+                if i - s >= 1:
+                    y = y + sign * 0.5 * v[k - s]
+                if i + s <= nd:
+                    y = y + sign * 0.5 * v[k + s]
+                out[k] = y
+            v = out
+        else:                                             # coarse -> fine with nodal ends
+            s = 1 << (T - 1)
+            while s >= 1:
+                for k in range(s, 1 << T, 2 * s):
+                    i = lo + k
+                    y = v[k]
+                    if i - s >= 1:
+                        y = y + 0.5 * v[k - s]
+                    if i + s <= nd:
+                        y = y + 0.5 * v[k + s]
+                    v[k] = y
+                s >>= 1
+        x[1 - off:] = v[1:off + R]                        # every row but the own first row
+
+    if not inverse:
+        interior()
+        coarse()
+        if rank:
+            x[0] = G[rank]
+    else:
+        coarse()
+        if rank:
+            x[0] = G[rank]
+        interior()                                        # halo = the now nodal G[rank + 1]
+    flat = torch.from_numpy(np.ascontiguousarray(x).ravel())
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([flat.numel()]))
+    mx = int(max(s.item() for s in sizes))
+    pad = torch.zeros(mx, dtype=torch.float64)
+    pad[:flat.numel()] = flat
+    parts = [torch.zeros(mx, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    if rank == 0:
+        got = np.concatenate([q[:int(s.item())].numpy() for q, s in zip(parts, sizes)])
+        want = op(si.fill_uniform(si.num_points(levels), si.SEED, 5), levels)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), "halo decomposition differs"
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("levels,world", [((6, 5), 2), ((3, 4, 5), 2), ((5, 2, 6), 4), ((2, 3, 2, 4), 4), ((7,), 4)],
+                         ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_sharded_halo_decomposition_gloo(levels, world, inverse):
+    mp.spawn(_halo_worker, args=(world, _free_port(), levels, inverse), nprocs=world, join=True)
