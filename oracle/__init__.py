@@ -66,6 +66,13 @@ def lib():
         L.sgo_fill_uniform.restype = None
         L.sgo_digest.argtypes = [_f64p, ctypes.c_int64, ctypes.c_int64]
         L.sgo_digest.restype = ctypes.c_uint64
+        L.sgo_sparse_num_points.argtypes = [ctypes.c_int32, ctypes.c_int32]
+        L.sgo_sparse_num_points.restype = ctypes.c_int64
+        _pp = ctypes.POINTER(ctypes.c_void_p)
+        L.sgo_gather.argtypes = [_pp, _i32p, _f64p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _f64p]
+        L.sgo_gather.restype = ctypes.c_int
+        L.sgo_scatter.argtypes = [_pp, _i32p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _f64p]
+        L.sgo_scatter.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -181,3 +188,43 @@ def fill_uniform(n: int, seed: int, grid_id: int, index_offset: int = 0) -> np.n
 def digest(grid: np.ndarray, index_offset: int = 0) -> int:
     g = np.ascontiguousarray(grid, dtype=np.float64).ravel()
     return int(lib().sgo_digest(_grid(g), int(g.size), int(index_offset)))
+
+
+# ----------------------------------------------- combination technique phase
+def sparse_num_points(d: int, n: int) -> int:
+    """Points of the sparse grid {W_lam : lam >= 1, |lam|_1 <= n} (oracle.h SG layout)."""
+    return int(lib().sgo_sparse_num_points(int(d), int(n)))
+
+
+def _ptrs(grids):
+    return (ctypes.c_void_p * len(grids))(*[g.ctypes.data for g in grids])
+
+
+def gather(grids, levels_list, coeffs, n: int) -> np.ndarray:
+    """sparse = sum_g coeffs[g] * alpha_g, accumulated grid by grid in list order
+    (the combination formula on surpluses)."""
+    d = len(levels_list[0])
+    for g, lv in zip(grids, levels_list):
+        _grid(g)
+        if g.size != num_points(lv):
+            raise ValueError("grid size does not match levels")
+    lv = np.ascontiguousarray(np.asarray(levels_list, dtype=np.int32))
+    c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64))
+    out = np.empty(sparse_num_points(d, n), dtype=np.float64)
+    rc = lib().sgo_gather(_ptrs(grids), lv.ctypes.data_as(_i32p), c.ctypes.data_as(_f64p), len(grids), d, int(n),
+                          _grid(out))
+    if rc:
+        raise ValueError("sgo_gather failed")
+    return out
+
+
+def scatter(sparse: np.ndarray, levels_list, n: int):
+    """Every point of every grid gets its sparse-grid value; returns new arrays."""
+    d = len(levels_list[0])
+    grids = [np.empty(num_points(lv), dtype=np.float64) for lv in levels_list]
+    lv = np.ascontiguousarray(np.asarray(levels_list, dtype=np.int32))
+    sp = np.ascontiguousarray(sparse, dtype=np.float64)
+    rc = lib().sgo_scatter(_ptrs(grids), lv.ctypes.data_as(_i32p), len(grids), d, int(n), _grid(sp))
+    if rc:
+        raise ValueError("sgo_scatter failed")
+    return grids

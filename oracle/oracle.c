@@ -282,3 +282,121 @@ uint64_t sgo_digest(const double *grid, int64_t n, int64_t index_offset) {
     }
     return h;
 }
+
+/* ---------------------------------------------------------------------------
+ * Combination technique gather / scatter (oracle.h).
+ * ------------------------------------------------------------------------- */
+struct sg_enum {
+  int32_t d, n;
+  int64_t *table; /* dense: index sum_k (lam_k - 1) n^k -> offset of W_lam */
+  int64_t next;   /* running offset */
+  int32_t lam[32];
+};
+
+static void sg_rec(struct sg_enum *E, int32_t k, int32_t remaining) {
+  if (k == E->d - 1) {
+    E->lam[k] = remaining;
+    int64_t idx = 0, mul = 1, size = 1;
+    for (int32_t q = 0; q < E->d; ++q) {
+      idx += (int64_t)(E->lam[q] - 1) * mul;
+      mul *= E->n;
+      size <<= (E->lam[q] - 1);
+    }
+    E->table[idx] = E->next;
+    E->next += size;
+    return;
+  }
+  for (int32_t v = 1; v <= remaining - (E->d - 1 - k); ++v) { /* lexicographic: lam_k ascending */
+    E->lam[k] = v;
+    sg_rec(E, k + 1, remaining - v);
+  }
+}
+
+/* builds the table; returns the number of sparse points, -1 if unsupported */
+static int64_t sg_table(int32_t d, int32_t n, int64_t **table_out) {
+  if (d < 1 || d > 32 || n < d) return -1;
+  double cells = 1;
+  for (int32_t k = 0; k < d; ++k) cells *= n;
+  if (cells > (double)(1 << 26)) return -1;
+  struct sg_enum E;
+  E.d = d;
+  E.n = n;
+  E.next = 0;
+  E.table = (int64_t *)malloc(sizeof(int64_t) * (size_t)cells);
+  if (!E.table) return -1;
+  for (int64_t c = 0; c < (int64_t)cells; ++c) E.table[c] = -1;
+  for (int32_t s = d; s <= n; ++s) sg_rec(&E, 0, s); /* level sum ascending */
+  if (table_out) *table_out = E.table;
+  else free(E.table);
+  return E.next;
+}
+
+int64_t sgo_sparse_num_points(int32_t d, int32_t n) { return sg_table(d, n, NULL); }
+
+static int tz64(int64_t i) {
+  int t = 0;
+  while (!(i & 1)) {
+    i >>= 1;
+    ++t;
+  }
+  return t;
+}
+
+/* sparse index of grid point (i_1..i_d) of a grid with levels l */
+static int64_t sg_index(const int64_t *table, int32_t d, int32_t n, const int32_t *l, const int64_t *i) {
+  int64_t idx = 0, mul = 1, in = 0, imul = 1;
+  for (int32_t k = 0; k < d; ++k) {
+    const int t = tz64(i[k]);
+    const int32_t lam = l[k] - t;
+    const int64_t j = i[k] >> (t + 1);
+    idx += (int64_t)(lam - 1) * mul;
+    mul *= n;
+    in += j * imul;
+    imul <<= (lam - 1);
+  }
+  return table[idx] + in;
+}
+
+static int sg_walk(double *const *grids, const double *const *cgrids, const int32_t *levels, const double *coeffs,
+                   int64_t num_grids, int32_t d, int32_t n, double *sparse, const double *csparse, int gather) {
+  int64_t *table = NULL;
+  const int64_t M = sg_table(d, n, &table);
+  if (M < 0) return -1;
+  if (gather)
+    for (int64_t m = 0; m < M; ++m) sparse[m] = 0.0;
+  for (int64_t g = 0; g < num_grids; ++g) {
+    const int32_t *l = levels + g * d;
+    int32_t sum = 0;
+    for (int32_t k = 0; k < d; ++k) sum += l[k];
+    if (sum > n || sgo_num_points(l, d) < 0) {
+      free(table);
+      return -1;
+    }
+    const int64_t N = sgo_num_points(l, d);
+    int64_t i[32];
+    for (int32_t k = 0; k < d; ++k) i[k] = 1;
+    for (int64_t p = 0; p < N; ++p) { /* row-major, x_1 fastest */
+      const int64_t s = sg_index(table, d, n, l, i);
+      if (gather) sparse[s] = sparse[s] + coeffs[g] * cgrids[g][p];
+      else grids[g][p] = csparse[s];
+      for (int32_t k = 0; k < d; ++k) {
+        if (++i[k] < ((int64_t)1 << l[k])) break;
+        i[k] = 1;
+      }
+    }
+  }
+  free(table);
+  return 0;
+}
+
+int sgo_gather(const double *const *grids, const int32_t *levels, const double *coeffs, int64_t num_grids,
+               int32_t d, int32_t n, double *sparse) {
+  if (!grids || !levels || !coeffs || !sparse) return -1;
+  return sg_walk(NULL, grids, levels, coeffs, num_grids, d, n, sparse, NULL, 1);
+}
+
+int sgo_scatter(double *const *grids, const int32_t *levels, int64_t num_grids, int32_t d, int32_t n,
+                const double *sparse) {
+  if (!grids || !levels || !sparse) return -1;
+  return sg_walk(grids, NULL, levels, NULL, num_grids, d, n, NULL, sparse, 0);
+}

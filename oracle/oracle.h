@@ -77,6 +77,31 @@ void sgo_fill_uniform(double *grid, int64_t n, uint64_t seed, uint64_t grid_id, 
 /* Order-independent digest: sum_i mix64(bits(v_i) ^ (i * 0x9E3779B97F4A7C15)) mod 2^64. */
 uint64_t sgo_digest(const double *grid, int64_t n, int64_t index_offset);
 
+/* ---- combination technique communication phase ----
+ * The sparse grid of level sum n is the set of hierarchical subspaces W_lam,
+ * lam_k >= 1, |lam|_1 <= n; a combination grid l holds exactly the
+ * subspaces lam <= l, its point (i_1..i_d) belonging to lam_k = l_k - tz(i_k),
+ * j_k = i_k >> (tz(i_k) + 1) (the predecessor structure of P:140).
+ * SG LAYOUT: subspaces by level sum ascending, then lexicographically ascending
+ * in (lam_1..lam_d); inside a subspace the 2^{lam_k - 1} odd points per axis,
+ * row-major with j_1 fastest (x_k = (2 j_k + 1) 2^{-lam_k}).
+ * The oracle enumerates the subspaces one by one (no counting formula); it
+ * supports n^d <= 2^26 (a dense lam -> offset table). */
+int64_t sgo_sparse_num_points(int32_t d, int32_t n);
+
+/* gather (the combination formula on hierarchical surpluses):
+ *   sparse = 0;  for g = 0..num_grids-1 in order:  for every point of grid g:
+ *     sparse[SG(lam, j)] = sparse[SG(lam, j)] + coeffs[g] * grid_g[point]
+ * (plain multiply then add; no FMA).  grids[g]: grid g's surpluses, levels
+ * row-major [num_grids][d].  Every grid must have |l_g|_1 <= n.  0 / -1. */
+int sgo_gather(const double *const *grids, const int32_t *levels, const double *coeffs, int64_t num_grids,
+               int32_t d, int32_t n, double *sparse);
+
+/* scatter: every point of every grid receives its sparse-grid value,
+ *   grid_g[point] = sparse[SG(lam, j)].  0 / -1. */
+int sgo_scatter(double *const *grids, const int32_t *levels, int64_t num_grids, int32_t d, int32_t n,
+                const double *sparse);
+
 #ifdef __cplusplus
 }
 #endif

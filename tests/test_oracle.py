@@ -6,6 +6,7 @@ DESIGN.md reading it pins.  A plausible mistake in the oracle (dropped term,
 wrong sign, wrong predecessor index, transposed axis, wrong level order) fails
 at least one of these; see test_negative_controls for explicit mutants.
 """
+import itertools
 import json
 import os
 
@@ -369,3 +370,110 @@ def test_bad_arguments():
     assert oracle.num_points([31, 31, 31]) == -1
     with pytest.raises(ValueError):
         oracle.hierarchize(np.zeros(3), [2], axis_order=[1])
+
+
+# ------------------------------------------- combination technique gather / scatter
+# (the communication phase the hierarchization serves)
+def _sg_subspaces(d, n):
+    """The SG layout by direct enumeration: subspaces lam >= 1, |lam|_1 <= n, level sum
+    ascending, then lexicographically ascending; returns [(lam, offset, size)]."""
+    out, off = [], 0
+    for s in range(d, n + 1):
+        for lam in sorted(c for c in itertools.product(range(1, s - d + 2), repeat=d) if sum(c) == s):
+            size = 1 << (s - d)
+            out.append((lam, off, size))
+            off += size
+    return out
+
+
+def _sg_point_coords(lam):
+    """Coordinates of the points of subspace lam in layout order (j_1 fastest)."""
+    axes = [(2 * np.arange(1 << (l - 1)) + 1) * 2.0 ** -l for l in lam]
+    mesh = np.meshgrid(*axes[::-1], indexing="ij")          # last axis slowest
+    return np.stack([m.ravel() for m in mesh[::-1]], axis=1)  # (points, d), x_1 fastest
+
+
+def _grid_coords(levels):
+    axes = [np.arange(1, 1 << l) * 2.0 ** -l for l in levels]
+    mesh = np.meshgrid(*axes[::-1], indexing="ij")
+    return np.stack([m.ravel() for m in mesh[::-1]], axis=1)
+
+
+@pytest.mark.parametrize("d,n", [(1, 6), (2, 2), (2, 7), (3, 6), (4, 9), (5, 8)])
+def test_sparse_layout_size(d, n):
+    assert oracle.sparse_num_points(d, n) == sum(sz for _, _, sz in _sg_subspaces(d, n))
+
+
+def _combi(d, n):
+    cs = si.combination_set(d, n)
+    return cs, [si.combination_coefficient(d, n, lv) for lv in cs]
+
+
+@pytest.mark.parametrize("d,n", [(2, 8), (3, 7), (4, 8)])
+def test_gather_closed_form_exact(d, n):
+    """f = prod x_k (1 - x_k) on every combination grid, hierarchized, gathered:
+    every sparse point gets prod 4^-lam_k EXACTLY -- the grids' surpluses are the
+    closed form (reading R11) and the coefficients of the grids holding W_lam sum
+    to 1 (the combination technique)."""
+    cs, co = _combi(d, n)
+    grids = [oracle.hierarchize(si.fill_smooth(lv), lv) for lv in cs]
+    sp = oracle.gather(grids, cs, co, n)
+    for lam, off, sz in _sg_subspaces(d, n):
+        assert np.all(sp[off:off + sz] == 4.0 ** -sum(lam)), lam
+
+
+def _hat(lam, x):
+    """phi_{lam,j}(x) for the unique j whose support holds x (0 elsewhere)."""
+    h = 2.0 ** -lam
+    j = np.floor(x / (2 * h)).astype(np.int64)
+    return j, np.maximum(0.0, 1.0 - np.abs(x - (2 * j + 1) * h) / h)
+
+
+@pytest.mark.parametrize("d,n", [(2, 7), (3, 6)])
+def test_gather_reproduces_sparse_interpolant(d, n):
+    """Random sparse-grid surpluses s; sample the sparse interpolant
+    f = sum s phi on every combination grid (direct hat evaluation, here),
+    hierarchize each grid (oracle), gather: the result is s again (the
+    combination formula is exact on the sparse grid space), up to rounding."""
+    rng = np.random.default_rng(5)
+    subs = _sg_subspaces(d, n)
+    s = rng.uniform(-1, 1, sum(sz for _, _, sz in subs))
+    cs, co = _combi(d, n)
+    grids = []
+    for lv in cs:
+        X = _grid_coords(lv)
+        f = np.zeros(len(X))
+        for lam, off, sz in subs:                     # one hat per subspace and point
+            w = np.ones(len(X))
+            idx = np.zeros(len(X), dtype=np.int64)
+            mul = 1
+            for k in range(d):
+                j, v = _hat(lam[k], X[:, k])
+                w *= v
+                idx += j * mul
+                mul <<= lam[k] - 1
+            f += w * s[off + idx]
+        grids.append(oracle.hierarchize(f, lv))
+    got = oracle.gather(grids, cs, co, n)
+    assert np.max(np.abs(got - s)) / np.max(np.abs(s)) <= 1e-13
+
+
+@pytest.mark.parametrize("d,n", [(2, 7), (3, 7), (4, 8)])
+def test_scatter_is_restriction(d, n):
+    """scatter: grid point x of grid l gets the sparse value of the subspace point
+    at x (found here by coordinates); then gather of the scattered surpluses
+    returns s (coefficients of the grids holding W_lam sum to 1)."""
+    rng = np.random.default_rng(6)
+    subs = _sg_subspaces(d, n)
+    s = rng.uniform(-1, 1, sum(sz for _, _, sz in subs))
+    where = {}
+    for lam, off, sz in subs:
+        for k, x in enumerate(_sg_point_coords(lam)):
+            where[tuple(x)] = off + k
+    cs, co = _combi(d, n)
+    out = oracle.scatter(s, cs, n)
+    for lv, g in zip(cs, out):
+        want = s[[where[tuple(x)] for x in _grid_coords(lv)]]
+        assert np.array_equal(g, want)
+    back = oracle.gather(out, cs, co, n)
+    assert np.max(np.abs(back - s)) / np.max(np.abs(s)) <= 1e-13   # rounding of the +-C(d-1,q) sums
