@@ -58,7 +58,7 @@ def peak_hbm():
 # ------------------------------------------------------------------ workload
 def workload(name):
     import sgh_inputs as si
-    if name == "C5":
+    if name in ("C5", "C5cycle"):
         cfg = si.CONFIGS["C5"]
         members = si.combination_set(cfg.d, cfg.n)
         desc = (f"C5: combination set d={cfg.d} n={cfg.n}, |l|_1 in {{{cfg.n},{cfg.n-1},{cfg.n-2},{cfg.n-3}}}, "
@@ -181,9 +181,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="C5", choices=["C5", "C2", "C3", "C4", "S1", "S10"],
+    ap.add_argument("--workload", default="C5", choices=["C5", "C2", "C3", "C4", "S1", "S10", "C5cycle"],
                     help="BASELINE.json configs C2..C5 (default C5, the metric's config); S1 / S10 are the "
-                         "paper's 1-D l=27 and 10-D (9,2,..,2) sweep tops (SURVEY 8(f))")
+                         "paper's 1-D l=27 and 10-D (9,2,..,2) sweep tops; C5cycle is the whole combination "
+                         "cycle on the C5 set: hierarchize, gather, scatter, dehierarchize (SURVEY 8(f))")
     ap.add_argument("--impl", default="sgh", choices=["sgh", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -242,12 +243,12 @@ def sgh_arm(args, rank, world, local_rank):
     members, ids, desc = workload(args.workload)
     sizes = [si.num_points(l) for l in members]
     sharded = args.workload == "C4" and world > 1
-    if args.workload == "C5" and world > 1:
+    if args.workload in ("C5", "C5cycle") and world > 1:
         part = si.lpt_partition(sizes, world)[rank]
         my_members, my_ids = [members[i] for i in part], [ids[i] for i in part]
     else:
         my_members, my_ids = members, ids
-    total_points = sum(sizes) if (args.workload == "C5" or sharded) else sum(sizes) * world
+    total_points = sum(sizes) if (args.workload in ("C5", "C5cycle") or sharded) else sum(sizes) * world
 
     def barrier():
         if world > 1:
@@ -277,6 +278,18 @@ def sgh_arm(args, rank, world, local_rank):
         batch.fill_uniform(si.SEED)
         fuse = not args.per_axis
         step = lambda: batch.transform(args.inverse, fuse=fuse)  # noqa: E731
+        if args.workload == "C5cycle":
+            cfg = si.CONFIGS["C5"]
+            coeffs = [float(si.combination_coefficient(cfg.d, cfg.n, lv)) for lv in my_members]
+            sparse = torch.empty(sgh.sparse_num_points(cfg.d, cfg.n), dtype=torch.float64, device=dev)
+
+            def step():
+                batch.hierarchize(fuse=fuse)
+                sgh.gather(batch.views, my_members, coeffs, cfg.n, sparse)
+                if world > 1:   # the combined surpluses are the sum over ranks (each holds some grids)
+                    dist.all_reduce(sparse)
+                sgh.scatter(sparse, batch.views, my_members, cfg.n)
+                batch.dehierarchize(fuse=fuse)
         my_points = batch.total_points
         deff_pts = sum(d_eff(l) * si.num_points(l) for l in my_members)
 
@@ -354,11 +367,11 @@ def sgh_arm(args, rank, world, local_rank):
 
     # e2e through the C ABI with host buffers
     e2e = None
-    if not args.no_e2e and not sharded:
+    if not args.no_e2e and not sharded and args.workload != "C5cycle":
         e2e = run_e2e(sgh, my_members, my_ids, dev, args.e2e_steps, world, rank)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload != "C5cycle":
         rate, sample, cores, _t, _n = oracle_rate(members, ids)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
 
@@ -366,12 +379,12 @@ def sgh_arm(args, rank, world, local_rank):
         metric = METRIC.replace("hierarchized", "dehierarchized") if args.inverse else METRIC
         out = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong"
-               if (args.workload == "C5" or sharded) else "weak", "vs_baseline": None, "dtype": "f64",
+               if (args.workload in ("C5", "C5cycle") or sharded) else "weak", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic",
                "config": {"workload": desc, "points": total_points, "bytes": 8 * total_points,
                           "l2": "inputs larger than L2 (no flush needed)" if 8 * total_points > 2 * 126e6
                           else "L2 not flushed; input < 2x L2",
-                          "parallelism": (f"grids LPT-balanced over {world} ranks" if args.workload == "C5"
+                          "parallelism": (f"grids LPT-balanced over {world} ranks" if args.workload in ("C5", "C5cycle")
                                           else ((f"sharded along x_d, {'halo + coarse-lattice all-gather' if args.sharded == 'halo' else 'NCCL all-to-all'}")
                                                 if sharded else "replicas")),
                           "seed": si.SEED},

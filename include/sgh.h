@@ -252,6 +252,43 @@ typedef struct {
 sgh_status sgh_profile_enable(int32_t on);
 int64_t sgh_profile_read(sgh_launch_record *out, int64_t capacity);
 
+/* ------------------------------- combination technique gather / scatter
+ * The communication phase the hierarchization exists for ("the
+ * hierarchical surpluses ... communicated").
+ * SPARSE GRID of level sum n: the hierarchical subspaces W_lam, lam_k >= 1,
+ * |lam|_1 <= n, stored in ONE device array in the SG LAYOUT: subspaces by level
+ * sum ascending, then lexicographically ascending in (lam_1..lam_d); inside
+ * W_lam its prod_k 2^{lam_k - 1} points row-major with j_1 fastest (point
+ * x_k = (2 j_k + 1) 2^{-lam_k}).  Grid l holds W_lam for lam <= l: its point
+ * (i_1..i_d) is (lam_k = l_k - tz(i_k), j_k = i_k >> (tz(i_k) + 1)).
+ * Limits: d <= SGH_MAX_D, n <= 62, every grid |l|_1 <= n and N < 2^31. */
+#define SGH_FLAG_SCATTER 8u   /* sgh_combi_workspace_bytes: size for sgh_scatter (default: sgh_gather) */
+
+/* Points of the sparse grid (sum over level sums s = d..n of C(s-1, d-1) 2^{s-d});
+ * -1 if (d, n) is unsupported. */
+int64_t sgh_sparse_num_points(int32_t d, int32_t n);
+
+/* Device workspace (task tables) of sgh_gather (flags 0) or sgh_scatter
+ * (SGH_FLAG_SCATTER) for these grids; 0 on invalid arguments. */
+size_t sgh_combi_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, int32_t n, uint32_t flags);
+
+/* GATHER: sparse[(lam, j)] = sum over the grids g holding W_lam, in the order
+ * given, of coeffs[g] * grids[g][point(lam, j)] (accumulated from +0.0, one
+ * rounded multiply and one rounded add per term: bitwise the oracle's
+ * grid-by-grid accumulation).  Subspaces held by no grid get 0.
+ *  grids:  host array of num_grids DEVICE pointers (hierarchical surpluses);
+ *  levels: host int32[num_grids][d];  coeffs: host double[num_grids] (the
+ *          combination coefficients (-1)^q C(d-1, q), or any weights);
+ *  sparse: device array of sgh_sparse_num_points(d, n) doubles (written). */
+sgh_status sgh_gather(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
+                      int64_t num_grids, int32_t n, double *sparse, void *workspace, size_t ws_bytes, void *stream);
+
+/* SCATTER: every point of every grid receives its sparse-grid value
+ * (restriction of the combined surpluses; dehierarchize the grids afterwards
+ * for nodal values). */
+sgh_status sgh_scatter(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, int32_t n,
+                       const double *sparse, void *workspace, size_t ws_bytes, void *stream);
+
 /* Host-only description of the plan the library would run for one grid with
  * these flags (no CUDA call): one line per pass ("pass k:"), then one line per
  * phase with its kernel kind, tile width, special axis / block level and the

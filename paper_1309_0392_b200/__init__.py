@@ -36,6 +36,7 @@ LIB_PATH = os.environ.get("SGH_LIB_PATH") or os.path.join(_HERE, "lib", "libsgh.
 FLAG_DEHIERARCHIZE = 1
 FLAG_PER_AXIS = 2
 FLAG_WHOLE_POLES = 4
+FLAG_SCATTER = 8
 STATUS = {0: "SGH_OK", 1: "SGH_ERR_INVALID_ARGUMENT", 2: "SGH_ERR_CAPACITY", 3: "SGH_ERR_CUDA",
           4: "SGH_ERR_NCCL", 5: "SGH_ERR_WORKSPACE"}
 
@@ -87,6 +88,11 @@ def _load():
         "sgh_digest_batched": (st, [vpp, i64p, ctypes.c_int64, u64p, vp, sz, vp]),
         "sgh_launch_count": (ctypes.c_uint64, []),
         "sgh_plan_describe": (ctypes.c_int64, [i32p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_char_p, sz]),
+        "sgh_sparse_num_points": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
+        "sgh_combi_workspace_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32]),
+        "sgh_gather": (st, [vpp, i32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64,
+                            ctypes.c_int32, vp, vp, sz, vp]),
+        "sgh_scatter": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, vp, vp, sz, vp]),
         "sgh_profile_enable": (st, [ctypes.c_int32]),
         "sgh_profile_read": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int64]),
         "sgh_status_string": (ctypes.c_char_p, [st]),
@@ -108,7 +114,8 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_sharded_halo_workspace_bytes",
             "sgh_transform_sharded_halo", "sgh_transform_sharded_halo_loopback", "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
-            "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe",
+            "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_sparse_num_points",
+            "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter",
             "sgh_status_string", "sgh_last_error", "sgh_version")
 
 
@@ -234,7 +241,7 @@ class _LaunchRecord(ctypes.Structure):
                 ("variant", ctypes.c_int32), ("bytes", ctypes.c_double), ("ms", ctypes.c_double)]
 
 
-KIND_NAMES = {0: "flat_slabs", 1: "flat_blocks", 2: "strided", 3: "reg", 4: "fused"}
+KIND_NAMES = {0: "flat_slabs", 1: "flat_blocks", 2: "strided", 3: "reg", 4: "fused", 5: "gather", 6: "scatter"}
 
 
 def profile_enable(on: bool = True):
@@ -489,3 +496,45 @@ def transform_sharded_halo_loopback(shards, levels, workspace: torch.Tensor, inv
                                                        ctypes.c_void_p(workspace.data_ptr()),
                                                        workspace.numel() * workspace.element_size(),
                                                        _stream(stream)))
+
+
+# ------------------------------------------- combination technique gather / scatter
+def sparse_num_points(d: int, n: int) -> int:
+    """Points of the sparse grid {W_lam : |lam|_1 <= n} in the SG layout (sgh.h)."""
+    return int(lib.sgh_sparse_num_points(int(d), int(n)))
+
+
+def _combi_common(grids, levels_list):
+    d = len(levels_list[0])
+    for g, lv in zip(grids, levels_list):
+        _grid_ptr(g, lv)
+    flat = _flat_levels(levels_list, d)
+    ptrs = (ctypes.c_void_p * len(grids))(*[g.data_ptr() for g in grids])
+    return d, flat, ptrs
+
+
+def gather(grids, levels_list, coeffs, n: int, sparse: torch.Tensor = None, stream=None) -> torch.Tensor:
+    """sparse = sum_g coeffs[g] * grids[g] (hierarchical surpluses) in the SG layout."""
+    d, flat, ptrs = _combi_common(grids, levels_list)
+    dev = grids[0].device
+    if sparse is None:
+        sparse = torch.empty(sparse_num_points(d, n), dtype=torch.float64, device=dev)
+    wsb = int(lib.sgh_combi_workspace_bytes(flat, d, len(grids), int(n), 0))
+    ws = torch.empty(max(wsb, 16) // 8 + 2, dtype=torch.float64, device=dev)
+    c = (ctypes.c_double * len(grids))(*[float(x) for x in coeffs])
+    with torch.cuda.device(dev):
+        _check(lib.sgh_gather(ptrs, flat, c, d, len(grids), int(n), ctypes.c_void_p(sparse.data_ptr()),
+                              ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
+    return sparse
+
+
+def scatter(sparse: torch.Tensor, grids, levels_list, n: int, stream=None):
+    """Every grid point gets its sparse-grid value (in place into ``grids``)."""
+    d, flat, ptrs = _combi_common(grids, levels_list)
+    dev = grids[0].device
+    wsb = int(lib.sgh_combi_workspace_bytes(flat, d, len(grids), int(n), FLAG_SCATTER))
+    ws = torch.empty(max(wsb, 16) // 8 + 2, dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        _check(lib.sgh_scatter(ptrs, flat, d, len(grids), int(n), ctypes.c_void_p(sparse.data_ptr()),
+                               ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
+    return grids

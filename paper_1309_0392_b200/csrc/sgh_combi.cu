@@ -1,0 +1,450 @@
+// sgh_combi.cu -- the communication phase of the combination technique that the
+// hierarchization exists for ("the combination technique
+// ... linear combination of the solutions on the anisotropic full grids",
+// P:77 "all combination grids are hierarchized in parallel ... communication",
+// P:86-88 hierarchical surpluses of nested grids).
+//
+// The sparse grid of level sum n is the set of hierarchical subspaces W_lam,
+// lam_k >= 1, |lam|_1 <= n.  A combination grid l holds exactly the subspaces
+// lam <= l; its point i (1-based per axis) is the point j of W_lam with
+// lam_k = l_k - tz(i_k), j_k = i_k >> (tz(i_k) + 1)  (predecessor rule).
+//
+// SG LAYOUT (include/sgh.h): subspaces by level sum s ascending, then
+// lexicographically ascending in (lam_1..lam_d); inside W_lam the
+// 2^{lam_k - 1} points per axis row-major with j_1 fastest.  All subspaces of
+// level sum s have 2^{s-d} points, so
+//   offset(lam) = sum_{s'<s} C(s'-1, d-1) 2^{s'-d} + rank_s(lam) 2^{s-d},
+//   rank_s(lam) = sum_k [ C(rem_k - 1, d-k-1) - C(rem_k - lam_k, d-k-1) ],
+// rem_k = s - lam_1 - .. - lam_{k-1} (the compositions of rem_k into d - k parts
+// whose first part is < lam_k, by the hockey-stick identity).
+//
+// gather:  sparse(lam, j) = sum over the grids g holding W_lam, in the given
+//          grid order, of coeff_g * alpha_g(point) -- a PULL per sparse point,
+//          accumulated sequentially from +0.0 with explicit __dmul_rn /
+//          __dadd_rn (no FMA), so the result is bitwise the oracle's
+//          "for g in order: sparse += coeff_g * alpha_g".
+// scatter: every grid point gets its sparse value (data movement only).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "../../include/sgh.h"
+#include "sgh_common.cuh"
+#include "sgh_plan.hpp"
+
+namespace sgh {
+
+constexpr int kCombiMaxN = 62;     // level sums up to 62 (binomial table rows)
+constexpr int kCombiPts = 1024;    // points per work item
+
+__constant__ int64_t c_binom[kCombiMaxN + 2][SGH_MAX_D + 1];
+
+struct CombiGrid {
+  double *grid;
+  double coeff;
+  int64_t N;
+  int8_t l[SGH_MAX_D];
+  FDiv fn[SGH_MAX_D];              // division by n_k = 2^{l_k} - 1 (scatter: unflatten)
+};
+
+struct CombiSub {                  // one subspace W_lam of the sparse grid
+  int64_t off;                     // its sparse offset (SG layout)
+  int64_t c0;                      // its contributing grids: contrib[c0 .. c0+nc)   (built on the device)
+  int32_t nc;
+  int32_t npts;                    // 2^{|lam|-d}
+  int8_t lam[SGH_MAX_D];
+};
+
+struct CombiArgs {
+  const CombiGrid *grids;
+  CombiSub *subs;
+  int32_t *contrib;                // grid indices, grouped per subspace, in grid order
+  const int64_t *prefix;           // tile prefix over subs (gather) or grids (scatter), items + 1 entries
+  int32_t items;                   // subspaces (gather) or grids (scatter)
+  int32_t num_grids;
+  int64_t tiles;
+  int64_t sbase[kCombiMaxN + 2];   // offset of the first subspace of level sum s
+  double *sparse;
+  int32_t d, n;
+};
+
+__device__ __forceinline__ int64_t sg_offset(const int8_t *lam, const CombiArgs &A) {
+  int s = 0;
+  for (int k = 0; k < A.d; ++k) s += lam[k];
+  int64_t rank = 0;
+  int rem = s;
+  for (int k = 0; k < A.d - 1; ++k) {
+    const int m = A.d - k - 1;
+    rank += c_binom[rem - 1][m] - c_binom[rem - lam[k]][m];
+    rem -= lam[k];
+  }
+  return A.sbase[s] + (rank << (s - A.d));
+}
+
+// owner item of tile q (tiles of a CTA increase): galloping search from the cursor
+__device__ __forceinline__ int combi_item(const CombiArgs &A, int idx, int64_t q) {
+  if (idx < 0) {
+    int lo = 0, hi = A.items - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&A.prefix[mid]) <= q) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  }
+  if (idx + 1 >= A.items || __ldg(&A.prefix[idx + 1]) > q) return idx;
+  int lo = idx + 1, step = 1, hi = lo + 1;
+  while (hi < A.items && __ldg(&A.prefix[hi]) <= q) {
+    lo = hi;
+    step <<= 1;
+    hi = lo + step;
+  }
+  if (hi > A.items) hi = A.items;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(&A.prefix[mid]) <= q) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// one warp per subspace: count (fill = false) or list (fill = true) the grids
+// holding it, in grid order (ballot + popc keeps the order)
+template <bool FILL>
+__global__ void __launch_bounds__(kThreads) k_contrib(const __grid_constant__ CombiArgs A) {
+  const int lane = threadIdx.x & 31;
+  for (int sidx = (blockIdx.x * kThreads + threadIdx.x) >> 5; sidx < A.items;
+       sidx += (gridDim.x * kThreads) >> 5) {
+    CombiSub &S = A.subs[sidx];
+    int64_t at = FILL ? S.c0 : 0;
+    int cnt = 0;
+    for (int g0 = 0; g0 < A.num_grids; g0 += 32) {
+      const int g = g0 + lane;
+      bool holds = g < A.num_grids;
+      for (int k = 0; k < A.d && holds; ++k) holds = S.lam[k] <= A.grids[g].l[k];
+      const unsigned m = __ballot_sync(0xffffffffu, holds);
+      if (FILL && holds) A.contrib[at + __popc(m & ((1u << lane) - 1))] = g;
+      at += __popc(m);
+      cnt += __popc(m);
+    }
+    if (!FILL && lane == 0) S.nc = cnt;
+  }
+}
+
+// exclusive scan of nc into c0 (one CTA; a few thousand subspaces)
+__global__ void __launch_bounds__(kThreads) k_contrib_scan(const __grid_constant__ CombiArgs A) {
+  __shared__ int64_t part[kThreads];
+  const int per = (A.items + kThreads - 1) / kThreads;
+  const int b = threadIdx.x * per, e = min(A.items, b + per);
+  int64_t acc = 0;
+  for (int i = b; i < e; ++i) acc += A.subs[i].nc;
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int t = 0; t < kThreads; ++t) {
+      const int64_t v = part[t];
+      part[t] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  acc = part[threadIdx.x];
+  for (int i = b; i < e; ++i) {
+    A.subs[i].c0 = acc;
+    acc += A.subs[i].nc;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ CombiArgs A) {
+  __shared__ CombiSub s_sub;
+  int idx = -1, cur = -1;
+  for (int64_t q = blockIdx.x; q < A.tiles; q += gridDim.x) {
+    idx = combi_item(A, idx, q);
+    if (idx != cur) {
+      __syncthreads();
+      if (threadIdx.x == 0) s_sub = A.subs[idx];
+      __syncthreads();
+      cur = idx;
+    }
+    const CombiSub &S = s_sub;
+    const int p0 = (int)(q - __ldg(&A.prefix[idx])) * kCombiPts;
+    const int np = min(kCombiPts, S.npts - p0);
+    for (int qq = threadIdx.x; qq < np; qq += kThreads) {
+      const int p = p0 + qq;
+      int j[SGH_MAX_D];
+      int rest = p;
+      for (int k = 0; k < A.d; ++k) {             // j_1 fastest
+        const int b = S.lam[k] - 1;
+        j[k] = rest & ((1 << b) - 1);
+        rest >>= b;
+      }
+      double sum = 0.0;
+      for (int c = 0; c < S.nc; ++c) {            // grid order (deterministic)
+        const CombiGrid &G = A.grids[__ldg(&A.contrib[S.c0 + c])];
+        int64_t gi = 0, stride = 1;
+        for (int k = 0; k < A.d; ++k) {
+          const int64_t i = int64_t(2 * j[k] + 1) << (G.l[k] - S.lam[k]);
+          gi += (i - 1) * stride;
+          stride *= (int64_t(1) << G.l[k]) - 1;
+        }
+        sum = __dadd_rn(sum, __dmul_rn(G.coeff, __ldg(G.grid + gi)));
+      }
+      A.sparse[S.off + p] = sum;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ CombiArgs A) {
+  int idx = -1;
+  for (int64_t q = blockIdx.x; q < A.tiles; q += gridDim.x) {
+    idx = combi_item(A, idx, q);
+    const CombiGrid &G = A.grids[idx];
+    const int64_t p0 = (q - __ldg(&A.prefix[idx])) * kCombiPts;
+    const int np = (int)min((int64_t)kCombiPts, G.N - p0);
+    for (int qq = threadIdx.x; qq < np; qq += kThreads) {
+      uint32_t rest = (uint32_t)(p0 + qq);       // N < 2^31 per grid (checked on the host)
+      int8_t lam[SGH_MAX_D];
+      int64_t in = 0;
+      int sh = 0;
+      for (int k = 0; k < A.d; ++k) {             // x_1 fastest
+        const uint32_t nk = (1u << G.l[k]) - 1;
+        const uint32_t qk = fdiv(rest, G.fn[k]);
+        const uint32_t i = rest - qk * nk + 1;    // 1-based
+        rest = qk;
+        const int t = __ffs(i) - 1;
+        lam[k] = (int8_t)(G.l[k] - t);
+        in += int64_t(i >> (t + 1)) << sh;
+        sh += lam[k] - 1;
+      }
+      G.grid[p0 + qq] = __ldg(A.sparse + sg_offset(lam, A) + in);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host
+static void init_binom() {
+  static std::once_flag once;
+  static int64_t tab[kCombiMaxN + 2][SGH_MAX_D + 1];
+  std::call_once(once, [] {
+    for (int a = 0; a < kCombiMaxN + 2; ++a)
+      for (int b = 0; b <= SGH_MAX_D; ++b) tab[a][b] = (b == 0) ? 1 : (a == 0 ? 0 : tab[a - 1][b - 1] + tab[a - 1][b]);
+  });
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemcpyToSymbol(c_binom, tab, sizeof tab);
+  done.push_back(dev);
+}
+
+static int64_t binom_host(int a, int b) {
+  if (b < 0 || a < b) return 0;
+  int64_t r = 1;
+  for (int i = 1; i <= b; ++i) r = r * (a - b + i) / i;
+  return r;
+}
+
+// offsets of the level-sum blocks; returns total points, -1 if invalid
+static int64_t sparse_bases(int d, int n, int64_t *sbase) {
+  if (d < 1 || d > SGH_MAX_D || n < d || n > kCombiMaxN) return -1;
+  int64_t acc = 0;
+  for (int s = 0; s <= n + 1 && s < kCombiMaxN + 2; ++s) {
+    if (sbase) sbase[s] = acc;
+    if (s >= d && s <= n) {
+      const int64_t cnt = binom_host(s - 1, d - 1);
+      if (s - d > 40 || cnt > (int64_t(1) << 40)) return -1;
+      acc += cnt << (s - d);
+    }
+  }
+  return acc;
+}
+
+// lexicographic successor of a composition of s into d positive parts
+static bool next_composition(int *lam, int d) {
+  int tail = lam[d - 1];                           // sum of positions k+1 .. d-1
+  for (int k = d - 2; k >= 0; --k) {
+    if (tail > d - 1 - k) {                        // position k can take 1 more
+      lam[k] += 1;
+      const int r = tail - 1;                      // remaining for positions k+1..d-1
+      for (int q = k + 1; q < d - 1; ++q) lam[q] = 1;
+      lam[d - 1] = r - (d - 2 - k);
+      return true;
+    }
+    tail += lam[k];
+  }
+  return false;
+}
+
+struct CombiPlan {
+  std::vector<CombiGrid> grids;
+  std::vector<CombiSub> subs;
+  std::vector<int64_t> prefix;
+  int64_t sbase[kCombiMaxN + 2];
+  int64_t M = 0;
+  int64_t ncontrib = 0;            // sum_g prod_k l_k: every (grid, subspace it holds) pair
+  // workspace: [grids][subs][prefix][contrib], each 256-byte aligned
+  size_t off_subs() const { return (grids.size() * sizeof(CombiGrid) + 255) / 256 * 256; }
+  size_t off_prefix() const { return off_subs() + (subs.size() * sizeof(CombiSub) + 255) / 256 * 256; }
+  size_t off_contrib() const { return off_prefix() + (prefix.size() * 8 + 255) / 256 * 256; }
+  size_t bytes() const { return off_contrib() + size_t(ncontrib) * 4 + 16; }
+};
+
+static sgh_status build_combi_plan(double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
+                                   int64_t num_grids, int32_t n, bool gather, CombiPlan &P) {
+  P.M = sparse_bases(d, n, P.sbase);
+  if (P.M < 0) return invalid("unsupported (d, n) for the sparse grid (d <= 16, n <= 62)");
+  if (num_grids >= (int64_t(1) << 31)) return invalid("too many grids");
+  P.grids.resize(num_grids);
+  P.ncontrib = 0;
+  for (int64_t g = 0; g < num_grids; ++g) {
+    int64_t N = 0;
+    sgh_status st = validate_levels(levels + g * d, d, &N);
+    if (st != SGH_OK) return st;
+    int sum = 0;
+    int64_t nsub = 1;
+    for (int k = 0; k < d; ++k) {
+      sum += levels[g * d + k];
+      nsub *= levels[g * d + k];
+    }
+    if (sum > n) return invalid("a grid's level sum exceeds the sparse grid's n");
+    if (N >= (int64_t(1) << 31)) return invalid("grid too large for gather/scatter (N >= 2^31)");
+    if (grids && !grids[g]) return invalid("grids[g] is NULL");
+    P.ncontrib += nsub;
+    CombiGrid &G = P.grids[g];
+    std::memset(&G, 0, sizeof G);
+    G.grid = grids ? grids[g] : nullptr;
+    G.coeff = coeffs ? coeffs[g] : 0.0;
+    G.N = N;
+    for (int k = 0; k < d; ++k) {
+      G.l[k] = (int8_t)levels[g * d + k];
+      G.fn[k] = make_fdiv((uint32_t)((1u << levels[g * d + k]) - 1));
+    }
+  }
+  int64_t acc = 0;
+  if (!gather) {
+    P.ncontrib = 0;
+    for (int64_t g = 0; g < num_grids; ++g) {
+      P.prefix.push_back(acc);
+      acc += (P.grids[g].N + kCombiPts - 1) / kCombiPts;
+    }
+    P.prefix.push_back(acc);
+    return SGH_OK;
+  }
+  std::vector<int> lam(d);
+  for (int s = d; s <= n; ++s) {                   // subspaces in SG order
+    for (int k = 0; k < d - 1; ++k) lam[k] = 1;
+    lam[d - 1] = s - (d - 1);
+    int64_t off = P.sbase[s];
+    do {
+      CombiSub S;
+      std::memset(&S, 0, sizeof S);
+      S.off = off;
+      S.npts = 1 << (s - d);
+      for (int k = 0; k < d; ++k) S.lam[k] = (int8_t)lam[k];
+      P.subs.push_back(S);
+      P.prefix.push_back(acc);
+      acc += (S.npts + kCombiPts - 1) / kCombiPts;
+      off += S.npts;
+    } while (next_composition(lam.data(), d));
+  }
+  P.prefix.push_back(acc);
+  if (P.subs.size() >= (size_t(1) << 31)) return invalid("too many subspaces");
+  return SGH_OK;
+}
+
+static sgh_status run_combi(double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
+                            int64_t num_grids, int32_t n, double *sparse, void *workspace, size_t ws_bytes,
+                            cudaStream_t s, bool gather) {
+  if (num_grids < 0) return invalid("num_grids < 0");
+  if (!levels || (num_grids > 0 && !grids) || !sparse || (gather && num_grids > 0 && !coeffs))
+    return invalid("NULL argument");
+  if (num_grids == 0 && !gather) return SGH_OK;
+  CombiPlan P;
+  sgh_status st = build_combi_plan(grids, levels, coeffs, d, num_grids, n, gather, P);
+  if (st != SGH_OK) return st;
+  const size_t need = P.bytes();
+  if (!workspace || ws_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 15)) {
+    set_error("workspace missing, misaligned or smaller than sgh_combi_workspace_bytes()");
+    return SGH_ERR_WORKSPACE;
+  }
+  init_binom();
+  const size_t up = P.off_contrib();               // tables uploaded; contrib is built on the device
+  std::vector<unsigned char> host(up, 0);
+  if (!P.grids.empty()) std::memcpy(host.data(), P.grids.data(), P.grids.size() * sizeof(CombiGrid));
+  if (!P.subs.empty()) std::memcpy(host.data() + P.off_subs(), P.subs.data(), P.subs.size() * sizeof(CombiSub));
+  std::memcpy(host.data() + P.off_prefix(), P.prefix.data(), P.prefix.size() * 8);
+  if ((st = staged_upload(workspace, host.data(), up, s)) != SGH_OK) return st;
+  unsigned char *ws = static_cast<unsigned char *>(workspace);
+  CombiArgs A;
+  std::memset(&A, 0, sizeof A);
+  A.grids = reinterpret_cast<const CombiGrid *>(ws);
+  A.subs = reinterpret_cast<CombiSub *>(ws + P.off_subs());
+  A.prefix = reinterpret_cast<const int64_t *>(ws + P.off_prefix());
+  A.contrib = reinterpret_cast<int32_t *>(ws + P.off_contrib());
+  A.items = gather ? (int32_t)P.subs.size() : (int32_t)P.grids.size();
+  A.num_grids = (int32_t)num_grids;
+  A.tiles = P.prefix.back();
+  std::memcpy(A.sbase, P.sbase, sizeof A.sbase);
+  A.sparse = sparse;
+  A.d = d;
+  A.n = n;
+  if (A.items == 0 || A.tiles == 0) return SGH_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaSuccess;
+  if (gather) {                                    // contributor lists, on the device
+    const int64_t warps_grid = std::min<int64_t>((A.items + 7) / 8, int64_t(sms) * 8);
+    k_contrib<false><<<(unsigned)warps_grid, kThreads, 0, s>>>(A);
+    k_contrib_scan<<<1, kThreads, 0, s>>>(A);
+    k_contrib<true><<<(unsigned)warps_grid, kThreads, 0, s>>>(A);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "contributor lists");
+    count_launch(3);
+  }
+  const int64_t grid = std::min<int64_t>(A.tiles, int64_t(sms) * 8);
+  ProfToken tok = prof_begin(s);
+  if (gather) k_gather<<<(unsigned)grid, kThreads, 0, s>>>(A);
+  else k_scatter<<<(unsigned)grid, kThreads, 0, s>>>(A);
+  e = cudaGetLastError();
+  double pts = 0;
+  for (const CombiGrid &G : P.grids) pts += double(G.N);
+  prof_end(tok, gather ? 5 : 6, 0, false, 8.0 * pts + 8.0 * double(P.M), s);
+  if (e != cudaSuccess) return cuda_fail(e, gather ? "gather launch" : "scatter launch");
+  count_launch();
+  return SGH_OK;
+}
+
+}  // namespace sgh
+
+using namespace sgh;
+
+extern "C" {
+
+int64_t sgh_sparse_num_points(int32_t d, int32_t n) { return sparse_bases(d, n, nullptr); }
+
+size_t sgh_combi_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, int32_t n, uint32_t flags) {
+  if (!levels || num_grids < 0) return 0;
+  CombiPlan P;
+  const bool gather = (flags & SGH_FLAG_SCATTER) == 0;
+  if (build_combi_plan(nullptr, levels, nullptr, d, num_grids, n, gather, P) != SGH_OK) return 0;
+  return P.bytes();
+}
+
+sgh_status sgh_gather(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
+                      int64_t num_grids, int32_t n, double *sparse, void *workspace, size_t ws_bytes, void *stream) {
+  return run_combi(const_cast<double *const *>(grids), levels, coeffs, d, num_grids, n, sparse, workspace, ws_bytes,
+                   static_cast<cudaStream_t>(stream), true);
+}
+
+sgh_status sgh_scatter(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, int32_t n,
+                       const double *sparse, void *workspace, size_t ws_bytes, void *stream) {
+  return run_combi(grids, levels, nullptr, d, num_grids, n, const_cast<double *>(sparse), workspace, ws_bytes,
+                   static_cast<cudaStream_t>(stream), false);
+}
+
+}  // extern "C"

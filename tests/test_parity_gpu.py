@@ -362,3 +362,50 @@ def test_launch_count_increases(sgh):
     sgh.hierarchize(g, [5, 5])
     torch.cuda.synchronize()
     assert sgh.launch_count() > before
+
+
+# --------------------------------------------- combination technique gather / scatter
+@pytest.mark.parametrize("d,n", [(1, 9), (2, 10), (3, 9), (4, 12), (5, 9), (4, 16)], ids=str)
+def test_gather_scatter_bitwise(sgh, d, n):
+    """gather (coefficient-weighted sum of the grids' surpluses into
+    the sparse grid, grid order) and scatter (restriction back to every grid),
+    on hierarchized random grids of the combination set: bitwise vs the oracle."""
+    cs = si.combination_set(d, n)
+    co = [float(si.combination_coefficient(d, n, lv)) for lv in cs]
+    hosts = [oracle.hierarchize(si.fill_uniform(si.num_points(lv), grid_id=g), lv) for g, lv in enumerate(cs)]
+    grids = [torch.from_numpy(h).cuda() for h in hosts]
+    sp = sgh.gather(grids, cs, co, n)
+    want = oracle.gather(hosts, cs, co, n)
+    assert sp.numel() == want.size == sgh.sparse_num_points(d, n)
+    assert_bitwise(sp.cpu().numpy(), want)
+    outs = [torch.full_like(g, float("nan")) for g in grids]
+    sgh.scatter(sp, outs, cs, n)
+    torch.cuda.synchronize()
+    for o, w in zip(outs, oracle.scatter(want, cs, n)):
+        assert_bitwise(o.cpu().numpy(), w)
+
+
+def test_gather_closed_form_c5_subset(sgh):
+    """f = prod x(1-x) on the largest members of the C5 set that fit the oracle
+    quickly... the full C5 set: every sparse point equals prod 4^-lam exactly
+    (coefficients of the grids holding W_lam sum to 1)."""
+    d, n = 4, 22
+    cs = si.combination_set(d, n)
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60e9:
+        pytest.skip("needs ~50 GB of device memory")
+    co = [float(si.combination_coefficient(d, n, lv)) for lv in cs]
+    b = sgh.GridBatch(cs)
+    for v, lv in zip(b.views, cs):
+        v.copy_(torch.from_numpy(si.fill_smooth(lv)))
+    b.hierarchize()
+    sp = sgh.gather(b.views, cs, co, n)
+    # expected: 4^-|lam|_1 per subspace, subspaces in SG order (level sum ascending)
+    import math
+    off = 0
+    for s in range(d, n + 1):
+        cnt = math.comb(s - 1, d - 1) << (s - d)
+        blk = sp[off:off + cnt]
+        assert bool((blk == 4.0 ** -s).all()), s
+        off += cnt
+    assert off == sp.numel()
