@@ -34,6 +34,12 @@
 
 namespace sgh {
 
+// threads of a FUSED CTA (tuning: SGH_FUSED_THREADS with FUSED_MINB CTAs per SM)
+#ifndef SGH_FUSED_THREADS
+#define SGH_FUSED_THREADS 256
+#endif
+constexpr int kFT = SGH_FUSED_THREADS;
+
 struct Src {
   const Task *tasks;      // device task table, or nullptr -> use `single`
   const int64_t *prefix;  // device exclusive prefix of task tiles, ntasks+1 entries
@@ -97,17 +103,18 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 
 // Copy len doubles gsrc[0..len) -> sdst[0..len) where sdst and gsrc have the
 // same 16-byte phase: 8-byte head/tail, 16-byte body.  Issue only.
+template <int NT = kThreads>
 __device__ __forceinline__ void copy_range_async(double *sdst, const double *gsrc, int len) {
   if (len <= 0) return;
   const int head = phase8(gsrc) ? 1 : 0;
   const int pairs = (len - head) >> 1;
   const int tail = len - head - 2 * pairs;
   if (head && threadIdx.x == 0) cp_async8(sdst, gsrc);
-  if (tail && threadIdx.x == kThreads - 1) cp_async8(sdst + len - 1, gsrc + len - 1);
+  if (tail && threadIdx.x == NT - 1) cp_async8(sdst + len - 1, gsrc + len - 1);
   const double *g = gsrc + head;
   double *s = sdst + head;
 #pragma unroll 4
-  for (int p = threadIdx.x; p < pairs; p += kThreads) cp_async16(s + 2 * p, g + 2 * p);
+  for (int p = threadIdx.x; p < pairs; p += NT) cp_async16(s + 2 * p, g + 2 * p);
 }
 
 // Task index owning tile q.  `idx` is the cursor from the previous tile of this
@@ -430,7 +437,7 @@ __device__ __forceinline__ void fused_load_rows_wide(double *sb, const double *g
   constexpr int LOGP = (NP == 32) ? 5 : 6;
   const int nslots = P * NP;
 #pragma unroll 4
-  for (int p = threadIdx.x; p < nslots; p += kThreads) {
+  for (int p = threadIdx.x; p < nslots; p += kFT) {
     const int r = p >> LOGP;
     const int k = p & (NP - 1);
     const int par = (par0 + r) & 1;
@@ -450,7 +457,7 @@ __device__ __forceinline__ void fused_load_rows(double *sb, const double *g, int
   constexpr int RS = W + 1;
   constexpr int NP = W / 2;                       // 16-byte slots per row
   constexpr int RPI = 32 / NP;                    // rows per warp instruction
-  constexpr int STEP = RPI * (kThreads / 32);     // rows per CTA iteration
+  constexpr int STEP = RPI * (kFT / 32);     // rows per CTA iteration
   const int lane = threadIdx.x & 31;
   const int k = lane % NP;
   int r = (threadIdx.x >> 5) * RPI + lane / NP;
@@ -513,9 +520,12 @@ __device__ __forceinline__ void pole_regs(double *p, int STR) {
 // nodal ends.  An end with !lo_ok / !hi_ok is the zero boundary: it is
 // never read and the update that would use it is skipped -- the same
 // operations as Alg. 1 on the whole pole, hence bitwise identical.
-template <int T, bool INV>
+// ENDS: both ends are known to be grid points (an interior block): the
+// boundary predicates fold away at compile time.
+template <int T, bool INV, bool ENDS = false>
 __device__ __forceinline__ void block_fine(double *p0, int STR, bool lo_ok, bool hi_ok) {
   constexpr int B = 1 << T;
+  if (ENDS) lo_ok = hi_ok = true;
   double v[B + 1];
   v[0] = lo_ok ? p0[0] : 0.0;
 #pragma unroll
@@ -555,13 +565,23 @@ __device__ __forceinline__ void block_fine(double *p0, int STR, bool lo_ok, bool
 #endif
 constexpr int kTB = SGH_TB;
 
+
 // One aligned block b of 2^kTB points of a (lattice) pole of nblk blocks: p0 is
 // the address of the virtual point j = 0 of the lattice (never dereferenced),
 // point j at p0[j*STR], n = 2^kTB nblk - 1 points; its ends are the boundary
 // only for the first / last block.  Writes only the block's fine points.
 template <bool INV>
 __device__ __forceinline__ void block_item(double *p0, int STR, int b, int nblk) {
-  block_fine<kTB, INV>(p0 + (b << kTB) * STR, STR, b > 0, b < nblk - 1);
+  if (b > 0 && b < nblk - 1) block_fine<kTB, INV, true>(p0 + (b << kTB) * STR, STR, true, true);
+  else block_fine<kTB, INV>(p0 + (b << kTB) * STR, STR, b > 0, b < nblk - 1);
+}
+
+// block b of a BLOCKED axis' sub-lattice: its ends are grid points unless it is
+// the first / last sub-block of a tile block that touches the boundary
+template <bool INV>
+__device__ __forceinline__ void block_item_ends(double *p0, int STR, bool lo, bool hi) {
+  if (lo && hi) block_fine<kTB, INV, true>(p0, STR, true, true);
+  else block_fine<kTB, INV>(p0, STR, lo, hi);
 }
 
 template <bool INV>
@@ -575,10 +595,10 @@ __device__ __forceinline__ void pole_regs_rt(double *p, int L, int STR) {
 }
 
 // Thread-strided walk over work items it = b * npoles + p (p fastest) without a
-// division per item: (b, p) advance by (kThreads / npoles, kThreads % npoles).
+// division per item: (b, p) advance by (kFT / npoles, kFT % npoles).
 struct ItemWalk {
   int np, db, dp, b0, p0;
-  __device__ __forceinline__ explicit ItemWalk(int npoles, int start = (int)threadIdx.x, int step = kThreads)
+  __device__ __forceinline__ explicit ItemWalk(int npoles, int start = (int)threadIdx.x, int step = kFT)
       : np(npoles) {
     db = step / npoles;
     dp = step - db * npoles;
@@ -617,22 +637,29 @@ struct HaloSkip {
 // the level-l pole, then on its coarse lattice (stride x2^kTB, level l-kTB),
 // ... until the lattice has l' <= 4, done as register poles.  A barrier between lattice
 // levels; hierarchization runs fine -> coarse, dehierarchization the reverse.
-template <bool INV, int W>
+// UNIT: the axis is the tile's first (R == 1): the point stride RS is a
+// compile-time constant (immediate SMEM offsets) and a pole index needs no division.
+template <bool INV, int W, bool UNIT = false>
 __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv fR, int Ok,
                                            const HaloSkip hs) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
+  if (UNIT) {
+    RS = (W == 1) ? 1 : W + 1;
+    R = 1;
+  }
   const int n = (1 << l) - 1;
   const int npoles = Ok * R * W;
   const int STR = R * RS;
   auto pole_row = [&](int p) -> int {
     const int rest = p >> LOGW;
+    if (UNIT) return rest * n;
     const int oo = (int)fdiv((uint32_t)rest, fR);
     const int rk = rest - oo * R;
     return oo * n * R + rk;
   };
   auto pole_base = [&](int p) -> double * { return sm + pole_row(p) * RS + (p & (W - 1)); };
   if (l <= 4) {
-    for (int p = threadIdx.x; p < npoles; p += kThreads) {
+    for (int p = threadIdx.x; p < npoles; p += kFT) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       pole_regs_rt<INV>(pole_base(p), l, STR);
     }
@@ -659,7 +686,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   auto lattice_phase = [&]() {
     if (lf <= 1) return;                         // a single point: no update
     const int m = 1 << (kTB * nlev);
-    for (int p = threadIdx.x; p < npoles; p += kThreads) {
+    for (int p = threadIdx.x; p < npoles; p += kFT) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       double *p0 = pole_base(p) - STR;           // virtual point 0
       pole_regs_rt<INV>(p0 + m * STR, lf, m * STR);
@@ -702,13 +729,13 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (t - kTB * k - kTB);
     for (int b = walk.b0, p = walk.p0; b < nblk; walk.next(b, p))
-      block_fine<kTB, INV>(pole_base(p) + (b << kTB) * m * STR, m * STR, lo_ok || b > 0, hi_ok || b < nblk - 1);
+      block_item_ends<INV>(pole_base(p) + (b << kTB) * m * STR, m * STR, lo_ok || b > 0, hi_ok || b < nblk - 1);
     __syncthreads();
   };
   auto top_phase = [&]() {
     if (tr == 0) return;                         // the top lattice is just the two ends
     const int m = 1 << (kTB * K);
-    for (int p = threadIdx.x; p < npoles; p += kThreads) {
+    for (int p = threadIdx.x; p < npoles; p += kFT) {
       if (tr == 1) block_fine<1, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else if (tr == 2 || kTB <= 3) block_fine<2, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else block_fine<(kTB > 3 ? 3 : 2), INV>(pole_base(p), m * STR, lo_ok, hi_ok);
@@ -840,11 +867,11 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
         const int lo = seg_lo(z, yy);
         double *gp = seg_g(z, yy);
         if (STORE) {
-          for (int e = threadIdx.x; e < len; e += kThreads) __stcg(gp + e, sm[lo + e]);
+          for (int e = threadIdx.x; e < len; e += kFT) __stcg(gp + e, sm[lo + e]);
         } else if (aligned) {
-          copy_range_async(sm + lo, gp, len);
+          copy_range_async<kFT>(sm + lo, gp, len);
         } else {
-          for (int e = threadIdx.x; e < len; e += kThreads) cp_async8(sm + lo + e, gp + e);
+          for (int e = threadIdx.x; e < len; e += kFT) cp_async8(sm + lo + e, gp + e);
         }
       }
     return;
@@ -857,7 +884,7 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
   const int logL = half > 16 ? 5 : half > 8 ? 4 : half > 4 ? 3 : half > 2 ? 2 : len > 1 ? 1 : 0;
   const int L = 1 << logL;
   const int lane = threadIdx.x & (L - 1);
-  const ItemWalk walk(nyw, (int)threadIdx.x >> logL, kThreads >> logL);
+  const ItemWalk walk(nyw, (int)threadIdx.x >> logL, kFT >> logL);
   if (!STORE && aligned && len > 1 && len <= 2 * L + 1) {   // straight-line: one 16-byte pair per lane
     const int c0 = 2 * lane;
     for (int z = walk.b0, yy = walk.p0; z < nz; walk.next(z, yy)) {
@@ -917,7 +944,7 @@ __device__ __forceinline__ void fused_rows_special(const Task &T, const FusedTil
   if (STORE) {
     constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
     constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
-    constexpr int STEP = RPI * (kThreads / 32);
+    constexpr int STEP = RPI * (kFT / 32);
     const int c0 = (W >= 32) ? lane : lane % W;
     for (int r = warp * RPI + ((W >= 32) ? 0 : lane / W); r < P; r += STEP) {
       double *gr;
@@ -934,7 +961,7 @@ __device__ __forceinline__ void fused_rows_special(const Task &T, const FusedTil
   constexpr int NP = W / 2;                        // 16-byte slots per row
   constexpr int RPI = (NP >= 32) ? 1 : 32 / NP;
   constexpr int SPL = (NP >= 32) ? NP / 32 : 1;    // slots per lane
-  constexpr int STEP = RPI * (kThreads / 32);
+  constexpr int STEP = RPI * (kFT / 32);
   const int k0 = (NP >= 32) ? lane : lane % NP;
   for (int r = warp * RPI + ((NP >= 32) ? 0 : lane / NP); r < P; r += STEP) {
     double *gr;
@@ -965,12 +992,15 @@ __device__ __forceinline__ void fused_rows_special(const Task &T, const FusedTil
 
 template <int W>
 __device__ __forceinline__ void fused_issue(const Task &T, const FusedTile &f, double *stage) {
+#ifdef SGH_DEBUG_NOMEMORY
+  return;                                         // timing experiment: compute only
+#endif
   if (T.bj >= 0) {
     if (W == 1) fused_segments<false>(T, f, stage + f.par);
     else fused_rows_special<(W == 1 ? 8 : W), false>(T, f, stage + f.par);
     return;
   }
-  if (W == 1) copy_range_async(stage + f.par, f.g, f.units * T.P);
+  if (W == 1) copy_range_async<kFT>(stage + f.par, f.g, f.units * T.P);
   else if (W >= 64) fused_load_rows_wide<(W >= 64 ? W : 64)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
   else fused_load_rows<(W == 1 || W >= 64 ? 8 : W)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
 }
@@ -1011,8 +1041,12 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     }
     const int n = (T.bj == j) ? T.ej : (1 << l) - 1;
     hs.on = blocked && INV && j < T.bj;             // nodal block ends stay as loaded
-    fused_axis<INV, W>(sm, RS, l, R, fR, rows_total / (n * R), hs);
+    if (R == 1) fused_axis<INV, W, true>(sm, RS, l, R, fR, rows_total / n, hs);
+    else fused_axis<INV, W>(sm, RS, l, R, fR, rows_total / (n * R), hs);
   }
+#ifdef SGH_DEBUG_NOMEMORY
+  return;                                         // timing experiment: compute only
+#endif
   if (T.bj >= 0) {
     if (W == 1) fused_segments<true>(T, f, sm);
     else fused_rows_special<(W == 1 ? 8 : W), true>(T, f, sm);
@@ -1026,12 +1060,12 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
         bulk_commit();
       }
     } else {
-      for (int e = threadIdx.x; e < rows_total; e += kThreads) __stcg(gbase + e, sm[e]);
+      for (int e = threadIdx.x; e < rows_total; e += kFT) __stcg(gbase + e, sm[e]);
     }
   } else {
     constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
     constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
-    constexpr int STEP = RPI * (kThreads / 32);
+    constexpr int STEP = RPI * (kFT / 32);
     const int lane = threadIdx.x & 31;
     const int c0 = (W >= 32) ? lane : lane % W;
     int row = (threadIdx.x >> 5) * RPI + ((W >= 32) ? 0 : lane / W);
@@ -1059,7 +1093,7 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
 #define FUSED_MINB2 2  // the same for the two-stage (double-buffered) variant
 #endif
 template <bool INV, int W, int STAGES>
-__global__ void __launch_bounds__(kThreads, (STAGES == 1 ? FUSED_MINB : FUSED_MINB2)) k_fused(const __grid_constant__ Src src) {
+__global__ void __launch_bounds__(kFT, (STAGES == 1 ? FUSED_MINB : FUSED_MINB2)) k_fused(const __grid_constant__ Src src) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Task s_task[2];                      // descriptors of the two in-flight tiles
   int64_t q = blockIdx.x;
@@ -1068,7 +1102,7 @@ __global__ void __launch_bounds__(kThreads, (STAGES == 1 ? FUSED_MINB : FUSED_MI
   auto stage_task = [&](Task *dst, const Task *from) {
     const uint64_t *a = reinterpret_cast<const uint64_t *>(from);
     uint64_t *b = reinterpret_cast<uint64_t *>(dst);
-    for (int i = threadIdx.x; i < (int)(sizeof(Task) / 8); i += kThreads) b[i] = a[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(Task) / 8); i += kFT) b[i] = a[i];
   };
   auto ref = [&](int64_t qq, int64_t &ql) -> const Task * {
     if (!src.tasks) {
@@ -1257,7 +1291,7 @@ size_t task_smem(const Task &t) {
 }
 
 // resident CTAs on the whole device for a kernel instance and smem size (cached)
-static int resident_ctas(KernelFn fn, size_t smem) {
+static int resident_ctas(KernelFn fn, size_t smem, int threads = kThreads) {
   int dev = 0;
   cudaGetDevice(&dev);
   struct Entry { KernelFn fn; int dev; size_t smem; int ctas; };
@@ -1270,7 +1304,7 @@ static int resident_ctas(KernelFn fn, size_t smem) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   }
   int ctas = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, kThreads, smem) != cudaSuccess || ctas < 1) ctas = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, threads, smem) != cudaSuccess || ctas < 1) ctas = 1;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int total = ctas * sms;
@@ -1293,11 +1327,12 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
     smem = size_t(fused_stages()) * src.stage_doubles * 8;
   }
-  const int64_t cap = resident_ctas(fn, smem);
+  const int nt = task.kind == KIND_FUSED ? kFT : kThreads;
+  const int64_t cap = resident_ctas(fn, smem, nt);
   const int64_t grid = task.tiles < cap ? task.tiles : cap;
   if (grid <= 0) return cudaSuccess;
   ProfToken tok = prof_begin(stream);
-  fn<<<(unsigned)grid, kThreads, smem, stream>>>(src);
+  fn<<<(unsigned)grid, nt, smem, stream>>>(src);
   cudaError_t e = cudaGetLastError();
   prof_end(tok, task.kind, task.kind == KIND_FUSED || task.kind == KIND_STRIDED ? task.W : task.l, inv,
            16.0 * task_points(task), stream, task_variant(task));
@@ -1320,11 +1355,12 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
     smem = size_t(fused_stages()) * src.stage_doubles * 8;
   }
-  const int64_t cap = resident_ctas(fn, smem);
+  const int nt = kind == KIND_FUSED ? kFT : kThreads;
+  const int64_t cap = resident_ctas(fn, smem, nt);
   const int64_t grid = total_tiles < cap ? total_tiles : cap;
   if (grid <= 0) return cudaSuccess;
   ProfToken tok = prof_begin(stream);
-  fn<<<(unsigned)grid, kThreads, smem, stream>>>(src);
+  fn<<<(unsigned)grid, nt, smem, stream>>>(src);
   cudaError_t e = cudaGetLastError();
   prof_end(tok, kind, kind == KIND_FUSED || kind == KIND_STRIDED ? w : l, inv, 16.0 * points, stream, variant);
   return e;
