@@ -176,6 +176,18 @@ static int fused_budget() {
   return T;
 }
 
+// W == 1 (contiguous) FUSED tile budget (kFusedT1); SGH_FUSED_T1 overrides
+// (experiments with smaller W == 1 CTAs, sgh_kernels.cu FT<1>)
+static int fused_budget_w1() {
+  static int T = -1;
+  if (T < 0) {
+    const char *e = getenv("SGH_FUSED_T1");
+    T = e ? atoi(e) : kFusedT1;
+    if (T < 1024 || T > 12288) T = kFusedT1;
+  }
+  return T;
+}
+
 static int fused_wmax() {
   static int wmax = -1;
   if (wmax < 0) {
@@ -216,13 +228,8 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
   t.O = O;
   t.l = levels[a];
   if (Sa == 1) {
-    static int t1 = -1;
-    if (t1 < 0) {
-      const char *e = getenv("SGH_FUSED_T1");  // tuning experiment override (contiguous tiles)
-      t1 = e ? atoi(e) : (int)kFusedT;
-      if (t1 < 1024 || t1 > 12288) t1 = (int)kFusedT;
-    }
-    if (P > kFusedT) return false;
+    const int t1 = fused_budget_w1();
+    if (P > t1) return false;
     t.W = 1;
     t.R = (int32_t)(std::max<int64_t>(t1, P) / P);
     t.OS = P;
@@ -255,7 +262,7 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
 // when a block tile reads them).  Returns false if no block of >= 4 points fits.
 static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a, int b, int j, int W,
                                std::vector<Task> &phases) {
-  const int64_t budget = fused_budget() + fused_budget() / 16;
+  const int64_t budget = W == 1 ? fused_budget_w1() + fused_budget_w1() / 16 : fused_budget() + fused_budget() / 16;
   if (b - a > 16 || b - a < 2 || levels[j] < 3) return false;
   int64_t Sa = 1, O = 1, Prest = 1, A = 1;
   for (int k = 0; k < a; ++k) Sa *= (int64_t(1) << levels[k]) - 1;
@@ -399,7 +406,7 @@ static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, 
   if (t1 < 2 || t2 < 2 || t1 >= la || t2 >= lb) return false;
   const int64_t na = (int64_t(1) << la) - 1, nb = (int64_t(1) << lb) - 1;
   const int64_t e1 = (int64_t(1) << t1) + 1, e2 = (int64_t(1) << t2) + 1;
-  if (e1 * e2 > fused_budget() + fused_budget() / 16) return false;
+  if (e1 * e2 > fused_budget_w1() + fused_budget_w1() / 16) return false;
   const size_t first = phases.size();
   Task t;
   std::memset(&t, 0, sizeof t);
@@ -436,7 +443,7 @@ static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, 
   phases.push_back(t);
   const int64_t s1 = int64_t(1) << t1, s2 = int64_t(1) << t2;
   const int64_t nla = (int64_t(1) << (la - t1)) - 1;   // coarse-a columns
-  if (nla * e2 > fused_budget() + fused_budget() / 16) {
+  if (nla * e2 > fused_budget_w1() + fused_budget_w1() / 16) {
     phases.resize(first);
     return false;
   }

@@ -29,7 +29,8 @@ constexpr int kFlatCap = kFlatT + kFlatMaxS + 2;
 constexpr int kStridedWMax = 128;  // STRIDED tile width W in {32, 64, 128} columns
 constexpr int kStridedTileDoubles = 8960;  // STRIDED tile budget: (2^t + 1) * (W + 2) doubles (70 KB)
 constexpr int kRegMaxL = 4;        // REG kernel: poles of up to 15 points in registers
-constexpr int kFusedT = 8192;      // FUSED tile budget per pipeline stage (doubles, excl. row padding)
+constexpr int kFusedT = 8192;      // FUSED W > 1 tile budget per pipeline stage (doubles, excl. row padding)
+constexpr int kFusedT1 = 8192;     // FUSED W == 1 tile budget (tuning: SGH_FUSED_T1)
 
 enum Kind : int32_t {
   KIND_FLAT_SLABS = 0,   // R whole slabs (o) per tile; needs PS==S, OS==n*S, n*S <= kFlatT

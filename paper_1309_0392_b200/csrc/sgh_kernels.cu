@@ -34,11 +34,21 @@
 
 namespace sgh {
 
-// threads of a FUSED CTA (tuning: SGH_FUSED_THREADS with FUSED_MINB CTAs per SM)
+// threads of a FUSED CTA, per tile kind (W == 1 contiguous / W > 1 column
+// tiles); default 256 threads, 3 CTAs per SM, 70 KB tiles for both.  Tuning
+// experiments: SGH_FUSED_THREADS(_W1), FUSED_MINB(_W1) with the planner's
+// SGH_FUSED_T(1) (128-thread W == 1 CTAs at 6 per SM run 3.78 vs 2.60 TB/s at
+// equal 35 KB tiles, but the smaller tiles cost passes: no net gain).
 #ifndef SGH_FUSED_THREADS
 #define SGH_FUSED_THREADS 256
 #endif
-constexpr int kFT = SGH_FUSED_THREADS;
+#ifndef SGH_FUSED_THREADS_W1
+#define SGH_FUSED_THREADS_W1 256
+#endif
+template <int W>
+struct FT {
+  static constexpr int v = (W == 1) ? SGH_FUSED_THREADS_W1 : SGH_FUSED_THREADS;
+};
 
 struct Src {
   const Task *tasks;      // device task table, or nullptr -> use `single`
@@ -437,7 +447,7 @@ __device__ __forceinline__ void fused_load_rows_wide(double *sb, const double *g
   constexpr int LOGP = (NP == 32) ? 5 : 6;
   const int nslots = P * NP;
 #pragma unroll 4
-  for (int p = threadIdx.x; p < nslots; p += kFT) {
+  for (int p = threadIdx.x; p < nslots; p += FT<W>::v) {
     const int r = p >> LOGP;
     const int k = p & (NP - 1);
     const int par = (par0 + r) & 1;
@@ -457,7 +467,7 @@ __device__ __forceinline__ void fused_load_rows(double *sb, const double *g, int
   constexpr int RS = W + 1;
   constexpr int NP = W / 2;                       // 16-byte slots per row
   constexpr int RPI = 32 / NP;                    // rows per warp instruction
-  constexpr int STEP = RPI * (kFT / 32);     // rows per CTA iteration
+  constexpr int STEP = RPI * (FT<W>::v / 32);     // rows per CTA iteration
   const int lane = threadIdx.x & 31;
   const int k = lane % NP;
   int r = (threadIdx.x >> 5) * RPI + lane / NP;
@@ -595,10 +605,10 @@ __device__ __forceinline__ void pole_regs_rt(double *p, int L, int STR) {
 }
 
 // Thread-strided walk over work items it = b * npoles + p (p fastest) without a
-// division per item: (b, p) advance by (kFT / npoles, kFT % npoles).
+// division per item: (b, p) advance by (step / npoles, step % npoles).
 struct ItemWalk {
   int np, db, dp, b0, p0;
-  __device__ __forceinline__ explicit ItemWalk(int npoles, int start = (int)threadIdx.x, int step = kFT)
+  __device__ __forceinline__ ItemWalk(int npoles, int start, int step)
       : np(npoles) {
     db = step / npoles;
     dp = step - db * npoles;
@@ -659,7 +669,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   };
   auto pole_base = [&](int p) -> double * { return sm + pole_row(p) * RS + (p & (W - 1)); };
   if (l <= 4) {
-    for (int p = threadIdx.x; p < npoles; p += kFT) {
+    for (int p = threadIdx.x; p < npoles; p += FT<W>::v) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       pole_regs_rt<INV>(pole_base(p), l, STR);
     }
@@ -672,7 +682,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
     levels[nlev++] = lf;
     lf -= kTB;
   }
-  const ItemWalk walk(npoles);
+  const ItemWalk walk(npoles, (int)threadIdx.x, FT<W>::v);
   auto block_phase = [&](int k) {                // k-th lattice level: stride 2^{kTB k}
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (levels[k] - kTB);
@@ -686,7 +696,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   auto lattice_phase = [&]() {
     if (lf <= 1) return;                         // a single point: no update
     const int m = 1 << (kTB * nlev);
-    for (int p = threadIdx.x; p < npoles; p += kFT) {
+    for (int p = threadIdx.x; p < npoles; p += FT<W>::v) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       double *p0 = pole_base(p) - STR;           // virtual point 0
       pole_regs_rt<INV>(p0 + m * STR, lf, m * STR);
@@ -724,7 +734,7 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
   };
   const int K = t / kTB;
   const int tr = t - kTB * K;
-  const ItemWalk walk(npoles);
+  const ItemWalk walk(npoles, (int)threadIdx.x, FT<W>::v);
   auto sub_phase = [&](int k) {
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (t - kTB * k - kTB);
@@ -735,7 +745,7 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
   auto top_phase = [&]() {
     if (tr == 0) return;                         // the top lattice is just the two ends
     const int m = 1 << (kTB * K);
-    for (int p = threadIdx.x; p < npoles; p += kFT) {
+    for (int p = threadIdx.x; p < npoles; p += FT<W>::v) {
       if (tr == 1) block_fine<1, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else if (tr == 2 || kTB <= 3) block_fine<2, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else block_fine<(kTB > 3 ? 3 : 2), INV>(pole_base(p), m * STR, lo_ok, hi_ok);
@@ -867,11 +877,11 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
         const int lo = seg_lo(z, yy);
         double *gp = seg_g(z, yy);
         if (STORE) {
-          for (int e = threadIdx.x; e < len; e += kFT) __stcg(gp + e, sm[lo + e]);
+          for (int e = threadIdx.x; e < len; e += FT<1>::v) __stcg(gp + e, sm[lo + e]);
         } else if (aligned) {
-          copy_range_async<kFT>(sm + lo, gp, len);
+          copy_range_async<FT<1>::v>(sm + lo, gp, len);
         } else {
-          for (int e = threadIdx.x; e < len; e += kFT) cp_async8(sm + lo + e, gp + e);
+          for (int e = threadIdx.x; e < len; e += FT<1>::v) cp_async8(sm + lo + e, gp + e);
         }
       }
     return;
@@ -884,7 +894,7 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
   const int logL = half > 16 ? 5 : half > 8 ? 4 : half > 4 ? 3 : half > 2 ? 2 : len > 1 ? 1 : 0;
   const int L = 1 << logL;
   const int lane = threadIdx.x & (L - 1);
-  const ItemWalk walk(nyw, (int)threadIdx.x >> logL, kFT >> logL);
+  const ItemWalk walk(nyw, (int)threadIdx.x >> logL, FT<1>::v >> logL);
   if (!STORE && aligned && len > 1 && len <= 2 * L + 1) {   // straight-line: one 16-byte pair per lane
     const int c0 = 2 * lane;
     for (int z = walk.b0, yy = walk.p0; z < nz; walk.next(z, yy)) {
@@ -944,7 +954,7 @@ __device__ __forceinline__ void fused_rows_special(const Task &T, const FusedTil
   if (STORE) {
     constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
     constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
-    constexpr int STEP = RPI * (kFT / 32);
+    constexpr int STEP = RPI * (FT<W>::v / 32);
     const int c0 = (W >= 32) ? lane : lane % W;
     for (int r = warp * RPI + ((W >= 32) ? 0 : lane / W); r < P; r += STEP) {
       double *gr;
@@ -961,7 +971,7 @@ __device__ __forceinline__ void fused_rows_special(const Task &T, const FusedTil
   constexpr int NP = W / 2;                        // 16-byte slots per row
   constexpr int RPI = (NP >= 32) ? 1 : 32 / NP;
   constexpr int SPL = (NP >= 32) ? NP / 32 : 1;    // slots per lane
-  constexpr int STEP = RPI * (kFT / 32);
+  constexpr int STEP = RPI * (FT<W>::v / 32);
   const int k0 = (NP >= 32) ? lane : lane % NP;
   for (int r = warp * RPI + ((NP >= 32) ? 0 : lane / NP); r < P; r += STEP) {
     double *gr;
@@ -1000,7 +1010,7 @@ __device__ __forceinline__ void fused_issue(const Task &T, const FusedTile &f, d
     else fused_rows_special<(W == 1 ? 8 : W), false>(T, f, stage + f.par);
     return;
   }
-  if (W == 1) copy_range_async<kFT>(stage + f.par, f.g, f.units * T.P);
+  if (W == 1) copy_range_async<FT<1>::v>(stage + f.par, f.g, f.units * T.P);
   else if (W >= 64) fused_load_rows_wide<(W >= 64 ? W : 64)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
   else fused_load_rows<(W == 1 || W >= 64 ? 8 : W)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
 }
@@ -1060,12 +1070,12 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
         bulk_commit();
       }
     } else {
-      for (int e = threadIdx.x; e < rows_total; e += kFT) __stcg(gbase + e, sm[e]);
+      for (int e = threadIdx.x; e < rows_total; e += FT<1>::v) __stcg(gbase + e, sm[e]);
     }
   } else {
     constexpr int RPI = (W >= 32) ? 1 : 32 / W;   // rows per warp instruction
     constexpr int CPL = (W >= 32) ? W / 32 : 1;   // columns per lane
-    constexpr int STEP = RPI * (kFT / 32);
+    constexpr int STEP = RPI * (FT<W>::v / 32);
     const int lane = threadIdx.x & 31;
     const int c0 = (W >= 32) ? lane : lane % W;
     int row = (threadIdx.x >> 5) * RPI + ((W >= 32) ? 0 : lane / W);
@@ -1087,13 +1097,16 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
 // the cp.async copies of tile k+1 fill the other, so HBM reads overlap the
 // SMEM work instead of alternating with it.
 #ifndef FUSED_MINB
-#define FUSED_MINB 3   // resident CTAs per SM the FUSED register budget is sized for
+#define FUSED_MINB 3   // resident CTAs per SM the FUSED register budget is sized for (W > 1)
+#endif
+#ifndef FUSED_MINB_W1
+#define FUSED_MINB_W1 3  // the same for the W == 1 kernels
 #endif
 #ifndef FUSED_MINB2
 #define FUSED_MINB2 2  // the same for the two-stage (double-buffered) variant
 #endif
 template <bool INV, int W, int STAGES>
-__global__ void __launch_bounds__(kFT, (STAGES == 1 ? FUSED_MINB : FUSED_MINB2)) k_fused(const __grid_constant__ Src src) {
+__global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_W1 : FUSED_MINB) : FUSED_MINB2)) k_fused(const __grid_constant__ Src src) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Task s_task[2];                      // descriptors of the two in-flight tiles
   int64_t q = blockIdx.x;
@@ -1102,7 +1115,7 @@ __global__ void __launch_bounds__(kFT, (STAGES == 1 ? FUSED_MINB : FUSED_MINB2))
   auto stage_task = [&](Task *dst, const Task *from) {
     const uint64_t *a = reinterpret_cast<const uint64_t *>(from);
     uint64_t *b = reinterpret_cast<uint64_t *>(dst);
-    for (int i = threadIdx.x; i < (int)(sizeof(Task) / 8); i += kFT) b[i] = a[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(Task) / 8); i += FT<W>::v) b[i] = a[i];
   };
   auto ref = [&](int64_t qq, int64_t &ql) -> const Task * {
     if (!src.tasks) {
@@ -1327,7 +1340,7 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
     smem = size_t(fused_stages()) * src.stage_doubles * 8;
   }
-  const int nt = task.kind == KIND_FUSED ? kFT : kThreads;
+  const int nt = task.kind == KIND_FUSED ? (task.W == 1 ? FT<1>::v : FT<8>::v) : kThreads;
   const int64_t cap = resident_ctas(fn, smem, nt);
   const int64_t grid = task.tiles < cap ? task.tiles : cap;
   if (grid <= 0) return cudaSuccess;
@@ -1355,7 +1368,7 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
     smem = size_t(fused_stages()) * src.stage_doubles * 8;
   }
-  const int nt = kind == KIND_FUSED ? kFT : kThreads;
+  const int nt = kind == KIND_FUSED ? (w == 1 ? FT<1>::v : FT<8>::v) : kThreads;
   const int64_t cap = resident_ctas(fn, smem, nt);
   const int64_t grid = total_tiles < cap ? total_tiles : cap;
   if (grid <= 0) return cudaSuccess;
