@@ -72,17 +72,20 @@ struct CombiArgs {
   int32_t d, n;
 };
 
-__device__ __forceinline__ int64_t sg_offset(const int8_t *lam, const CombiArgs &A) {
+// binom / sbase: the tables staged in SMEM (lanes index them with different
+// values; constant-bank reads would serialise)
+__device__ __forceinline__ int64_t sg_offset(const int8_t *lam, int d, const int64_t (*binom)[SGH_MAX_D + 1],
+                                             const int64_t *sbase) {
   int s = 0;
-  for (int k = 0; k < A.d; ++k) s += lam[k];
+  for (int k = 0; k < d; ++k) s += lam[k];
   int64_t rank = 0;
   int rem = s;
-  for (int k = 0; k < A.d - 1; ++k) {
-    const int m = A.d - k - 1;
-    rank += c_binom[rem - 1][m] - c_binom[rem - lam[k]][m];
+  for (int k = 0; k < d - 1; ++k) {
+    const int m = d - k - 1;
+    rank += binom[rem - 1][m] - binom[rem - lam[k]][m];
     rem -= lam[k];
   }
-  return A.sbase[s] + (rank << (s - A.d));
+  return sbase[s] + (rank << (s - d));
 }
 
 // owner item of tile q (tiles of a CTA increase): galloping search from the cursor
@@ -198,6 +201,12 @@ __global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ Com
 }
 
 __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ CombiArgs A) {
+  __shared__ int64_t s_binom[kCombiMaxN + 2][SGH_MAX_D + 1];
+  __shared__ int64_t s_sbase[kCombiMaxN + 2];
+  for (int i = threadIdx.x; i < (kCombiMaxN + 2) * (SGH_MAX_D + 1); i += kThreads)
+    (&s_binom[0][0])[i] = (&c_binom[0][0])[i];
+  for (int i = threadIdx.x; i < kCombiMaxN + 2; i += kThreads) s_sbase[i] = A.sbase[i];
+  __syncthreads();
   int idx = -1;
   for (int64_t q = blockIdx.x; q < A.tiles; q += gridDim.x) {
     idx = combi_item(A, idx, q);
@@ -219,7 +228,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Co
         in += int64_t(i >> (t + 1)) << sh;
         sh += lam[k] - 1;
       }
-      G.grid[p0 + qq] = __ldg(A.sparse + sg_offset(lam, A) + in);
+      G.grid[p0 + qq] = __ldg(A.sparse + sg_offset(lam, A.d, s_binom, s_sbase) + in);
     }
   }
 }

@@ -409,3 +409,28 @@ def test_gather_closed_form_c5_subset(sgh):
         assert bool((blk == 4.0 ** -s).all()), s
         off += cnt
     assert off == sp.numel()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_shapes_fuzz(sgh, seed, monkeypatch):
+    """Planner fuzz: random level vectors (d = 1..6, up to ~2 M points) under every
+    plan family -- automatic, whole-pole fusion only, per axis, forced two-blocked
+    -- hierarchize and dehierarchize, bitwise vs the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    done = 0
+    while done < 12:
+        d = int(rng.integers(1, 7))
+        lv = tuple(int(x) for x in rng.integers(1, 15 - 2 * d if d < 6 else 4, size=d))
+        N = si.num_points(lv)
+        if N > 2_000_000:
+            continue
+        done += 1
+        u = si.fill_uniform(N, grid_id=done + 100 * seed)
+        want_h = oracle.hierarchize(u.copy(), lv)
+        want_d = oracle.dehierarchize(u.copy(), lv)
+        for fuse in (True, "whole", False):
+            assert_bitwise(gpu_transform(sgh, u, lv, fuse=fuse, guard=64), want_h)
+            assert_bitwise(gpu_transform(sgh, u, lv, inverse=True, fuse=fuse, guard=64), want_d)
+        monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
+        assert_bitwise(gpu_transform(sgh, u, lv, guard=64), want_h)
+        monkeypatch.delenv("SGH_TWO_BLOCKED")
