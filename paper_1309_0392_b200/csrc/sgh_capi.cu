@@ -171,7 +171,7 @@ static int fused_budget() {
   if (T < 0) {
     const char *e = getenv("SGH_FUSED_T");  // tuning experiment override
     T = e ? atoi(e) : kFusedT;
-    if (T < 1024 || T > 12288) T = kFusedT;
+    if (T < 1024 || T > 14336) T = kFusedT;
   }
   return T;
 }
@@ -183,7 +183,7 @@ static int fused_budget_w1() {
   if (T < 0) {
     const char *e = getenv("SGH_FUSED_T1");
     T = e ? atoi(e) : kFusedT1;
-    if (T < 1024 || T > 12288) T = kFusedT1;
+    if (T < 1024 || T > 14336) T = kFusedT1;
   }
   return T;
 }

@@ -712,6 +712,58 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   }
 }
 
+// Hierarchization of a W == 1 tile's FIRST axis (rows contiguous in SMEM,
+// levels 5..9) without CTA barriers: one warp per row, the one-pass stencil
+// (SURVEY 8(a)): every lane reads its points i = lane + 1 + 32 m and their two
+// predecessors i -+ 2^{tz(i)} -- all values entering the pass -- then, after a
+// __syncwarp, writes them.  The warp owns its row, so no other warp races it;
+// the same operations as Alg. 1 per point (bitwise).
+template <int C>
+__device__ __forceinline__ void warp_rows_hier(double *sm, int nrows, int l) {
+  const int lane = threadIdx.x & 31;
+  const int n = (1 << l) - 1;
+  for (int r = threadIdx.x >> 5; r < nrows; r += FT<1>::v / 32) {
+    double *row = sm + r * n;                      // point i (1-based) at row[i - 1]
+    double out[C];
+#pragma unroll
+    for (int m = 0; m < C; ++m) {
+      const int i = lane + 1 + 32 * m;
+      const int s = i & -i;
+      if (i <= n) {
+        double x = row[i - 1];
+        if (i - s >= 1) x = x - 0.5 * row[i - s - 1];   // left predecessor
+        if (i + s <= n) x = x - 0.5 * row[i + s - 1];   // right predecessor
+        out[m] = x;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < C; ++m) {
+      const int i = lane + 1 + 32 * m;
+      if (i <= n) row[i - 1] = out[m];
+    }
+    __syncwarp();
+  }
+}
+
+#ifndef SGH_WARP_ROWS_MAXL
+#define SGH_WARP_ROWS_MAXL 7
+#endif
+__device__ __forceinline__ bool warp_rows_dispatch(double *sm, int nrows, int l) {
+  switch (l) {
+    case 5: warp_rows_hier<1>(sm, nrows, l); return true;
+    case 6: warp_rows_hier<2>(sm, nrows, l); return true;
+    case 7: warp_rows_hier<4>(sm, nrows, l); return true;
+#if SGH_WARP_ROWS_MAXL >= 8
+    case 8: warp_rows_hier<8>(sm, nrows, l); return true;
+#endif
+#if SGH_WARP_ROWS_MAXL >= 9
+    case 9: warp_rows_hier<16>(sm, nrows, l); return true;
+#endif
+    default: return false;
+  }
+}
+
 // The BLOCKED axis of a tile: every pole holds one aligned block of 2^t points
 // plus its two ends (local y = 0..2^t, point stride R*RS); only the fine points
 // y = 1..2^t-1 are transformed.  Inside the block the same
@@ -1051,6 +1103,12 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     }
     const int n = (T.bj == j) ? T.ej : (1 << l) - 1;
     hs.on = blocked && INV && j < T.bj;             // nodal block ends stay as loaded
+#ifdef SGH_WARP_ROWS   // experiment (off): inlining it costs spills elsewhere in k_fused (C5 117 vs 130)
+    if (W == 1 && !INV && R == 1 && !hs.on && warp_rows_dispatch(sm, rows_total / n, l)) {
+      __syncthreads();                              // the next axis reads other rows
+      continue;
+    }
+#endif
     if (R == 1) fused_axis<INV, W, true>(sm, RS, l, R, fR, rows_total / n, hs);
     else fused_axis<INV, W>(sm, RS, l, R, fR, rows_total / (n * R), hs);
   }
@@ -1314,7 +1372,13 @@ static int resident_ctas(KernelFn fn, size_t smem, int threads = kThreads) {
     if (cache[i].fn == fn && cache[i].dev == dev && cache[i].smem == smem) return cache[i].ctas;
   if (smem > 48 * 1024) {
     // opt in to large dynamic shared memory (FUSED tiles up to ~70 KB)
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    // the device's opt-in maximum minus the kernel's static shared memory
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    size_t stat = 0;
+    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) stat = fa.sharedSizeBytes;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(optin - (int)stat));
   }
   int ctas = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, threads, smem) != cudaSuccess || ctas < 1) ctas = 1;
