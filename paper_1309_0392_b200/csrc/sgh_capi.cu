@@ -778,11 +778,14 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
     }
     for (size_t j = 0; j < maxp; ++j) {
       // group phase j of all grids by kernel instance (kind, and l for REG)
-      std::map<std::tuple<int, int, int>, std::vector<const Task *>> groups;
+      // SGH_SPLIT_VARIANTS=1 (profiling): dense / blocked / lattice FUSED tasks in separate launches
+      static const bool split = getenv("SGH_SPLIT_VARIANTS") != nullptr;
+      std::map<std::tuple<int, int, int, int>, std::vector<const Task *>> groups;
       for (int64_t g = 0; g < num_grids; ++g)
         if (j < per[g].size()) {
           const Task &t = per[g][j];
-          groups[{t.kind, t.kind == KIND_REG ? t.l : 0, (t.kind == KIND_STRIDED || t.kind == KIND_FUSED) ? t.W : 0}]
+          groups[{t.kind, t.kind == KIND_REG ? t.l : 0, (t.kind == KIND_STRIDED || t.kind == KIND_FUSED) ? t.W : 0,
+                  split ? task_variant(t) : 0}]
               .push_back(&t);
         }
       for (auto &kv : groups) {
