@@ -198,6 +198,21 @@ static int fused_wmax() {
   return wmax;
 }
 
+// per-axis constants of a full FUSED tile (Task::gOk, Task::fNP)
+static void finish_fused(Task &t) {
+  const int64_t rows = int64_t(t.P) * ((t.W == 1 && t.bj < 0) ? t.R : 1);
+  const int Wc = t.W == 1 ? 1 : t.W;
+  for (int j = 0; j < t.m; ++j) {
+    int64_t e = (int64_t(1) << t.gl[j]) - 1;
+    if (t.bj >= 0 && j == t.bj) e = t.ej;
+    if (t.bj >= 0 && t.bt2 >= 0 && j == t.bj + 1) e = (int64_t(1) << t.bt2) + 1;
+    const int64_t ok = rows / (e * t.gR[j]);
+    t.gOk[j] = (int32_t)ok;
+    const int64_t np = ok * t.gR[j] * Wc;
+    t.fNP[j] = make_fdiv((uint32_t)std::max<int64_t>(1, np));
+  }
+}
+
 static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, int b, Task &t) {
   const int64_t kFusedT = fused_budget();
   int64_t Sa = 1, P = 1, O = 1;
@@ -234,6 +249,7 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
     t.R = (int32_t)(std::max<int64_t>(t1, P) / P);
     t.OS = P;
     t.tiles = (O + t.R - 1) / t.R;
+    finish_fused(t);
     return true;
   }
   // widest tile that fits: long contiguous row segments keep DRAM efficient
@@ -246,6 +262,7 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
   t.OS = P * Sa;
   t.ncb = (Sa + W - 1) / W;
   t.tiles = O * t.ncb;
+  finish_fused(t);
   return true;
 }
 
@@ -336,6 +353,7 @@ static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a
     t.ncb = (W > 1) ? (Sa + W - 1) / W : 1;
     t.tiles = (O << t.nb_log) * t.ncb;
     if (lj <= 1 && busy - (levels[j] > 1) == 0) break;   // nothing left to transform
+    finish_fused(t);
     phases.push_back(t);
     if (!blocked) break;
     base += ((int64_t(1) << bt) - 1) * Gj;            // first lattice point i = 2^bt
@@ -440,6 +458,7 @@ static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, 
   t.nb2_log = lb - t2;
   t.ncb = 1;
   t.tiles = int64_t(1) << (t.nb_log + t.nb2_log);
+  finish_fused(t);
   phases.push_back(t);
   const int64_t s1 = int64_t(1) << t1, s2 = int64_t(1) << t2;
   const int64_t nla = (int64_t(1) << (la - t1)) - 1;   // coarse-a columns
@@ -464,6 +483,7 @@ static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, 
   c.Gj = s1;
   c.aligned = 0;
   c.tiles = int64_t(1) << c.nb2_log;
+  finish_fused(c);
   phases.push_back(c);
   // 3: the a-lattice on the coarse-b rows (the points coarse along both axes)
   plan_view(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, s1, 1, (s2 - 1) * na + s1 - 1, la - t1, phases);

@@ -118,6 +118,12 @@ struct Task {
   uint32_t skipmask;
   int32_t O1;
   int64_t OS2;
+  // per-axis constants of a FULL tile (R units / one special box), precomputed
+  // on the host so a tile needs no integer division: gOk[j] = tile rows /
+  // (extent_j gR[j]) (outer pole index count), fNP[j] = division by the
+  // number of poles gOk[j] gR[j] W
+  int32_t gOk[16];
+  FDiv fNP[16];
 };
 
 static_assert(sizeof(Task) % 8 == 0, "Task must stay 8-byte aligned");

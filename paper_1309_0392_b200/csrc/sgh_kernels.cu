@@ -608,11 +608,16 @@ __device__ __forceinline__ void pole_regs_rt(double *p, int L, int STR) {
 // division per item: (b, p) advance by (step / npoles, step % npoles).
 struct ItemWalk {
   int np, db, dp, b0, p0;
-  __device__ __forceinline__ ItemWalk(int npoles, int start, int step)
+  __device__ __forceinline__ ItemWalk(int npoles, int start, int step, const FDiv *f = nullptr)
       : np(npoles) {
-    db = step / npoles;
+    if (f) {                                      // host-precomputed division by npoles
+      db = (int)fdiv((uint32_t)step, *f);
+      b0 = (int)fdiv((uint32_t)start, *f);
+    } else {
+      db = step / npoles;
+      b0 = start / npoles;
+    }
     dp = step - db * npoles;
-    b0 = start / npoles;
     p0 = start - b0 * npoles;
   }
   __device__ __forceinline__ void next(int &b, int &p) const {
@@ -651,7 +656,7 @@ struct HaloSkip {
 // compile-time constant (immediate SMEM offsets) and a pole index needs no division.
 template <bool INV, int W, bool UNIT = false>
 __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv fR, int Ok,
-                                           const HaloSkip hs) {
+                                           const HaloSkip hs, const FDiv *fnp = nullptr) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   if (UNIT) {
     RS = (W == 1) ? 1 : W + 1;
@@ -682,7 +687,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
     levels[nlev++] = lf;
     lf -= kTB;
   }
-  const ItemWalk walk(npoles, (int)threadIdx.x, FT<W>::v);
+  const ItemWalk walk(npoles, (int)threadIdx.x, FT<W>::v, fnp);
   auto block_phase = [&](int k) {                // k-th lattice level: stride 2^{kTB k}
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (levels[k] - kTB);
@@ -772,7 +777,7 @@ __device__ __forceinline__ bool warp_rows_dispatch(double *sm, int nrows, int l)
 // lo_ok / hi_ok: the block's ends are grid points (false: the zero boundary).
 template <bool INV, int W>
 __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int R, const FDiv fR, int Ok,
-                                                 bool lo_ok, bool hi_ok) {
+                                                 bool lo_ok, bool hi_ok, const FDiv *fnp = nullptr) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   const int ej = (1 << t) + 1;
   const int npoles = Ok * R * W;
@@ -786,7 +791,7 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
   };
   const int K = t / kTB;
   const int tr = t - kTB * K;
-  const ItemWalk walk(npoles, (int)threadIdx.x, FT<W>::v);
+  const ItemWalk walk(npoles, (int)threadIdx.x, FT<W>::v, fnp);
   auto sub_phase = [&](int k) {
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (t - kTB * k - kTB);
@@ -1093,12 +1098,16 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     if (l <= 1 || ((T.skipmask >> j) & 1u)) continue;
     const int R = T.gR[j];
     const FDiv fR = T.fR[j];
+    const bool full = (f.units == T.R);               // precomputed per-axis constants apply
+    const FDiv fnp = T.fNP[j];
     if (blocked && j == T.bj) {
-      fused_axis_block<INV, W>(sm, RS, T.bt, R, fR, rows_total / (T.ej * R), f.lo_ok, f.hi_ok);
+      fused_axis_block<INV, W>(sm, RS, T.bt, R, fR, full ? T.gOk[j] : rows_total / (T.ej * R), f.lo_ok, f.hi_ok,
+                               full ? &fnp : nullptr);
       continue;
     }
     if (T.bt2 >= 0 && j == T.bj + 1) {              // second blocked axis (hierarchization only)
-      fused_axis_block<INV, W>(sm, RS, T.bt2, R, fR, rows_total / (((1 << T.bt2) + 1) * R), f.lo2_ok, f.hi2_ok);
+      fused_axis_block<INV, W>(sm, RS, T.bt2, R, fR, full ? T.gOk[j] : rows_total / (((1 << T.bt2) + 1) * R),
+                               f.lo2_ok, f.hi2_ok, full ? &fnp : nullptr);
       continue;
     }
     const int n = (T.bj == j) ? T.ej : (1 << l) - 1;
@@ -1109,8 +1118,9 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
       continue;
     }
 #endif
-    if (R == 1) fused_axis<INV, W, true>(sm, RS, l, R, fR, rows_total / n, hs);
-    else fused_axis<INV, W>(sm, RS, l, R, fR, rows_total / (n * R), hs);
+    const int Ok = full ? T.gOk[j] : rows_total / (n * R);
+    if (R == 1) fused_axis<INV, W, true>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr);
+    else fused_axis<INV, W>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr);
   }
 #ifdef SGH_DEBUG_NOMEMORY
   return;                                         // timing experiment: compute only
@@ -1204,6 +1214,7 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
   cp_async_commit();
   stage_task(&s_task[0], Tc);
   staged = idx;
+  int slot = 0;                                   // s_task slot of the current tile (STAGES == 1)
   for (int k = 0;; ++k) {
     double *cur = smem + (STAGES == 2 ? (k & 1) * src.stage_doubles : 0);
     const int64_t qn = q + qstep;
@@ -1222,21 +1233,38 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
       cp_async_wait<0>();
     }
     __syncthreads();
-    fused_compute_store<INV, W>(s_task[STAGES == 2 ? (k & 1) : 0], fc, cur + fc.par);
+    // STAGES == 1: fetch the NEXT tile's task descriptor into the other slot
+    // now (cp.async), so the next tile's geometry is read from SMEM instead of
+    // a chain of global loads on the critical path (C5: every tile of a CTA is
+    // a different task)
+    int64_t qln = 0;
+    bool newtask = false;
+    if (STAGES == 1 && more) {
+      Tn = ref(qn, qln);
+      newtask = (idx != staged);
+      if (newtask) {
+        const uint64_t *a = reinterpret_cast<const uint64_t *>(Tn);
+        uint64_t *b = reinterpret_cast<uint64_t *>(&s_task[slot ^ 1]);
+        for (int i = threadIdx.x; i < (int)(sizeof(Task) / 8); i += FT<W>::v)
+          cp_async8(reinterpret_cast<double *>(b + i), reinterpret_cast<const double *>(a + i));
+        cp_async_commit();
+      }
+    }
+    fused_compute_store<INV, W>(s_task[STAGES == 2 ? (k & 1) : slot], fc, cur + fc.par);
     if (W == 1 && SGH_BULK_STORE && threadIdx.x == 0) bulk_wait_read();   // bulk stores have read the stage
+    if (STAGES == 1 && newtask) cp_async_wait<0>();
     __syncthreads();                              // the stage is free for the next load
     if (!more) break;
     q = qn;
     if (STAGES == 1) {                            // single stage: load the next tile now
-      int64_t qln;
-      Tn = ref(qn, qln);
-      fn = fused_tile<W>(*Tn, qln);
-      fused_issue<W>(*Tn, fn, smem);
-      cp_async_commit();
-      if (idx != staged) {                        // a new task: its descriptor to SMEM
-        stage_task(&s_task[0], Tn);
+      if (newtask) {
+        slot ^= 1;
         staged = idx;
       }
+      const Task &TS = s_task[slot];
+      fn = fused_tile<W>(TS, qln);
+      fused_issue<W>(TS, fn, smem);
+      cp_async_commit();
     }
     Tc = Tn;
     fc = fn;
