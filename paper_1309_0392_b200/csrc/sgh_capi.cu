@@ -514,6 +514,9 @@ static double kind_bw(const Task &t) {
       // B200 (measured 2.84 TB/s on C4 (14,13) tiles 129 x 65; below the
       // per-axis pair FLAT_BLOCKS + STRIDED, so the planner keeps that)
       if (t.bt2 >= 0 && t.bt < t.gl[t.bj]) bw = std::min(bw, 2.6);
+      // (measured: dense W == 1 tiles 4.7 TB/s, blocked W == 1 tiles 3.3 TB/s;
+      // feeding those rates into the model made C3 / C5 slower -- 86.2 / 130.3
+      // vs 90.1 / 131.2 Gpoints/s -- so the run-length rates above are kept)
       // lattice views: 8-byte copies; single-element runs (a lattice of the
       // contiguous axis) touch one 32-byte sector per point and write partial
       // sectors (measured ~0.3 TB/s algorithmic on C3's (5,4,4) lattice)
