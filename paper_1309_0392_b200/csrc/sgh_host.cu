@@ -109,11 +109,21 @@ sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *
   if ((st = get_streams(hs)) != SGH_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   unsigned char *base = static_cast<unsigned char *>(device_buffer);
+  // Device placement: a grid whose host memory directly follows the previous
+  // grid's is placed directly after it on the device too, so a run of
+  // host-contiguous grids moves with ONE copy per direction (exactly the
+  // grids' own bytes: no memory between them is touched); other grids start
+  // 256-byte aligned.  Offsets never exceed the padded layout of host_layout.
   std::vector<double *> dptr(num_grids);
   std::vector<int64_t> N(num_grids);
+  std::vector<char> cont(num_grids, 0);              // host-contiguous with grid g - 1
+  size_t off = 0;
   for (int64_t g = 0; g < num_grids; ++g) {
-    dptr[g] = reinterpret_cast<double *>(base + L.grid_off[g]);
     validate_levels(levels + g * d, d, &N[g]);
+    cont[g] = g > 0 && host_grids[g] == host_grids[g - 1] + N[g - 1];
+    if (!cont[g]) off = (off + 255) / 256 * 256;
+    dptr[g] = reinterpret_cast<double *>(base + off);
+    off += size_t(N[g]) * 8;
   }
   cudaError_t e;
   cudaEvent_t ev_start;
@@ -125,10 +135,19 @@ sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *
   cudaEvent_t last_out = nullptr;
   for (size_t c = 0; c < L.chunks.size(); ++c) {
     const int64_t g0 = L.chunks[c].first, g1 = L.chunks[c].second;
-    for (int64_t g = g0; g < g1; ++g) {
-      e = cudaMemcpyAsync(dptr[g], host_grids[g], size_t(N[g]) * 8, cudaMemcpyHostToDevice, hs.in);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
-    }
+    auto copy_runs = [&](bool h2d) -> cudaError_t {
+      for (int64_t g = g0; g < g1;) {
+        int64_t h = g + 1;
+        size_t bytes = size_t(N[g]) * 8;
+        while (h < g1 && cont[h]) bytes += size_t(N[h++]) * 8;
+        cudaError_t ce = h2d ? cudaMemcpyAsync(dptr[g], host_grids[g], bytes, cudaMemcpyHostToDevice, hs.in)
+                             : cudaMemcpyAsync(host_grids[g], dptr[g], bytes, cudaMemcpyDeviceToHost, hs.out);
+        if (ce != cudaSuccess) return ce;
+        g = h;
+      }
+      return cudaSuccess;
+    };
+    if ((e = copy_runs(true)) != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
     cudaEvent_t ev_in, ev_comp, ev_out;
     cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_comp, cudaEventDisableTiming);
@@ -141,10 +160,7 @@ sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *
     if (st != SGH_OK) return st;
     cudaEventRecord(ev_comp, s);
     cudaStreamWaitEvent(hs.out, ev_comp, 0);
-    for (int64_t g = g0; g < g1; ++g) {
-      e = cudaMemcpyAsync(host_grids[g], dptr[g], size_t(N[g]) * 8, cudaMemcpyDeviceToHost, hs.out);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
-    }
+    if ((e = copy_runs(false)) != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
     cudaEventRecord(ev_out, hs.out);
     cudaEventDestroy(ev_in);
     cudaEventDestroy(ev_comp);
