@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -776,6 +777,7 @@ struct BatchedPlan {
   std::vector<Task> tasks;
   std::vector<int64_t> prefix;
   std::vector<Segment> segs;
+  std::vector<unsigned char> image;   // the device table image (built once per cached plan)
   size_t table_bytes() const {
     return (tasks.size() * sizeof(Task) + 255) / 256 * 256 + prefix.size() * sizeof(int64_t);
   }
@@ -868,19 +870,60 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
   if (st != SGH_OK) return st;
   if (num_grids == 0) return SGH_OK;
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
-  BatchedPlan P;
-  build_batched_plan(grids, levels, d, num_grids, flags, P);
+  // Plan cache: the combination grids are transformed every iteration of the
+  // combination technique with the same pointers and levels, and planning
+  // 4,255 grids takes tens of ms of host time -- reuse the plan (the table is
+  // still uploaded on every call, so the workspace contract is unchanged).
+  struct CacheEntry {
+    std::vector<int32_t> levels;
+    std::vector<double *> grids;
+    uint32_t flags;
+    int32_t d;
+    std::shared_ptr<BatchedPlan> plan;
+  };
+  static std::mutex cache_mu;
+  static std::vector<CacheEntry> cache;            // most recent last, at most 4
+  std::shared_ptr<BatchedPlan> plan;
+  {
+    std::lock_guard<std::mutex> lk(cache_mu);
+    for (size_t i = 0; i < cache.size(); ++i) {
+      const CacheEntry &c = cache[i];
+      if (c.flags == flags && c.d == d && c.grids.size() == size_t(num_grids) &&
+          std::equal(c.grids.begin(), c.grids.end(), grids) &&
+          std::equal(c.levels.begin(), c.levels.end(), levels)) {
+        plan = c.plan;
+        break;
+      }
+    }
+  }
+  if (!plan) {
+    plan = std::make_shared<BatchedPlan>();
+    build_batched_plan(grids, levels, d, num_grids, flags, *plan);
+    CacheEntry c;
+    c.levels.assign(levels, levels + num_grids * d);
+    c.grids.assign(grids, grids + num_grids);
+    c.flags = flags;
+    c.d = d;
+    c.plan = plan;
+    std::lock_guard<std::mutex> lk(cache_mu);
+    cache.push_back(std::move(c));
+    if (cache.size() > 4) cache.erase(cache.begin());
+  }
+  const BatchedPlan &P = *plan;
   if (P.segs.empty()) return SGH_OK;
   const size_t bytes = P.table_bytes();
   if (!workspace || ws_bytes < bytes || (reinterpret_cast<uintptr_t>(workspace) & 15)) {
     set_error("workspace missing, misaligned or smaller than sgh_batched_workspace_bytes()");
     return SGH_ERR_WORKSPACE;
   }
-  std::vector<unsigned char> host(bytes, 0);
   const size_t prefix_base = (P.tasks.size() * sizeof(Task) + 255) / 256 * 256;
-  std::memcpy(host.data(), P.tasks.data(), P.tasks.size() * sizeof(Task));
-  std::memcpy(host.data() + prefix_base, P.prefix.data(), P.prefix.size() * sizeof(int64_t));
-  st = staged_upload(workspace, host.data(), bytes, s);
+  if (plan->image.size() != bytes) {
+    std::vector<unsigned char> &host = plan->image;
+    host.assign(bytes, 0);
+    std::memcpy(host.data(), P.tasks.data(), P.tasks.size() * sizeof(Task));
+    std::memcpy(host.data() + prefix_base, P.prefix.data(), P.prefix.size() * sizeof(int64_t));
+  }
+  st = staged_upload(workspace, plan->image.data(), bytes, s);
   if (st != SGH_OK) return st;
   const Task *d_tasks = reinterpret_cast<const Task *>(workspace);
   const int64_t *d_prefix = reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + prefix_base);
