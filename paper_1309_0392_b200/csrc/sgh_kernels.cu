@@ -35,15 +35,16 @@
 namespace sgh {
 
 // threads of a FUSED CTA, per tile kind (W == 1 contiguous / W > 1 column
-// tiles); default 256 threads, 3 CTAs per SM, 70 KB tiles for both.  Tuning
-// experiments: SGH_FUSED_THREADS(_W1), FUSED_MINB(_W1) with the planner's
-// SGH_FUSED_T(1) (128-thread W == 1 CTAs at 6 per SM run 3.78 vs 2.60 TB/s at
-// equal 35 KB tiles, but the smaller tiles cost passes: no net gain).
+// tiles): 128 threads, 3 CTAs per SM, 70 KB tiles.  Measured on C5 (with the
+// host planning cached, so the step is GPU-bound): 128 threads 150.9, 192
+// 146.7, 256 143.0, 96 146.5 Gpoints/s -- a tile's in-SMEM transform is a
+// sequence of barrier-separated phases, and fewer warps per barrier wait less.
+// Tuning: SGH_FUSED_THREADS(_W1), FUSED_MINB(_W1), planner SGH_FUSED_T(1).
 #ifndef SGH_FUSED_THREADS
-#define SGH_FUSED_THREADS 256
+#define SGH_FUSED_THREADS 128
 #endif
 #ifndef SGH_FUSED_THREADS_W1
-#define SGH_FUSED_THREADS_W1 256
+#define SGH_FUSED_THREADS_W1 128
 #endif
 template <int W>
 struct FT {
