@@ -568,11 +568,12 @@ __device__ __forceinline__ void block_fine(double *p0, int STR, bool lo_ok, bool
 }
 
 // Work items of the in-SMEM pole transforms are aligned blocks of 2^kTB points
-// (kTB + 1 ... fine levels in 2^kTB + 1 registers per item); a pole of level l
+// (kTB fine levels in 2^kTB + 1 registers per item; kTB = 4 with 128-thread CTAs: C2 +1.5 %,
+// C3 +3 %, C5 +0.5 % over kTB = 3); a pole of level l
 // is done as blocks at stride 1, then its coarse lattice (stride 2^kTB, level
 // l - kTB) the same way, until the lattice fits one register pole.
 #ifndef SGH_TB
-#define SGH_TB 3
+#define SGH_TB 4
 #endif
 constexpr int kTB = SGH_TB;
 
