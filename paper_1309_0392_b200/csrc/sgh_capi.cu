@@ -511,10 +511,11 @@ static double kind_bw(const Task &t) {
         if (t.bj >= 0) run = (t.Gj == t.A) ? int64_t(t.A) * t.ej : t.A;
       }
       double bw = run >= 256 ? 5.2 : run >= 128 ? 4.6 : run >= 64 ? 4.3 : run >= 32 ? 4.0 : run >= 16 ? 3.3 : 2.2;
-      // two blocked axes: two block transforms per tile, compute-bound on
-      // B200 (measured 2.84 TB/s on C4 (14,13) tiles 129 x 65; below the
-      // per-axis pair FLAT_BLOCKS + STRIDED, so the planner keeps that)
-      if (t.bt2 >= 0 && t.bt < t.gl[t.bj]) bw = std::min(bw, 2.6);
+      // two blocked axes: two block transforms per tile (measured on C4's
+      // 129 x 65 tiles: 2.84 TB/s with 256-thread CTAs, 3.35 TB/s with the
+      // 128-thread ones -- then one round trip + cross phases beats the
+      // per-axis pair FLAT_BLOCKS + STRIDED: 169.6 vs 157.7 Gpoints/s)
+      if (t.bt2 >= 0 && t.bt < t.gl[t.bj]) bw = std::min(bw, 3.3);
       // (measured: dense W == 1 tiles 4.7 TB/s, blocked W == 1 tiles 3.3 TB/s;
       // feeding those rates into the model made C3 / C5 slower -- 86.2 / 130.3
       // vs 90.1 / 131.2 Gpoints/s -- so the run-length rates above are kept)

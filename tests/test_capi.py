@@ -156,11 +156,15 @@ def test_plan_c2_c3_use_blocked_fusion():
 
 def test_plan_two_blocked_available():
     """Two-blocked plans (SURVEY 8(a) a4 block scheme: both axes of a 2-D grid
-    in aligned blocks, one round trip + cross phases) exist for hierarchization;
-    the cost model (measured 2.84 TB/s tiles) keeps C4 on its per-axis pair."""
+    in aligned blocks, one round trip + cross phases) are chosen for C4's
+    hierarchization (measured 169.6 vs 157.7 Gpoints/s per-axis); its
+    dehierarchization keeps the per-axis pair."""
     p = _plan_passes((14, 13))
-    assert len(p) == 2
+    assert len(p) == 1 and int(p[0][0][1]["bt2"]) >= 2
+    N = si.num_points((14, 13))
+    assert p[0][0][2] < N <= sum(x for _, _, x in p[0]) < 1.06 * N
     assert len(_plan_passes((14, 13), inverse=True)) == 2
+
 
 def test_plan_two_blocked_forced(monkeypatch):
     """SGH_TWO_BLOCKED=force selects the two-blocked plan wherever one exists
