@@ -515,7 +515,11 @@ static double kind_bw(const Task &t) {
       // 129 x 65 tiles: 2.84 TB/s with 256-thread CTAs, 3.35 TB/s with the
       // 128-thread ones -- then one round trip + cross phases beats the
       // per-axis pair FLAT_BLOCKS + STRIDED: 169.6 vs 157.7 Gpoints/s)
-      if (t.bt2 >= 0 && t.bt < t.gl[t.bj]) bw = std::min(bw, 3.3);
+      if (t.bt2 >= 0 && t.bt < t.gl[t.bj]) {
+        // measured (C4): 257 x 33 tiles 4.09 TB/s, 129 x 65 3.35, 257 x 17 3.3
+        bw = std::min(bw, t.ej >= 257 ? 4.1 : 3.3);
+        if (t.P < (fused_budget_w1() * 3) / 4) bw *= 0.85;
+      }
       // (measured: dense W == 1 tiles 4.7 TB/s, blocked W == 1 tiles 3.3 TB/s;
       // feeding those rates into the model made C3 / C5 slower -- 86.2 / 130.3
       // vs 90.1 / 131.2 Gpoints/s -- so the run-length rates above are kept)
@@ -544,6 +548,10 @@ static double pass_cost(const std::vector<Task> &phases) {
       // a view whose elements are isolated (one per 32-byte sector, no two in
       // a row): measured ~0.13 TB/s algorithmic (STRIDED, C4 cross phases)
       c += task_points(t) / std::max(1.0, task_points(phases[0])) / 0.15;
+    } else if (task_points(t) > 0.01 * task_points(phases[0])) {
+      // a sizeable later phase of contiguous rows (e.g. the coarse-b rows of a
+      // two-blocked plan): half the kernel's streaming rate
+      c += task_points(t) / std::max(1.0, task_points(phases[0])) / (0.5 * bw);
     } else {
       // later phases are coarse lattices: a small fraction of the points, latency bound
       c += 2.0 * task_points(t) / std::max(1.0, task_points(phases[0])) / 1.0;
@@ -618,9 +626,13 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
     // SGH_TWO_BLOCKED=force: take a two-blocked plan whenever one exists (tests)
     const char *tb = getenv("SGH_TWO_BLOCKED");
     double bc = (tb && std::strcmp(tb, "force") == 0) ? 1e30 : cost[d];
+    // SGH_TWO_BLOCKED_T=t1,t2 (experiments): only that pair of block levels
+    int ft1 = -1, ft2 = -1;
+    if (const char *e = getenv("SGH_TWO_BLOCKED_T")) std::sscanf(e, "%d,%d", &ft1, &ft2);
     for (int a = 0; a + 1 < d; ++a)
       for (int t1 = 2; t1 < levels[a]; ++t1)
         for (int t2 = 2; t2 < levels[a + 1]; ++t2) {
+          if (ft1 >= 0 && (t1 != ft1 || t2 != ft2)) continue;
           std::vector<Task> ph;
           if (!plan_two_blocked(grid, levels, d, a, t1, t2, ph)) continue;
           const double c = pass_cost(ph);

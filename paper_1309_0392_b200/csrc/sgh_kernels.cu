@@ -1417,14 +1417,16 @@ static int resident_ctas(KernelFn fn, size_t smem, int threads = kThreads) {
   static int ncache = 0;
   for (int i = 0; i < ncache; ++i)
     if (cache[i].fn == fn && cache[i].dev == dev && cache[i].smem == smem) return cache[i].ctas;
-  if (smem > 48 * 1024) {
-    // opt in to large dynamic shared memory (FUSED tiles up to ~70 KB)
-    // the device's opt-in maximum minus the kernel's static shared memory
+  // Opt in to large dynamic shared memory (FUSED / STRIDED tiles up to ~70 KB):
+  // the default limit of 48 KB covers static + dynamic shared memory, so the
+  // opt-in is needed as soon as both together exceed it; the opt-in maximum is
+  // the device's per-block limit minus the kernel's static shared memory.
+  cudaFuncAttributes fa;
+  size_t stat = 0;
+  if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) stat = fa.sharedSizeBytes;
+  if (smem + stat > 48 * 1024) {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa;
-    size_t stat = 0;
-    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) stat = fa.sharedSizeBytes;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(optin - (int)stat));
   }
   int ctas = 1;
