@@ -188,125 +188,6 @@ __device__ __forceinline__ void for_each_tile(const Src &src, F &&body) {
   }
 }
 
-// ----------------------------------------------------------------- FLAT_SLABS
-// Tile = R consecutive slabs (o0 .. o0+R-1), each n*S contiguous doubles.
-template <bool INV>
-__global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__ Src src) {
-  extern __shared__ __align__(16) double smem[];  // 1 + R*n*S doubles (<= kFlatT + 1)
-  for_each_tile(src, [&](const Task &T, int64_t q) {
-    const int l = T.l;
-    const int n = (1 << l) - 1;
-    const int S = (int)T.S;
-    const int nS = n * S;
-    const int64_t o0 = q * T.R;
-    const int ns = (int)min((int64_t)T.R, T.O - o0);
-    const int len = ns * nS;
-    const FDiv fS = T.fS, fNS = T.fNS;
-    double *__restrict__ g = T.grid + T.base + o0 * T.OS;
-    double *sm = smem + phase8(g);                      // same 16-byte phase as g
-    copy_range_async(sm, g, len);
-    cp_async_wait_all();
-    __syncthreads();
-    if (!INV) {
-      for (int e = threadIdx.x; e < len; e += kThreads) {
-        const uint32_t slab = fdiv((uint32_t)e, fNS);
-        const uint32_t p = (uint32_t)e - slab * (uint32_t)nS;
-        const int i = (int)fdiv(p, fS) + 1;           // 1-based pole index
-        const int s = i & -i;                          // 2^{tz(i)}
-        const int sS = s * S;
-        double x = sm[e];
-        if (i - s >= 1) x = x - 0.5 * sm[e - sS];      // left predecessor (P:129)
-        if (i + s <= n) x = x - 0.5 * sm[e + sS];      // right predecessor (P:130)
-        g[e] = x;
-      }
-    } else {
-      for (int lam = 2; lam <= l; ++lam) {             // coarse -> fine (reading R9)
-        const int s = 1 << (l - lam);
-        const int rows = 1 << (lam - 1);
-        const int cnt = ns * rows * S;
-        const int sS = s * S;
-        for (int k = threadIdx.x; k < cnt; k += kThreads) {
-          const uint32_t qq = fdiv((uint32_t)k, fS);
-          const int r = k - (int)qq * S;
-          const int slab = (int)(qq >> (lam - 1));
-          const int j = (int)qq & (rows - 1);
-          const int i = s * (2 * j + 1);
-          const int e = slab * nS + (i - 1) * S + r;
-          double x = sm[e];
-          if (i - s >= 1) x = x + 0.5 * sm[e - sS];
-          if (i + s <= n) x = x + 0.5 * sm[e + sS];
-          sm[e] = x;
-        }
-        __syncthreads();
-      }
-      for (int e = threadIdx.x; e < len; e += kThreads) g[e] = sm[e];
-    }
-    __syncthreads();
-  });
-}
-
-// ---------------------------------------------------------------- FLAT_BLOCKS
-// Tile = rows [b 2^t, (b+1) 2^t] (local rb = 0..2^t) of slab o; rows are S
-// contiguous doubles and consecutive rows are adjacent (PS == S).  Only the
-// fine rows rb = 1..2^t-1 are written; rb = 0 and rb = 2^t are coarse-lattice
-// points owned by another phase (read-only halo here).
-template <bool INV>
-__global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant__ Src src) {
-  extern __shared__ __align__(16) double smem[];  // 1 + (2^t + 1) * S doubles
-  for_each_tile(src, [&](const Task &T, int64_t q) {
-    const int t = T.t;
-    const int B = 1 << t;
-    const int nb_log = T.l - t;                            // global blocks per pole
-    const int64_t o = q >> T.rlog;
-    const int b = (int)(T.blk0 + (q & ((int64_t(1) << T.rlog) - 1)));
-    const int S = (int)T.S;
-    const int n = (1 << T.l) - 1;
-    const int i0 = b * B;                                  // pole index of local row 0
-    const int rb_lo = (b == 0) ? 1 : 0;                    // row 0 of block 0 is the boundary
-    const int rb_hi = (b == (1 << nb_log) - 1) ? B - 1 : B;  // row 2^l is the boundary
-    const FDiv fS = T.fS;
-    // global element of local e = rb*S + r is  gr[e]
-    double *__restrict__ gr = T.grid + T.base + o * T.OS + (int64_t)(i0 - 1) * S;
-    double *sm = smem + phase8(gr);
-    copy_range_async(sm + rb_lo * S, gr + rb_lo * S, (rb_hi - rb_lo + 1) * S);
-    cp_async_wait_all();
-    __syncthreads();
-    if (!INV) {
-      const int e1 = B * S;
-      for (int e = S + threadIdx.x; e < e1; e += kThreads) {
-        const int rb = (int)fdiv((uint32_t)e, fS);
-        const int i = i0 + rb;
-        const int s = rb & -rb;                            // tz(i) = tz(rb) < t
-        const int sS = s * S;
-        double x = sm[e];
-        if (i - s >= 1) x = x - 0.5 * sm[e - sS];
-        if (i + s <= n) x = x - 0.5 * sm[e + sS];
-        gr[e] = x;
-      }
-    } else {
-      for (int s = B >> 1; s >= 1; s >>= 1) {              // block-local levels, coarse -> fine
-        const int cnt = (B / (2 * s)) * S;
-        const int sS = s * S;
-        for (int k = threadIdx.x; k < cnt; k += kThreads) {
-          const int jj = (int)fdiv((uint32_t)k, fS);
-          const int r = k - jj * S;
-          const int rb = s * (2 * jj + 1);
-          const int e = rb * S + r;
-          const int i = i0 + rb;
-          double x = sm[e];
-          if (i - s >= 1) x = x + 0.5 * sm[e - sS];
-          if (i + s <= n) x = x + 0.5 * sm[e + sS];
-          sm[e] = x;
-        }
-        __syncthreads();
-      }
-      const int e1 = B * S;
-      for (int e = S + threadIdx.x; e < e1; e += kThreads) gr[e] = sm[e];
-    }
-    __syncthreads();
-  });
-}
-
 // ------------------------------------------------------------------- STRIDED
 // Tile = (o, block b, column group cb): rows rb = 0..2^t (pole index b 2^t + rb),
 // W adjacent columns c0 .. c0+W-1 (W = 32/64/128, T.W).  t == l: whole pole.
@@ -656,7 +537,7 @@ struct HaloSkip {
 // levels; hierarchization runs fine -> coarse, dehierarchization the reverse.
 // UNIT: the axis is the tile's first (R == 1): the point stride RS is a
 // compile-time constant (immediate SMEM offsets) and a pole index needs no division.
-template <bool INV, int W, bool UNIT = false>
+template <bool INV, int W, bool UNIT = false, int NT = FT<W>::v>
 __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv fR, int Ok,
                                            const HaloSkip hs, const FDiv *fnp = nullptr) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
@@ -676,7 +557,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   };
   auto pole_base = [&](int p) -> double * { return sm + pole_row(p) * RS + (p & (W - 1)); };
   if (l <= 4) {
-    for (int p = threadIdx.x; p < npoles; p += FT<W>::v) {
+    for (int p = threadIdx.x; p < npoles; p += NT) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       pole_regs_rt<INV>(pole_base(p), l, STR);
     }
@@ -689,7 +570,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
     levels[nlev++] = lf;
     lf -= kTB;
   }
-  const ItemWalk walk(npoles, (int)threadIdx.x, FT<W>::v, fnp);
+  const ItemWalk walk(npoles, (int)threadIdx.x, NT, fnp);
   auto block_phase = [&](int k) {                // k-th lattice level: stride 2^{kTB k}
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (levels[k] - kTB);
@@ -703,7 +584,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   auto lattice_phase = [&]() {
     if (lf <= 1) return;                         // a single point: no update
     const int m = 1 << (kTB * nlev);
-    for (int p = threadIdx.x; p < npoles; p += FT<W>::v) {
+    for (int p = threadIdx.x; p < npoles; p += NT) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       double *p0 = pole_base(p) - STR;           // virtual point 0
       pole_regs_rt<INV>(p0 + m * STR, lf, m * STR);
@@ -777,7 +658,7 @@ __device__ __forceinline__ bool warp_rows_dispatch(double *sm, int nrows, int l)
 // lattice recursion as fused_axis: 2^kTB-point sub-blocks at strides 1, 2^kTB,
 // .. (K = t / kTB levels), then the top lattice of 2^{t - kTB K} + 1 points.
 // lo_ok / hi_ok: the block's ends are grid points (false: the zero boundary).
-template <bool INV, int W>
+template <bool INV, int W, int NT = FT<W>::v>
 __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int R, const FDiv fR, int Ok,
                                                  bool lo_ok, bool hi_ok, const FDiv *fnp = nullptr) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
@@ -793,7 +674,7 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
   };
   const int K = t / kTB;
   const int tr = t - kTB * K;
-  const ItemWalk walk(npoles, (int)threadIdx.x, FT<W>::v, fnp);
+  const ItemWalk walk(npoles, (int)threadIdx.x, NT, fnp);
   auto sub_phase = [&](int k) {
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (t - kTB * k - kTB);
@@ -804,7 +685,7 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
   auto top_phase = [&]() {
     if (tr == 0) return;                         // the top lattice is just the two ends
     const int m = 1 << (kTB * K);
-    for (int p = threadIdx.x; p < npoles; p += FT<W>::v) {
+    for (int p = threadIdx.x; p < npoles; p += NT) {
       if (tr == 1) block_fine<1, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else if (tr == 2 || kTB <= 3) block_fine<2, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else block_fine<(kTB > 3 ? 3 : 2), INV>(pole_base(p), m * STR, lo_ok, hi_ok);
@@ -818,6 +699,125 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
     top_phase();
     for (int k = K - 1; k >= 0; --k) sub_phase(k);
   }
+}
+
+// ----------------------------------------------------------------- FLAT_SLABS
+// Tile = R consecutive slabs (o0 .. o0+R-1), each n*S contiguous doubles.
+template <bool INV>
+__global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__ Src src) {
+  extern __shared__ __align__(16) double smem[];  // 1 + R*n*S doubles (<= kFlatT + 1)
+  for_each_tile(src, [&](const Task &T, int64_t q) {
+    const int l = T.l;
+    const int n = (1 << l) - 1;
+    const int S = (int)T.S;
+    const int nS = n * S;
+    const int64_t o0 = q * T.R;
+    const int ns = (int)min((int64_t)T.R, T.O - o0);
+    const int len = ns * nS;
+    const FDiv fS = T.fS, fNS = T.fNS;
+    double *__restrict__ g = T.grid + T.base + o0 * T.OS;
+    double *sm = smem + phase8(g);                      // same 16-byte phase as g
+    copy_range_async(sm, g, len);
+    cp_async_wait_all();
+    __syncthreads();
+    if (!INV) {
+      for (int e = threadIdx.x; e < len; e += kThreads) {
+        const uint32_t slab = fdiv((uint32_t)e, fNS);
+        const uint32_t p = (uint32_t)e - slab * (uint32_t)nS;
+        const int i = (int)fdiv(p, fS) + 1;           // 1-based pole index
+        const int s = i & -i;                          // 2^{tz(i)}
+        const int sS = s * S;
+        double x = sm[e];
+        if (i - s >= 1) x = x - 0.5 * sm[e - sS];      // left predecessor (P:129)
+        if (i + s <= n) x = x - 0.5 * sm[e + sS];      // right predecessor (P:130)
+        g[e] = x;
+      }
+    } else {
+      for (int lam = 2; lam <= l; ++lam) {             // coarse -> fine (reading R9)
+        const int s = 1 << (l - lam);
+        const int rows = 1 << (lam - 1);
+        const int cnt = ns * rows * S;
+        const int sS = s * S;
+        for (int k = threadIdx.x; k < cnt; k += kThreads) {
+          const uint32_t qq = fdiv((uint32_t)k, fS);
+          const int r = k - (int)qq * S;
+          const int slab = (int)(qq >> (lam - 1));
+          const int j = (int)qq & (rows - 1);
+          const int i = s * (2 * j + 1);
+          const int e = slab * nS + (i - 1) * S + r;
+          double x = sm[e];
+          if (i - s >= 1) x = x + 0.5 * sm[e - sS];
+          if (i + s <= n) x = x + 0.5 * sm[e + sS];
+          sm[e] = x;
+        }
+        __syncthreads();
+      }
+      for (int e = threadIdx.x; e < len; e += kThreads) g[e] = sm[e];
+    }
+    __syncthreads();
+  });
+}
+
+// ---------------------------------------------------------------- FLAT_BLOCKS
+// Tile = rows [b 2^t, (b+1) 2^t] (local rb = 0..2^t) of slab o; rows are S
+// contiguous doubles and consecutive rows are adjacent (PS == S).  Only the
+// fine rows rb = 1..2^t-1 are written; rb = 0 and rb = 2^t are coarse-lattice
+// points owned by another phase (read-only halo here).
+template <bool INV>
+__global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant__ Src src) {
+  extern __shared__ __align__(16) double smem[];  // 1 + (2^t + 1) * S doubles
+  for_each_tile(src, [&](const Task &T, int64_t q) {
+    const int t = T.t;
+    const int B = 1 << t;
+    const int nb_log = T.l - t;                            // global blocks per pole
+    const int64_t o = q >> T.rlog;
+    const int b = (int)(T.blk0 + (q & ((int64_t(1) << T.rlog) - 1)));
+    const int S = (int)T.S;
+    const int n = (1 << T.l) - 1;
+    const int i0 = b * B;                                  // pole index of local row 0
+    const int rb_lo = (b == 0) ? 1 : 0;                    // row 0 of block 0 is the boundary
+    const int rb_hi = (b == (1 << nb_log) - 1) ? B - 1 : B;  // row 2^l is the boundary
+    const FDiv fS = T.fS;
+    // global element of local e = rb*S + r is  gr[e]
+    double *__restrict__ gr = T.grid + T.base + o * T.OS + (int64_t)(i0 - 1) * S;
+    double *sm = smem + phase8(gr);
+    copy_range_async(sm + rb_lo * S, gr + rb_lo * S, (rb_hi - rb_lo + 1) * S);
+    cp_async_wait_all();
+    __syncthreads();
+    if (!INV) {
+      const int e1 = B * S;
+      for (int e = S + threadIdx.x; e < e1; e += kThreads) {
+        const int rb = (int)fdiv((uint32_t)e, fS);
+        const int i = i0 + rb;
+        const int s = rb & -rb;                            // tz(i) = tz(rb) < t
+        const int sS = s * S;
+        double x = sm[e];
+        if (i - s >= 1) x = x - 0.5 * sm[e - sS];
+        if (i + s <= n) x = x - 0.5 * sm[e + sS];
+        gr[e] = x;
+      }
+    } else {
+      for (int s = B >> 1; s >= 1; s >>= 1) {              // block-local levels, coarse -> fine
+        const int cnt = (B / (2 * s)) * S;
+        const int sS = s * S;
+        for (int k = threadIdx.x; k < cnt; k += kThreads) {
+          const int jj = (int)fdiv((uint32_t)k, fS);
+          const int r = k - jj * S;
+          const int rb = s * (2 * jj + 1);
+          const int e = rb * S + r;
+          const int i = i0 + rb;
+          double x = sm[e];
+          if (i - s >= 1) x = x + 0.5 * sm[e - sS];
+          if (i + s <= n) x = x + 0.5 * sm[e + sS];
+          sm[e] = x;
+        }
+        __syncthreads();
+      }
+      const int e1 = B * S;
+      for (int e = S + threadIdx.x; e < e1; e += kThreads) gr[e] = sm[e];
+    }
+    __syncthreads();
+  });
 }
 
 // geometry of one FUSED tile
