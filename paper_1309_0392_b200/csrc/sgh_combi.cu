@@ -74,18 +74,21 @@ struct CombiArgs {
 
 // binom / sbase: the tables staged in SMEM (lanes index them with different
 // values; constant-bank reads would serialise)
-__device__ __forceinline__ int64_t sg_offset(const int8_t *lam, int d, const int64_t (*binom)[SGH_MAX_D + 1],
+template <int D>
+__device__ __forceinline__ int64_t sg_offset(const int *lam, const int64_t (*binom)[SGH_MAX_D + 1],
                                              const int64_t *sbase) {
   int s = 0;
-  for (int k = 0; k < d; ++k) s += lam[k];
+#pragma unroll
+  for (int k = 0; k < D; ++k) s += lam[k];
   int64_t rank = 0;
   int rem = s;
-  for (int k = 0; k < d - 1; ++k) {
-    const int m = d - k - 1;
+#pragma unroll
+  for (int k = 0; k < D - 1; ++k) {
+    const int m = D - k - 1;
     rank += binom[rem - 1][m] - binom[rem - lam[k]][m];
     rem -= lam[k];
   }
-  return sbase[s] + (rank << (s - d));
+  return sbase[s] + (rank << (s - D));
 }
 
 // owner item of tile q (tiles of a CTA increase): galloping search from the cursor
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(kThreads) k_contrib_scan(const __grid_constant
   }
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ CombiArgs A) {
   __shared__ CombiSub s_sub;
   int idx = -1, cur = -1;
@@ -177,10 +181,12 @@ __global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ Com
     const int np = min(kCombiPts, S.npts - p0);
     for (int qq = threadIdx.x; qq < np; qq += kThreads) {
       const int p = p0 + qq;
-      int j[SGH_MAX_D];
+      int j[D], lam[D];
       int rest = p;
-      for (int k = 0; k < A.d; ++k) {             // j_1 fastest
-        const int b = S.lam[k] - 1;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {               // j_1 fastest
+        lam[k] = S.lam[k];
+        const int b = lam[k] - 1;
         j[k] = rest & ((1 << b) - 1);
         rest >>= b;
       }
@@ -188,10 +194,12 @@ __global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ Com
       for (int c = 0; c < S.nc; ++c) {            // grid order (deterministic)
         const CombiGrid &G = A.grids[__ldg(&A.contrib[S.c0 + c])];
         int64_t gi = 0, stride = 1;
-        for (int k = 0; k < A.d; ++k) {
-          const int64_t i = int64_t(2 * j[k] + 1) << (G.l[k] - S.lam[k]);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const int lk = G.l[k];
+          const int64_t i = int64_t(2 * j[k] + 1) << (lk - lam[k]);
           gi += (i - 1) * stride;
-          stride *= (int64_t(1) << G.l[k]) - 1;
+          stride *= (int64_t(1) << lk) - 1;
         }
         sum = __dadd_rn(sum, __dmul_rn(G.coeff, __ldg(G.grid + gi)));
       }
@@ -200,6 +208,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ Com
   }
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ CombiArgs A) {
   __shared__ int64_t s_binom[kCombiMaxN + 2][SGH_MAX_D + 1];
   __shared__ int64_t s_sbase[kCombiMaxN + 2];
@@ -215,20 +224,22 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const __grid_constant__ Co
     const int np = (int)min((int64_t)kCombiPts, G.N - p0);
     for (int qq = threadIdx.x; qq < np; qq += kThreads) {
       uint32_t rest = (uint32_t)(p0 + qq);       // N < 2^31 per grid (checked on the host)
-      int8_t lam[SGH_MAX_D];
+      int lam[D];
       int64_t in = 0;
       int sh = 0;
-      for (int k = 0; k < A.d; ++k) {             // x_1 fastest
-        const uint32_t nk = (1u << G.l[k]) - 1;
-        const uint32_t qk = fdiv(rest, G.fn[k]);
+#pragma unroll
+      for (int k = 0; k < D; ++k) {               // x_1 fastest
+        const int lk = G.l[k];
+        const uint32_t nk = (1u << lk) - 1;
+        const uint32_t qk = (k == D - 1) ? 0u : fdiv(rest, G.fn[k]);
         const uint32_t i = rest - qk * nk + 1;    // 1-based
         rest = qk;
         const int t = __ffs(i) - 1;
-        lam[k] = (int8_t)(G.l[k] - t);
+        lam[k] = lk - t;
         in += int64_t(i >> (t + 1)) << sh;
         sh += lam[k] - 1;
       }
-      G.grid[p0 + qq] = __ldg(A.sparse + sg_offset(lam, A.d, s_binom, s_sbase) + in);
+      G.grid[p0 + qq] = __ldg(A.sparse + sg_offset<D>(lam, s_binom, s_sbase) + in);
     }
   }
 }
@@ -417,8 +428,19 @@ static sgh_status run_combi(double *const *grids, const int32_t *levels, const d
   }
   const int64_t grid = std::min<int64_t>(A.tiles, int64_t(sms) * 8);
   ProfToken tok = prof_begin(s);
-  if (gather) k_gather<<<(unsigned)grid, kThreads, 0, s>>>(A);
-  else k_scatter<<<(unsigned)grid, kThreads, 0, s>>>(A);
+  switch (d) {
+#define SGH_COMBI_CASE(DD)                                             \
+  case DD:                                                             \
+    if (gather) k_gather<DD><<<(unsigned)grid, kThreads, 0, s>>>(A);   \
+    else k_scatter<DD><<<(unsigned)grid, kThreads, 0, s>>>(A);         \
+    break;
+    SGH_COMBI_CASE(1) SGH_COMBI_CASE(2) SGH_COMBI_CASE(3) SGH_COMBI_CASE(4) SGH_COMBI_CASE(5)
+    SGH_COMBI_CASE(6) SGH_COMBI_CASE(7) SGH_COMBI_CASE(8) SGH_COMBI_CASE(9) SGH_COMBI_CASE(10)
+    SGH_COMBI_CASE(11) SGH_COMBI_CASE(12) SGH_COMBI_CASE(13) SGH_COMBI_CASE(14) SGH_COMBI_CASE(15)
+    SGH_COMBI_CASE(16)
+#undef SGH_COMBI_CASE
+    default: return invalid("d out of range");
+  }
   e = cudaGetLastError();
   double pts = 0;
   for (const CombiGrid &G : P.grids) pts += double(G.N);
