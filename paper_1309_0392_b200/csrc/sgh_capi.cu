@@ -539,6 +539,8 @@ static double pass_cost(const std::vector<Task> &phases) {
     const Task &t = phases[i];
     const double bw = kind_bw(t);
     if (i == 0) {
+      // (charging blocked tiles for their 2 end rows, 2 / (2^t + 1), was tried:
+      // C5 150.3 vs 151.6 Gpoints/s -- not charged)
       c += 1.0 / bw;
     } else if (t.kind == KIND_FUSED) {
       // a lattice view of a blocked group: its share of the points, plus a
