@@ -34,6 +34,27 @@
 
 namespace sgh {
 
+// The hierarchization update of one point from its two predecessors, each
+// skipped if it lies on the boundary: x - 0.5 L, then
+// - 0.5 R (reading R5).  -DSGH_REDUCED_OP builds the paper's reduced-op
+// variant x - 0.5 (L + R) as an ablation: one multiply less, different
+// rounding (the paper saw no runtime gain; DESIGN.md reports B200).
+#ifdef SGH_REDUCED_OP
+#define HIER_UPDATE(x, cl, el, cr, er)           \
+  do {                                           \
+    const bool hl_ = (cl), hr_ = (cr);           \
+    if (hl_ && hr_) x = x - 0.5 * ((el) + (er)); \
+    else if (hl_) x = x - 0.5 * (el);            \
+    else if (hr_) x = x - 0.5 * (er);            \
+  } while (0)
+#else
+#define HIER_UPDATE(x, cl, el, cr, er) \
+  do {                                 \
+    if (cl) x = x - 0.5 * (el);        \
+    if (cr) x = x - 0.5 * (er);        \
+  } while (0)
+#endif
+
 // threads of a FUSED CTA, per tile kind (W == 1 contiguous / W > 1 column
 // tiles): 128 threads, 3 CTAs per SM, 70 KB tiles.  Measured on C5 (with the
 // host planning cached, so the step is GPU-bound): 128 threads 150.9, 192
@@ -262,8 +283,7 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
           const int c = lane + 32 * u;
           if (c < wc) {
             double x = xm[c];
-            if (i - s >= 1) x = x - 0.5 * xl[c];
-            if (i + s <= n) x = x - 0.5 * xr[c];
+            HIER_UPDATE(x, i - s >= 1, xl[c], i + s <= n, xr[c]);
             gout[c] = x;
           }
         }
@@ -383,8 +403,7 @@ __device__ __forceinline__ void pole_regs(double *p, int STR) {
     for (int i = 1; i <= n; ++i) {
       const int s = i & -i;
       double x = v[i - 1];
-      if (i - s >= 1) x = x - 0.5 * v[i - s - 1];
-      if (i + s <= n) x = x - 0.5 * v[i + s - 1];
+      HIER_UPDATE(x, i - s >= 1, v[i - s - 1], i + s <= n, v[i + s - 1]);
       p[(i - 1) * STR] = x;
     }
   } else {
@@ -428,8 +447,7 @@ __device__ __forceinline__ void block_fine(double *p0, int STR, bool lo_ok, bool
     for (int r = 1; r < B; ++r) {
       const int s = r & -r;
       double x = v[r];
-      if (r - s > 0 || lo_ok) x = x - 0.5 * v[r - s];   // left predecessor
-      if (r + s < B || hi_ok) x = x - 0.5 * v[r + s];   // right predecessor
+      HIER_UPDATE(x, r - s > 0 || lo_ok, v[r - s], r + s < B || hi_ok, v[r + s]);   // left, right
       p0[r * STR] = x;
     }
   } else {
@@ -619,8 +637,7 @@ __device__ __forceinline__ void warp_rows_hier(double *sm, int nrows, int l) {
       const int s = i & -i;
       if (i <= n) {
         double x = row[i - 1];
-        if (i - s >= 1) x = x - 0.5 * row[i - s - 1];   // left predecessor
-        if (i + s <= n) x = x - 0.5 * row[i + s - 1];   // right predecessor
+        HIER_UPDATE(x, i - s >= 1, row[i - s - 1], i + s <= n, row[i + s - 1]);
         out[m] = x;
       }
     }
@@ -728,8 +745,7 @@ __global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__
         const int s = i & -i;                          // 2^{tz(i)}
         const int sS = s * S;
         double x = sm[e];
-        if (i - s >= 1) x = x - 0.5 * sm[e - sS];      // left predecessor
-        if (i + s <= n) x = x - 0.5 * sm[e + sS];      // right predecessor
+        HIER_UPDATE(x, i - s >= 1, sm[e - sS], i + s <= n, sm[e + sS]);   // left, right
         g[e] = x;
       }
     } else {
@@ -792,8 +808,7 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
         const int s = rb & -rb;                            // tz(i) = tz(rb) < t
         const int sS = s * S;
         double x = sm[e];
-        if (i - s >= 1) x = x - 0.5 * sm[e - sS];
-        if (i + s <= n) x = x - 0.5 * sm[e + sS];
+        HIER_UPDATE(x, i - s >= 1, sm[e - sS], i + s <= n, sm[e + sS]);
         gr[e] = x;
       }
     } else {
@@ -1315,8 +1330,7 @@ __global__ void __launch_bounds__(kThreads) k_reg(const __grid_constant__ Src sr
         for (int i = 1; i <= n; ++i) {
           const int s = i & -i;
           double x = v[c][i - 1];
-          if (i - s >= 1) x = x - 0.5 * v[c][i - s - 1];
-          if (i + s <= n) x = x - 0.5 * v[c][i + s - 1];
+          HIER_UPDATE(x, i - s >= 1, v[c][i - s - 1], i + s <= n, v[c][i + s - 1]);
           p[c][(i - 1) * PS] = x;
         }
       } else {
