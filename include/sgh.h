@@ -127,7 +127,7 @@ size_t sgh_batched_host_buffer_bytes(const int32_t *levels, int32_t d, int64_t n
 /* End-to-end variant with HOST buffers (the e2e path): host_grids[g] are host
  * pointers (pinned for full PCIe speed), transformed in place.
  * device_buffer: >= sgh_batched_host_buffer_bytes() bytes, 256-byte aligned.
- * Grids are copied in, transformed and copied back in chunks of ~512 MB; the
+ * Grids are copied in, transformed and copied back in chunks of ~64 MB; the
  * copies run on two library-owned streams overlapped with the transform, and
  * `stream` waits for the last copy-out, so after synchronising `stream` every
  * host grid holds its result.  Asynchronous w.r.t. the host. */

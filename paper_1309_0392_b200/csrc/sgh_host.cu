@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -18,7 +19,16 @@
 
 namespace sgh {
 
-constexpr size_t kChunkBytes = size_t(512) << 20;
+// transfer chunk (SGH_E2E_CHUNK_MB overrides, experiments)
+static size_t chunk_bytes() {
+  static size_t b = 0;
+  if (!b) {
+    const char *e = getenv("SGH_E2E_CHUNK_MB");
+    const long mb = e ? atol(e) : 64;   // measured on C5: 64 MB 5.36, 128 MB 5.23, 512 MB 5.14, 2 GB 4.63 Gpoints/s
+    b = size_t(mb >= 16 && mb <= 8192 ? mb : 64) << 20;
+  }
+  return b;
+}
 
 struct HostLayout {
   std::vector<size_t> grid_off;              // byte offset of each grid in the device buffer
@@ -40,7 +50,7 @@ static sgh_status host_layout(const int32_t *levels, int32_t d, int64_t num_grid
     const size_t bytes = size_t(N) * 8;
     off += (bytes + 255) / 256 * 256;
     acc += bytes;
-    if (acc >= kChunkBytes || g == num_grids - 1) {
+    if (acc >= chunk_bytes() || g == num_grids - 1) {
       L.chunks.push_back({g0, g + 1});
       g0 = g + 1;
       acc = 0;
