@@ -734,10 +734,39 @@ __global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__
     const FDiv fS = T.fS, fNS = T.fNS;
     double *__restrict__ g = T.grid + T.base + o0 * T.OS;
     double *sm = smem + phase8(g);                      // same 16-byte phase as g
-    copy_range_async(sm, g, len);
+    // dehierarchization with few columns (S < 32): the lanes of a level are
+    // 2s S doubles apart, so the SMEM tile is padded by one double per 32
+    // (element e at e + e/32) to spread them over the banks
+    const bool padded = INV && S < 32;
+    if (padded) {
+      for (int e = threadIdx.x; e < len; e += kThreads) cp_async8(smem + e + (e >> 5), g + e);
+    } else {
+      copy_range_async(sm, g, len);
+    }
     cp_async_wait_all();
     __syncthreads();
-    if (!INV) {
+    if (padded) {
+      for (int lam = 2; lam <= l; ++lam) {             // coarse -> fine (reading R9)
+        const int s = 1 << (l - lam);
+        const int rows = 1 << (lam - 1);
+        const int cnt = ns * rows * S;
+        const int sS = s * S;
+        for (int k = threadIdx.x; k < cnt; k += kThreads) {
+          const uint32_t qq = fdiv((uint32_t)k, fS);
+          const int r = k - (int)qq * S;
+          const int slab = (int)(qq >> (lam - 1));
+          const int j = (int)qq & (rows - 1);
+          const int i = s * (2 * j + 1);
+          const int e = slab * nS + (i - 1) * S + r;
+          double x = smem[e + (e >> 5)];
+          if (i - s >= 1) x = x + 0.5 * smem[(e - sS) + ((e - sS) >> 5)];
+          if (i + s <= n) x = x + 0.5 * smem[(e + sS) + ((e + sS) >> 5)];
+          smem[e + (e >> 5)] = x;
+        }
+        __syncthreads();
+      }
+      for (int e = threadIdx.x; e < len; e += kThreads) g[e] = smem[e + (e >> 5)];
+    } else if (!INV) {
       for (int e = threadIdx.x; e < len; e += kThreads) {
         const uint32_t slab = fdiv((uint32_t)e, fNS);
         const uint32_t p = (uint32_t)e - slab * (uint32_t)nS;
@@ -797,10 +826,35 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
     // global element of local e = rb*S + r is  gr[e]
     double *__restrict__ gr = T.grid + T.base + o * T.OS + (int64_t)(i0 - 1) * S;
     double *sm = smem + phase8(gr);
-    copy_range_async(sm + rb_lo * S, gr + rb_lo * S, (rb_hi - rb_lo + 1) * S);
+    const bool padded = INV && S < 32;                 // see k_flat_slabs: one pad double per 32
+    if (padded) {
+      const int e0 = rb_lo * S, e1 = (rb_hi + 1) * S;
+      for (int e = e0 + threadIdx.x; e < e1; e += kThreads) cp_async8(smem + e + (e >> 5), gr + e);
+    } else {
+      copy_range_async(sm + rb_lo * S, gr + rb_lo * S, (rb_hi - rb_lo + 1) * S);
+    }
     cp_async_wait_all();
     __syncthreads();
-    if (!INV) {
+    if (padded) {
+      for (int s = B >> 1; s >= 1; s >>= 1) {              // block-local levels, coarse -> fine
+        const int cnt = (B / (2 * s)) * S;
+        const int sS = s * S;
+        for (int k = threadIdx.x; k < cnt; k += kThreads) {
+          const int jj = (int)fdiv((uint32_t)k, fS);
+          const int r = k - jj * S;
+          const int rb = s * (2 * jj + 1);
+          const int e = rb * S + r;
+          const int i = i0 + rb;
+          double x = smem[e + (e >> 5)];
+          if (i - s >= 1) x = x + 0.5 * smem[(e - sS) + ((e - sS) >> 5)];
+          if (i + s <= n) x = x + 0.5 * smem[(e + sS) + ((e + sS) >> 5)];
+          smem[e + (e >> 5)] = x;
+        }
+        __syncthreads();
+      }
+      const int e1 = B * S;
+      for (int e = S + threadIdx.x; e < e1; e += kThreads) gr[e] = smem[e + (e >> 5)];
+    } else if (!INV) {
       const int e1 = B * S;
       for (int e = S + threadIdx.x; e < e1; e += kThreads) {
         const int rb = (int)fdiv((uint32_t)e, fS);
@@ -1413,8 +1467,14 @@ static KernelFn kernel_for(int kind, int l, int w, bool inv) {
 size_t task_smem(const Task &t) {
   const int64_t n = (int64_t(1) << t.l) - 1;
   switch (t.kind) {
-    case KIND_FLAT_SLABS: return (size_t(t.R) * size_t(n * t.S) + 2) * 8;            // +1 phase shift
-    case KIND_FLAT_BLOCKS: return (size_t((int64_t(1) << t.t) + 1) * size_t(t.S) + 2) * 8;
+    case KIND_FLAT_SLABS: {                       // +1 phase shift, + 1 pad per 32 (INV, S < 32)
+      const size_t e = size_t(t.R) * size_t(n * t.S);
+      return (e + e / 32 + 2) * 8;
+    }
+    case KIND_FLAT_BLOCKS: {
+      const size_t e = size_t((int64_t(1) << t.t) + 1) * size_t(t.S);
+      return (e + e / 32 + 2) * 8;
+    }
     case KIND_STRIDED: return size_t((int64_t(1) << t.t) + 1) * size_t(t.W + 2) * 8;
     case KIND_FUSED:
       return t.W == 1 ? (size_t(t.R) * size_t(t.P) + 2) * 8 : (size_t(t.P) * size_t(t.W + 1) + 2) * 8;
