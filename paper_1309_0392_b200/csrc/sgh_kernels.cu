@@ -1193,8 +1193,8 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     if (R == 1) fused_axis<INV, W, true>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr);
     else fused_axis<INV, W>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr);
   }
-#ifdef SGH_DEBUG_NOMEMORY
-  return;                                         // timing experiment: compute only
+#if defined(SGH_DEBUG_NOMEMORY) || defined(SGH_DEBUG_NOSTORE)
+  return;                                         // timing experiments: compute only / no store
 #endif
   if (T.bj >= 0) {
     if (W == 1) fused_segments<true>(T, f, sm);
