@@ -243,9 +243,12 @@ def sgh_arm(args, rank, world, local_rank):
     members, ids, desc = workload(args.workload)
     sizes = [si.num_points(l) for l in members]
     sharded = args.workload == "C4" and world > 1
-    if args.workload in ("C5", "C5cycle") and world > 1:
+    if args.workload == "C5" and world > 1:
         part = si.lpt_partition(sizes, world)[rank]
         my_members, my_ids = [members[i] for i in part], [ids[i] for i in part]
+    elif args.workload == "C5cycle" and world > 1:   # the gather chain needs contiguous grid blocks
+        b0, b1 = si.contiguous_partition(sizes, world)[rank]
+        my_members, my_ids = members[b0:b1], ids[b0:b1]
     else:
         my_members, my_ids = members, ids
     total_points = sum(sizes) if (args.workload in ("C5", "C5cycle") or sharded) else sum(sizes) * world
@@ -285,9 +288,10 @@ def sgh_arm(args, rank, world, local_rank):
 
             def step():
                 batch.hierarchize(fuse=fuse)
-                sgh.gather(batch.views, my_members, coeffs, cfg.n, sparse)
-                if world > 1:   # the combined surpluses are the sum over ranks (each holds some grids)
-                    dist.all_reduce(sparse)
+                if world > 1:   # ranks continue each other's sums in grid order, then broadcast
+                    sgh.gather_chain(batch.views, my_members, coeffs, cfg.n, sparse)
+                else:
+                    sgh.gather(batch.views, my_members, coeffs, cfg.n, sparse)
                 sgh.scatter(sparse, batch.views, my_members, cfg.n)
                 batch.dehierarchize(fuse=fuse)
         my_points = batch.total_points
@@ -398,7 +402,9 @@ def sgh_arm(args, rank, world, local_rank):
                "config": {"workload": desc, "points": total_points, "bytes": 8 * total_points,
                           "l2": ("L2 flushed before every step (256 MB write, outside the per-step events)"
                                  if flush_l2 else "inputs larger than L2 (no flush needed)"),
-                          "parallelism": (f"grids LPT-balanced over {world} ranks" if args.workload in ("C5", "C5cycle")
+                          "parallelism": (f"grids LPT-balanced over {world} ranks" if args.workload == "C5" else
+                                          f"contiguous grid blocks over {world} ranks, gather chain + broadcast"
+                                          if args.workload == "C5cycle"
                                           else ((f"sharded along x_d, {'halo + coarse-lattice all-gather' if args.sharded == 'halo' else 'NCCL all-to-all'}")
                                                 if sharded else "replicas")),
                           "seed": si.SEED},

@@ -283,6 +283,32 @@ size_t sgh_combi_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_g
 sgh_status sgh_gather(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
                       int64_t num_grids, int32_t n, double *sparse, void *workspace, size_t ws_bytes, void *stream);
 
+/* GATHER over a RANGE of subspaces, optionally continuing a running sum.
+ *  sub_begin, sub_end: subspace indices in SG order (level sum ascending,
+ *          then lexicographic, 0 <= sub_begin <= sub_end <=
+ *          sgh_sparse_num_subspaces(d, n)); only the sparse points of these
+ *          subspaces -- the contiguous range [sgh_sparse_subspace_offset(d, n,
+ *          sub_begin), ..offset(sub_end)) -- are read or written.
+ *  flags:  0 or SGH_FLAG_ACCUMULATE: each sum starts from the value already in
+ *          sparse (the running sum of the grids that come earlier in the global
+ *          grid order) instead of +0.0.  A partition of the grid list into
+ *          CONTIGUOUS blocks, gathered block after block with ACCUMULATE,
+ *          performs exactly the additions of one gather over the whole list,
+ *          in the same order: bitwise equal.  That is the multi-GPU
+ *          gather: rank r owns grid block r and continues the
+ *          partial sums received from rank r-1, pipelined over subspace
+ *          ranges (paper_1309_0392_b200.gather_chain).
+ *  The workspace of sgh_combi_workspace_bytes (full range) is sufficient. */
+#define SGH_FLAG_ACCUMULATE 16u
+sgh_status sgh_gather_ex(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
+                         int64_t num_grids, int32_t n, double *sparse, int64_t sub_begin, int64_t sub_end,
+                         uint32_t flags, void *workspace, size_t ws_bytes, void *stream);
+/* Number of subspaces W_lam of the sparse grid (C(n, d)), and the sparse
+ * offset of subspace index i in SG order (i = count: the total points); -1 on
+ * invalid arguments. */
+int64_t sgh_sparse_num_subspaces(int32_t d, int32_t n);
+int64_t sgh_sparse_subspace_offset(int32_t d, int32_t n, int64_t index);
+
 /* SCATTER: every point of every grid receives its sparse-grid value
  * (restriction of the combined surpluses; dehierarchize the grids afterwards
  * for nodal values). */

@@ -37,6 +37,7 @@ FLAG_DEHIERARCHIZE = 1
 FLAG_PER_AXIS = 2
 FLAG_WHOLE_POLES = 4
 FLAG_SCATTER = 8
+FLAG_ACCUMULATE = 16
 STATUS = {0: "SGH_OK", 1: "SGH_ERR_INVALID_ARGUMENT", 2: "SGH_ERR_CAPACITY", 3: "SGH_ERR_CUDA",
           4: "SGH_ERR_NCCL", 5: "SGH_ERR_WORKSPACE"}
 
@@ -93,6 +94,10 @@ def _load():
         "sgh_gather": (st, [vpp, i32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64,
                             ctypes.c_int32, vp, vp, sz, vp]),
         "sgh_scatter": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, vp, vp, sz, vp]),
+        "sgh_gather_ex": (st, [vpp, i32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64,
+                               ctypes.c_int32, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
+        "sgh_sparse_num_subspaces": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
+        "sgh_sparse_subspace_offset": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]),
         "sgh_profile_enable": (st, [ctypes.c_int32]),
         "sgh_profile_read": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int64]),
         "sgh_status_string": (ctypes.c_char_p, [st]),
@@ -115,7 +120,8 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_transform_sharded_halo", "sgh_transform_sharded_halo_loopback", "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
             "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_sparse_num_points",
-            "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter",
+            "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter", "sgh_gather_ex",
+            "sgh_sparse_num_subspaces", "sgh_sparse_subspace_offset",
             "sgh_status_string", "sgh_last_error", "sgh_version")
 
 
@@ -525,6 +531,88 @@ def gather(grids, levels_list, coeffs, n: int, sparse: torch.Tensor = None, stre
     with torch.cuda.device(dev):
         _check(lib.sgh_gather(ptrs, flat, c, d, len(grids), int(n), ctypes.c_void_p(sparse.data_ptr()),
                               ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
+    return sparse
+
+
+def sparse_num_subspaces(d: int, n: int) -> int:
+    """Subspaces W_lam of the sparse grid of level sum n (C(n, d))."""
+    return int(lib.sgh_sparse_num_subspaces(int(d), int(n)))
+
+
+def sparse_subspace_offset(d: int, n: int, index: int) -> int:
+    """Sparse offset of subspace ``index`` in SG order (index == count: the total)."""
+    r = int(lib.sgh_sparse_subspace_offset(int(d), int(n), int(index)))
+    if r < 0:
+        raise SGHError(1, "subspace index out of range")
+    return r
+
+
+def gather_ex(grids, levels_list, coeffs, n: int, sparse: torch.Tensor, sub_begin: int, sub_end: int,
+              accumulate: bool = False, stream=None) -> torch.Tensor:
+    """Gather restricted to subspaces [sub_begin, sub_end) (SG order); with
+    ``accumulate`` every sum continues from the value already in ``sparse``
+    (sgh.h sgh_gather_ex, SGH_FLAG_ACCUMULATE)."""
+    d, flat, ptrs = _combi_common(grids, levels_list)
+    dev = grids[0].device
+    wsb = int(lib.sgh_combi_workspace_bytes(flat, d, len(grids), int(n), 0))
+    ws = torch.empty(max(wsb, 16) // 8 + 2, dtype=torch.float64, device=dev)
+    c = (ctypes.c_double * len(grids))(*[float(x) for x in coeffs])
+    with torch.cuda.device(dev):
+        _check(lib.sgh_gather_ex(ptrs, flat, c, d, len(grids), int(n), ctypes.c_void_p(sparse.data_ptr()),
+                                 int(sub_begin), int(sub_end), FLAG_ACCUMULATE if accumulate else 0,
+                                 ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
+    return sparse
+
+
+def subspace_chunks(d: int, n: int, chunks: int):
+    """Split the subspaces (SG order) into at most ``chunks`` consecutive ranges
+    of about equal point counts: [(sub_begin, sub_end, off_begin, off_end)]."""
+    nsub = sparse_num_subspaces(d, n)
+    total = sparse_subspace_offset(d, n, nsub)
+    out, b = [], 0
+    for k in range(1, chunks + 1):
+        target = total * k // chunks
+        lo, hi = b, nsub                       # smallest e with offset(e) >= target
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if sparse_subspace_offset(d, n, mid) >= target:
+                hi = mid
+            else:
+                lo = mid + 1
+        e = max(lo, b + 1) if k < chunks else nsub
+        e = min(e, nsub)
+        if e > b:
+            out.append((b, e, sparse_subspace_offset(d, n, b), sparse_subspace_offset(d, n, e)))
+            b = e
+        if b >= nsub:
+            break
+    return out
+
+
+def gather_chain(grids, levels_list, coeffs, n: int, sparse: torch.Tensor, group=None, chunks: int = 16,
+                 gather_fn=None) -> torch.Tensor:
+    """Multi-rank gather, bitwise equal to one gather over the
+    concatenation of the ranks' grid lists in rank order: each rank must hold
+    a CONTIGUOUS block of the global grid order.  Rank r receives the running
+    sums of a subspace range from rank r-1, continues them over its own grids
+    (SGH_FLAG_ACCUMULATE), and passes them on, range after range, so the ranks
+    work on different ranges at once; the last rank then broadcasts the
+    sparse grid to all (every rank's scatter needs it).  ``gather_fn(b, e,
+    accumulate)`` replaces the device gather in CPU tests of the exchange."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    d = len(levels_list[0])
+    if gather_fn is None:
+        gather_fn = lambda b, e, acc: gather_ex(grids, levels_list, coeffs, n, sparse, b, e, accumulate=acc)  # noqa: E731
+    for b, e, lo, hi in subspace_chunks(d, n, chunks):
+        part = sparse[lo:hi]
+        if rank > 0:
+            dist.recv(part, src=dist.get_global_rank(group, rank - 1) if group is not None else rank - 1, group=group)
+        gather_fn(b, e, rank > 0)
+        if rank < world - 1:
+            dist.send(part, dst=dist.get_global_rank(group, rank + 1) if group is not None else rank + 1, group=group)
+    last = dist.get_global_rank(group, world - 1) if group is not None else world - 1
+    dist.broadcast(sparse, src=last, group=group)
     return sparse
 
 

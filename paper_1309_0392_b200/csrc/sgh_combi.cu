@@ -71,6 +71,7 @@ struct CombiArgs {
   int64_t sbase[kCombiMaxN + 2];   // offset of the first subspace of level sum s
   double *sparse;
   int32_t d, n;
+  int32_t accumulate;              // gather: sums start from the values in sparse (SGH_FLAG_ACCUMULATE)
 };
 
 // binom / sbase: the tables staged in SMEM (lanes index them with different
@@ -211,9 +212,12 @@ __global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ Com
         rest >>= b;
       }
     }
-    double sum[K];
+    double sum[K];                                 // +0.0, or the running sum of earlier grids
 #pragma unroll
-    for (int u = 0; u < K; ++u) sum[u] = 0.0;
+    for (int u = 0; u < K; ++u) {
+      const int qq = threadIdx.x + u * kThreads;
+      sum[u] = (A.accumulate && qq < np) ? A.sparse[s_sub.off + p0 + qq] : 0.0;
+    }
     for (int cb = 0; cb < nc; cb += kGBatch) {
       const int nb = min(kGBatch, nc - cb);
       __syncthreads();                             // previous batch consumed
@@ -359,7 +363,8 @@ struct CombiPlan {
 };
 
 static sgh_status build_combi_plan(double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
-                                   int64_t num_grids, int32_t n, bool gather, CombiPlan &P) {
+                                   int64_t num_grids, int32_t n, bool gather, CombiPlan &P, int64_t sub_begin = 0,
+                                   int64_t sub_end = INT64_MAX) {
   P.M = sparse_bases(d, n, P.sbase);
   if (P.M < 0) return invalid("unsupported (d, n) for the sparse grid (d <= 16, n <= 62)");
   if (num_grids >= (int64_t(1) << 31)) return invalid("too many grids");
@@ -403,11 +408,23 @@ static sgh_status build_combi_plan(double *const *grids, const int32_t *levels, 
     return SGH_OK;
   }
   std::vector<int> lam(d);
-  for (int s = d; s <= n; ++s) {                   // subspaces in SG order
+  int64_t si = 0;                                  // subspace index in SG order
+  for (int s = d; s <= n && si < sub_end; ++s) {   // subspaces in SG order
+    const int64_t cnt = binom_host(s - 1, d - 1);
+    if (si + cnt <= sub_begin) {                   // level sum entirely before the range
+      si += cnt;
+      continue;
+    }
     for (int k = 0; k < d - 1; ++k) lam[k] = 1;
     lam[d - 1] = s - (d - 1);
     int64_t off = P.sbase[s];
     do {
+      const bool in = si >= sub_begin && si < sub_end;
+      ++si;
+      if (!in) {
+        off += int64_t(1) << (s - d);
+        continue;
+      }
       CombiSub S;
       std::memset(&S, 0, sizeof S);
       S.off = off;
@@ -435,13 +452,15 @@ static int64_t resident_grid(KernelFn fn, int64_t tiles, int sms) {
 
 static sgh_status run_combi(double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
                             int64_t num_grids, int32_t n, double *sparse, void *workspace, size_t ws_bytes,
-                            cudaStream_t s, bool gather) {
+                            cudaStream_t s, bool gather, int64_t sub_begin = 0, int64_t sub_end = INT64_MAX,
+                            uint32_t flags = 0) {
   if (num_grids < 0) return invalid("num_grids < 0");
   if (!levels || (num_grids > 0 && !grids) || !sparse || (gather && num_grids > 0 && !coeffs))
     return invalid("NULL argument");
   if (num_grids == 0 && !gather) return SGH_OK;
+  if (flags & ~uint32_t(SGH_FLAG_ACCUMULATE)) return invalid("unknown gather flags");
   CombiPlan P;
-  sgh_status st = build_combi_plan(grids, levels, coeffs, d, num_grids, n, gather, P);
+  sgh_status st = build_combi_plan(grids, levels, coeffs, d, num_grids, n, gather, P, sub_begin, sub_end);
   if (st != SGH_OK) return st;
   const size_t need = P.bytes();
   if (!workspace || ws_bytes < need || (reinterpret_cast<uintptr_t>(workspace) & 15)) {
@@ -469,6 +488,7 @@ static sgh_status run_combi(double *const *grids, const int32_t *levels, const d
   A.sparse = sparse;
   A.d = d;
   A.n = n;
+  A.accumulate = (flags & SGH_FLAG_ACCUMULATE) ? 1 : 0;
   if (A.items == 0 || A.tiles == 0) return SGH_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -513,6 +533,23 @@ extern "C" {
 
 int64_t sgh_sparse_num_points(int32_t d, int32_t n) { return sparse_bases(d, n, nullptr); }
 
+int64_t sgh_sparse_num_subspaces(int32_t d, int32_t n) {
+  if (sparse_bases(d, n, nullptr) < 0) return -1;
+  return binom_host(n, d);                         // sum_{s=d}^{n} C(s-1, d-1)
+}
+
+int64_t sgh_sparse_subspace_offset(int32_t d, int32_t n, int64_t index) {
+  int64_t sbase[kCombiMaxN + 2];
+  if (sparse_bases(d, n, sbase) < 0 || index < 0 || index > binom_host(n, d)) return -1;
+  int64_t first = 0;                               // index of the first subspace of level sum s
+  for (int s = d; s <= n; ++s) {
+    const int64_t cnt = binom_host(s - 1, d - 1);
+    if (index < first + cnt) return sbase[s] + ((index - first) << (s - d));
+    first += cnt;
+  }
+  return sbase[n + 1];                             // index == count: the total
+}
+
 size_t sgh_combi_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, int32_t n, uint32_t flags) {
   if (!levels || num_grids < 0) return 0;
   CombiPlan P;
@@ -525,6 +562,17 @@ sgh_status sgh_gather(const double *const *grids, const int32_t *levels, const d
                       int64_t num_grids, int32_t n, double *sparse, void *workspace, size_t ws_bytes, void *stream) {
   return run_combi(const_cast<double *const *>(grids), levels, coeffs, d, num_grids, n, sparse, workspace, ws_bytes,
                    static_cast<cudaStream_t>(stream), true);
+}
+
+sgh_status sgh_gather_ex(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
+                         int64_t num_grids, int32_t n, double *sparse, int64_t sub_begin, int64_t sub_end,
+                         uint32_t flags, void *workspace, size_t ws_bytes, void *stream) {
+  const int64_t nsub = sgh_sparse_num_subspaces(d, n);
+  if (nsub < 0) return invalid("unsupported (d, n) for the sparse grid");
+  if (sub_begin < 0 || sub_end < sub_begin || sub_end > nsub) return invalid("subspace range out of bounds");
+  if (sub_begin == sub_end) return SGH_OK;
+  return run_combi(const_cast<double *const *>(grids), levels, coeffs, d, num_grids, n, sparse, workspace, ws_bytes,
+                   static_cast<cudaStream_t>(stream), true, sub_begin, sub_end, flags);
 }
 
 sgh_status sgh_scatter(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, int32_t n,

@@ -163,3 +163,28 @@ def lpt_partition(sizes, nparts: int):
     for p in parts:
         p.sort()
     return parts
+
+
+def contiguous_partition(sizes, nparts: int):
+    """Split the ORDERED item list into nparts contiguous, non-empty blocks of
+    about equal size sums: [(begin, end)].  (The multi-rank gather needs each
+    rank to hold a contiguous block of the grid order; workload partitioning,
+    not method arithmetic.)"""
+    n = len(sizes)
+    if nparts < 1 or n < nparts:
+        raise ValueError("need at least one item per part")
+    prefix = [0]
+    for s in sizes:
+        prefix.append(prefix[-1] + s)
+    total = prefix[-1]
+    bounds = [0]
+    for k in range(1, nparts):
+        target = total * k / nparts
+        i = bounds[-1] + 1                          # smallest end whose prefix reaches the target
+        while i < n - (nparts - k) and prefix[i] < target:
+            i += 1
+        if i > bounds[-1] + 1 and abs(prefix[i - 1] - target) <= abs(prefix[i] - target):
+            i -= 1                                  # the nearer boundary
+        bounds.append(i)
+    bounds.append(n)
+    return [(bounds[k], bounds[k + 1]) for k in range(nparts)]

@@ -176,3 +176,30 @@ def test_plan_two_blocked_forced(monkeypatch):
         N = si.num_points(lv)
         assert p[0][0][2] < N <= sum(x for _, _, x in p[0])
     assert len(_plan_passes((14, 13), inverse=True)) == 2       # hierarchization only
+
+
+@pytest.mark.parametrize("d,n", [(1, 9), (2, 7), (3, 8), (4, 22), (5, 9)])
+def test_sparse_subspace_offsets(d, n):
+    """sgh_sparse_num_subspaces / sgh_sparse_subspace_offset (host): the SG
+    order enumerated directly (level sum ascending, then lexicographic, each
+    W_lam of 2^{|lam|-d} points) gives the same offsets; the last is the total."""
+    import itertools
+    from math import comb
+    import paper_1309_0392_b200 as sgh
+    nsub = sgh.sparse_num_subspaces(d, n)
+    assert nsub == comb(n, d)
+    if nsub > 20000:
+        idx = [0, 1, nsub // 3, nsub - 1, nsub]
+    else:
+        idx = list(range(nsub + 1))
+    subs = []
+    for s in range(d, n + 1):
+        subs += sorted(c for c in itertools.product(range(1, s - d + 2), repeat=d) if sum(c) == s) if nsub <= 20000 else []
+    if subs:
+        off = [0]
+        for lam in subs:
+            off.append(off[-1] + (1 << (sum(lam) - d)))
+        assert [sgh.sparse_subspace_offset(d, n, i) for i in idx] == off
+    assert sgh.sparse_subspace_offset(d, n, nsub) == sgh.sparse_num_points(d, n)
+    with pytest.raises(sgh.SGHError):
+        sgh.sparse_subspace_offset(d, n, nsub + 1)

@@ -252,3 +252,55 @@ def _halo_worker(rank, world, port, levels, inverse):
 @pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
 def test_sharded_halo_decomposition_gloo(levels, world, inverse):
     mp.spawn(_halo_worker, args=(world, _free_port(), levels, inverse), nprocs=world, join=True)
+
+
+def _chain_worker(rank, world, port, d, n, chunks):
+    """Multi-rank gather (paper_1309_0392_b200.gather_chain):
+    rank r holds a contiguous block of the combination set's grid order and
+    continues, subspace range by range, the running sums received from rank
+    r-1 (the library's exchange code, with the oracle's per-grid products as
+    the per-rank compute); the last rank broadcasts.  Every rank ends with the
+    single-process oracle gather, bitwise."""
+    _init(rank, world, port)
+    import oracle
+    import paper_1309_0392_b200 as sgh
+    import sgh_inputs as si
+    cs = si.combination_set(d, n)
+    co = [float(si.combination_coefficient(d, n, lv)) for lv in cs]
+    hosts = [oracle.hierarchize(si.fill_uniform(si.num_points(lv), grid_id=g), lv) for g, lv in enumerate(cs)]
+    b0, b1 = si.contiguous_partition([si.num_points(lv) for lv in cs], world)[rank]
+    terms = [oracle.gather([hosts[g]], [cs[g]], [co[g]], n) for g in range(b0, b1)]   # coeff_g * alpha_g
+    sparse = torch.full((sgh.sparse_num_points(d, n),), float("nan"), dtype=torch.float64)
+
+    def gather_fn(b, e, accumulate):                  # the oracle's accumulation, grid after grid
+        lo, hi = sgh.sparse_subspace_offset(d, n, b), sgh.sparse_subspace_offset(d, n, e)
+        seg = sparse[lo:hi].numpy()
+        if not accumulate:
+            seg[:] = 0.0
+        for t in terms:
+            seg[:] = seg + t[lo:hi]
+
+    sgh.gather_chain(None, cs[b0:b1], co[b0:b1], n, sparse, chunks=chunks, gather_fn=gather_fn)
+    want = oracle.gather(hosts, cs, co, n)
+    assert np.array_equal(sparse.numpy().view(np.uint64), want.view(np.uint64))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d,n,world,chunks", [(3, 8, 2, 5), (2, 9, 3, 4), (4, 8, 4, 16)], ids=str)
+def test_gather_chain_gloo(d, n, world, chunks):
+    mp.spawn(_chain_worker, args=(world, _free_port(), d, n, chunks), nprocs=world, join=True)
+
+
+def test_contiguous_partition():
+    import sys
+    sys.path.insert(0, ROOT)
+    import sgh_inputs as si
+    cs = si.combination_set(4, 22)
+    sizes = [si.num_points(lv) for lv in cs]
+    for P in (2, 4, 8):
+        blocks = si.contiguous_partition(sizes, P)
+        assert blocks[0][0] == 0 and blocks[-1][1] == len(cs)
+        assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(blocks, blocks[1:] + [(len(cs), len(cs) + 1)]))
+        loads = [sum(sizes[b:e]) for b, e in blocks]
+        assert max(loads) / (sum(loads) / P) < 1.01

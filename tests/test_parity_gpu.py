@@ -385,6 +385,28 @@ def test_gather_scatter_bitwise(sgh, d, n):
         assert_bitwise(o.cpu().numpy(), w)
 
 
+@pytest.mark.parametrize("d,n,split,chunks", [(2, 8, 3, 4), (3, 8, 10, 5), (4, 9, 17, 16), (5, 8, 40, 7)])
+def test_gather_ex_chain_bitwise(sgh, d, n, split, chunks):
+    """sgh_gather_ex: the grid list split into two CONTIGUOUS blocks, the
+    second gathered range by range with SGH_FLAG_ACCUMULATE onto the first's
+    sums (what gather_chain does across ranks), equals one gather over all
+    grids bitwise; so do range-by-range gathers without accumulation."""
+    cs = si.combination_set(d, n)
+    co = [float(si.combination_coefficient(d, n, lv)) for lv in cs]
+    hosts = [oracle.hierarchize(si.fill_uniform(si.num_points(lv), grid_id=g), lv) for g, lv in enumerate(cs)]
+    grids = [torch.from_numpy(h).cuda() for h in hosts]
+    want = oracle.gather(hosts, cs, co, n)
+    split = min(split, len(cs) - 1)
+    sp = sgh.gather(grids[:split], cs[:split], co[:split], n)
+    for b, e, lo, hi in sgh.subspace_chunks(d, n, chunks):
+        sgh.gather_ex(grids[split:], cs[split:], co[split:], n, sp, b, e, accumulate=True)
+    assert_bitwise(sp.cpu().numpy(), want)
+    sp2 = torch.full((sgh.sparse_num_points(d, n),), float("nan"), dtype=torch.float64, device="cuda")
+    for b, e, lo, hi in sgh.subspace_chunks(d, n, chunks):
+        sgh.gather_ex(grids, cs, co, n, sp2, b, e)
+    assert_bitwise(sp2.cpu().numpy(), want)
+
+
 def test_gather_closed_form_c5_subset(sgh):
     """f = prod x(1-x) on the largest members of the C5 set that fit the oracle
     quickly... the full C5 set: every sparse point equals prod 4^-lam exactly
