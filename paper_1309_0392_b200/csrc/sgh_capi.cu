@@ -416,8 +416,19 @@ bool plan_view_fine(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, 
 //   4  the coarse-b lattice over all columns (level l_b - t2, stride 2^t2 n_a).
 // Phases 1-4 move ~2^-t1 + 2^-t2 of the points.  Bitwise equal to Alg. 1: every
 // point receives the same operations in the same order (axis a, then b).
+// Dehierarchization (inv): the oracle applies H_a^-1 to every point, then
+// H_b^-1, each coarse -> fine.  Execution order: (1) the a-lattice of every
+// row, (2) the fine-a part of the coarse-b rows, (3) the b-lattice of the
+// coarse-b rows -- the coarse-b rows are now final -- (4) the tiles: H_a^-1 on
+// their fine-b rows (a-ends: the coarse-a points of those rows, a-inverted by
+// (1), not yet b-inverted), then H_b^-1 on the fine-a columns with the final
+// b-end rows, written fine along both axes; the tile must not touch its b-end
+// rows; (5) the fine-b part of the coarse-a columns (task 2 without its a
+// transform).  Every point sees the oracle's operations in its order:
+// bitwise.  Phases are emitted so that the runner's reversal for
+// dehierarchization yields this order.
 static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, int t1, int t2,
-                             std::vector<Task> &phases) {
+                             std::vector<Task> &phases, bool inv = false) {
   if (a + 1 >= d) return false;
   for (int k = 0; k < d; ++k)
     if (k != a && k != a + 1 && levels[k] != 1) return false;
@@ -460,15 +471,9 @@ static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, 
   t.ncb = 1;
   t.tiles = int64_t(1) << (t.nb_log + t.nb2_log);
   finish_fused(t);
-  phases.push_back(t);
   const int64_t s1 = int64_t(1) << t1, s2 = int64_t(1) << t2;
   const int64_t nla = (int64_t(1) << (la - t1)) - 1;   // coarse-a columns
-  if (nla * e2 > fused_budget_w1() + fused_budget_w1() / 16) {
-    phases.resize(first);
-    return false;
-  }
-  // 1: fine-a part on the coarse-b rows
-  bool ok = plan_view_fine(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, 1, 1, (s2 - 1) * na, la, t1, phases);
+  if (nla * e2 > fused_budget_w1() + fused_budget_w1() / 16) return false;
   // 2: the coarse-a columns in b-blocks: the whole a-lattice of every row of the
   //    block (its end rows only as halo, not written), then the fine-b part
   Task c = t;
@@ -485,11 +490,30 @@ static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, 
   c.aligned = 0;
   c.tiles = int64_t(1) << c.nb2_log;
   finish_fused(c);
-  phases.push_back(c);
-  // 3: the a-lattice on the coarse-b rows (the points coarse along both axes)
-  plan_view(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, s1, 1, (s2 - 1) * na + s1 - 1, la - t1, phases);
-  // 4: the coarse-b lattice over all columns
-  plan_view(grid, 1, 0, s2 * na, na, (s2 - 1) * na, lb - t2, phases);
+  bool ok;
+  if (!inv) {
+    phases.push_back(t);
+    // 1: fine-a part on the coarse-b rows
+    ok = plan_view_fine(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, 1, 1, (s2 - 1) * na, la, t1, phases);
+    phases.push_back(c);
+    // 3: the a-lattice on the coarse-b rows (the points coarse along both axes)
+    plan_view(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, s1, 1, (s2 - 1) * na + s1 - 1, la - t1, phases);
+    // 4: the coarse-b lattice over all columns
+    plan_view(grid, 1, 0, s2 * na, na, (s2 - 1) * na, lb - t2, phases);
+  } else {                                           // emitted reversed (see above)
+    Task c5 = c;
+    c5.skipmask = 1u;                                // (5) fine-b of the coarse-a columns only
+    phases.push_back(c5);
+    phases.push_back(t);                             // (4)
+    plan_view(grid, 1, 0, s2 * na, na, (s2 - 1) * na, lb - t2, phases);                           // (3)
+    ok = plan_view_fine(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, 1, 1, (s2 - 1) * na, la, t1, phases);  // (2)
+    // (1) the a-lattice: of the coarse-b rows as a view, of the fine-b rows as
+    //     task 2's tiles without their b transform (they store the fine-b rows)
+    plan_view(grid, (int64_t(1) << (lb - t2)) - 1, s2 * na, s1, 1, (s2 - 1) * na + s1 - 1, la - t1, phases);
+    Task c1 = c;
+    c1.skipmask = 2u;
+    phases.push_back(c1);
+  }
   if (!ok) phases.resize(first);
   return ok;
 }
@@ -535,28 +559,35 @@ static double kind_bw(const Task &t) {
 
 static double pass_cost(const std::vector<Task> &phases) {
   double c = 0;
+  // the main phase (most points; phases[0] in hierarchization order, but not
+  // in the reversed-emitted dehierarchization two-blocked list); the others
+  // are charged relative to it
+  size_t m0 = 0;
+  for (size_t i = 1; i < phases.size(); ++i)
+    if (task_points(phases[i]) > task_points(phases[m0])) m0 = i;
+  const double ref = phases.empty() ? 1.0 : std::max(1.0, task_points(phases[m0]));
   for (size_t i = 0; i < phases.size(); ++i) {
     const Task &t = phases[i];
     const double bw = kind_bw(t);
-    if (i == 0) {
+    if (i == m0) {
       // (charging blocked tiles for their 2 end rows, 2 / (2^t + 1), was tried:
       // C5 150.3 vs 151.6 Gpoints/s -- not charged)
       c += 1.0 / bw;
     } else if (t.kind == KIND_FUSED) {
       // a lattice view of a blocked group: its share of the points, plus a
       // fixed per-phase cost (a few % of a pass: launch tail, small tiles)
-      c += task_points(t) / std::max(1.0, task_points(phases[0])) / (0.7 * bw) + 0.01;
+      c += task_points(t) / ref / (0.7 * bw) + 0.01;
     } else if (t.S < 8 && t.PS != t.S) {
       // a view whose elements are isolated (one per 32-byte sector, no two in
       // a row): measured ~0.13 TB/s algorithmic (STRIDED, C4 cross phases)
-      c += task_points(t) / std::max(1.0, task_points(phases[0])) / 0.15;
-    } else if (task_points(t) > 0.01 * task_points(phases[0])) {
+      c += task_points(t) / ref / 0.15;
+    } else if (task_points(t) > 0.01 * ref) {
       // a sizeable later phase of contiguous rows (e.g. the coarse-b rows of a
       // two-blocked plan): half the kernel's streaming rate
-      c += task_points(t) / std::max(1.0, task_points(phases[0])) / (0.5 * bw);
+      c += task_points(t) / ref / (0.5 * bw);
     } else {
       // later phases are coarse lattices: a small fraction of the points, latency bound
-      c += 2.0 * task_points(t) / std::max(1.0, task_points(phases[0])) / 1.0;
+      c += 2.0 * task_points(t) / ref / 1.0;
     }
   }
   return c;
@@ -623,7 +654,7 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
     }
   }
   // two-blocked plan (grids with exactly two adjacent non-trivial axes)
-  if (blocked_ok && !inv) {
+  if (blocked_ok) {
     std::vector<Task> bestp;
     // SGH_TWO_BLOCKED=force: take a two-blocked plan whenever one exists (tests)
     const char *tb = getenv("SGH_TWO_BLOCKED");
@@ -636,7 +667,7 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
         for (int t2 = 2; t2 < levels[a + 1]; ++t2) {
           if (ft1 >= 0 && (t1 != ft1 || t2 != ft2)) continue;
           std::vector<Task> ph;
-          if (!plan_two_blocked(grid, levels, d, a, t1, t2, ph)) continue;
+          if (!plan_two_blocked(grid, levels, d, a, t1, t2, ph, inv)) continue;
           const double c = pass_cost(ph);
           if (c < bc - 1e-12) {
             bc = c;

@@ -675,9 +675,13 @@ __device__ __forceinline__ bool warp_rows_dispatch(double *sm, int nrows, int l)
 // lattice recursion as fused_axis: 2^kTB-point sub-blocks at strides 1, 2^kTB,
 // .. (K = t / kTB levels), then the top lattice of 2^{t - kTB K} + 1 points.
 // lo_ok / hi_ok: the block's ends are grid points (false: the zero boundary).
+// skip_oe (dehierarchization of a two-blocked tile, axis a): poles in the
+// first / last outer row (oo = 0, Ok - 1: the second blocked axis' end rows,
+// final values) are left untouched.
 template <bool INV, int W, int NT = FT<W>::v>
 __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int R, const FDiv fR, int Ok,
-                                                 bool lo_ok, bool hi_ok, const FDiv *fnp = nullptr) {
+                                                 bool lo_ok, bool hi_ok, const FDiv *fnp = nullptr,
+                                                 bool skip_oe = false) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   const int ej = (1 << t) + 1;
   const int npoles = Ok * R * W;
@@ -692,17 +696,25 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
   const int K = t / kTB;
   const int tr = t - kTB * K;
   const ItemWalk walk(npoles, (int)threadIdx.x, NT, fnp);
+  auto skip = [&](int p) -> bool {
+    if (!skip_oe) return false;
+    const int oo = (int)fdiv((uint32_t)(p >> LOGW), fR);
+    return oo == 0 || oo == Ok - 1;
+  };
   auto sub_phase = [&](int k) {
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (t - kTB * k - kTB);
-    for (int b = walk.b0, p = walk.p0; b < nblk; walk.next(b, p))
+    for (int b = walk.b0, p = walk.p0; b < nblk; walk.next(b, p)) {
+      if (skip(p)) continue;
       block_item_ends<INV>(pole_base(p) + (b << kTB) * m * STR, m * STR, lo_ok || b > 0, hi_ok || b < nblk - 1);
+    }
     __syncthreads();
   };
   auto top_phase = [&]() {
     if (tr == 0) return;                         // the top lattice is just the two ends
     const int m = 1 << (kTB * K);
     for (int p = threadIdx.x; p < npoles; p += NT) {
+      if (skip(p)) continue;
       if (tr == 1) block_fine<1, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else if (tr == 2 || kTB <= 3) block_fine<2, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else block_fine<(kTB > 3 ? 3 : 2), INV>(pole_base(p), m * STR, lo_ok, hi_ok);
@@ -1172,11 +1184,12 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     const bool full = (f.units == T.R);               // precomputed per-axis constants apply
     const FDiv fnp = T.fNP[j];
     if (blocked && j == T.bj) {
+      // dehierarchization of a two-blocked tile: the second axis' end rows are final
       fused_axis_block<INV, W>(sm, RS, T.bt, R, fR, full ? T.gOk[j] : rows_total / (T.ej * R), f.lo_ok, f.hi_ok,
-                               full ? &fnp : nullptr);
+                               full ? &fnp : nullptr, INV && T.bt2 >= 0);
       continue;
     }
-    if (T.bt2 >= 0 && j == T.bj + 1) {              // second blocked axis (hierarchization only)
+    if (T.bt2 >= 0 && j == T.bj + 1) {              // second blocked axis
       fused_axis_block<INV, W>(sm, RS, T.bt2, R, fR, full ? T.gOk[j] : rows_total / (((1 << T.bt2) + 1) * R),
                                f.lo2_ok, f.hi2_ok, full ? &fnp : nullptr);
       continue;

@@ -220,6 +220,22 @@ def test_two_blocked_bitwise(sgh, levels, monkeypatch):
     assert_bitwise(gpu_transform(sgh, u, levels), want)
 
 
+@pytest.mark.parametrize("levels", TWO_BLOCKED_SHAPES, ids=str)
+def test_two_blocked_dehier_bitwise(sgh, levels, monkeypatch):
+    """Dehierarchization with the two-blocked plan (a-lattice of every row,
+    fine-a of the coarse-b rows, b-lattice, the tiles with their b-end rows
+    untouched, fine-b of the coarse-a columns) forced on 2-D grids: bitwise vs
+    the oracle, also for the round trip (the oracle's own round trip, which
+    is not the identity bit for bit)."""
+    monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
+    N = si.num_points(levels)
+    a = si.fill_uniform(N, grid_id=N % 983)
+    want = oracle.dehierarchize(a.copy(), levels)
+    assert_bitwise(gpu_transform(sgh, a, levels, inverse=True), want)
+    h = oracle.hierarchize(a.copy(), levels)
+    assert_bitwise(gpu_transform(sgh, h, levels, inverse=True), oracle.dehierarchize(h.copy(), levels))
+
+
 def test_two_blocked_c4_golden(sgh, monkeypatch):
     monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
     c = SD["configs"]["C4"]
