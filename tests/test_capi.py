@@ -123,8 +123,8 @@ def _plan_passes(levels, **kw):
 def test_plan_blocked_groups_cover_each_point_once(levels, inverse):
     """A fused pass (whole poles, or a BLOCKED group: block tiles + coarse-lattice
     views) writes every point of the grid exactly once; a dehierarchization plan
-    never transforms a group axis after its blocked axis (the block ends must be
-    final values when a tile reads them)."""
+    with group axes after the blocked one runs its lattice phases in two halves
+    split by axes (before / after the tiles), each covering the lattice once."""
     N = si.num_points(levels)
     for ph in _plan_passes(levels, inverse=inverse):
         if ph[0][0] != "FUSED":
@@ -136,12 +136,27 @@ def test_plan_blocked_groups_cover_each_point_once(levels, inverse):
             main = max(p for _, _, p in ph)
             assert main < N <= sum(p for _, _, p in ph)
             continue
-        assert sum(p for _, _, p in ph) == N
-        a = ph[0][1]
+        skips = [int(a.get("skip", "0")) for _, a, _ in ph]
+        if not any(skips):
+            assert sum(p for _, _, p in ph) == N
+            continue
+        # dehierarchization with axes after the blocked one: the lattice phases
+        # run twice, split by axes (split_inverse_lattice): T_k^B .. T_1^B, T_0,
+        # T_1^A .. T_k^A; each half with the tiles covers every point once
+        assert inverse
+        main = max(range(len(ph)), key=lambda i: ph[i][2])
+        assert skips[main] == 0
+        before, after = ph[:main], ph[main + 1:]
+        assert len(before) == len(after)
+        assert [p for _, _, p in before] == [p for _, _, p in after][::-1]
+        assert ph[main][2] + sum(p for _, _, p in after) == N
+        a = ph[main][1]
         gl = [int(x) for x in a["levels"].strip("()").split(",")]
-        j, bt = int(a["special"]), int(a["bt"])
-        if j >= 0 and bt < gl[j] and inverse:
-            assert all(l == 1 for l in gl[j + 1:])
+        jb = int(a["special"])
+        low = sum(1 << k for k in range(jb + 1))
+        high = sum(1 << k for k in range(jb + 1, len(gl)))
+        assert all(sk == low for sk in skips[:main])        # B halves: axes <= jb skipped
+        assert all(sk == high for sk in skips[main + 1:])   # A halves: axes > jb skipped
 
 
 def test_plan_c2_c3_use_blocked_fusion():
