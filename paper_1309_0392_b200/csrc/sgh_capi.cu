@@ -414,7 +414,12 @@ bool plan_view_fine(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, 
   if (PS == S && S < kFlatMaxS && (int64_t(1) << tb) * S <= kFlatT) {
     t.kind = KIND_FLAT_BLOCKS;
     t.fS = make_fdiv((uint32_t)S);
-    t.tiles = O << (l - tb);
+    // consecutive blocks per tile while they fit the FLAT budget (small tb:
+    // the two-blocked cross phases, C4's 256-point blocks of single rows)
+    int nbl = 0;
+    while (nbl < l - tb && (int64_t(2) << (tb + nbl)) * S <= kFlatT) ++nbl;
+    t.R = 1 << nbl;
+    t.tiles = O << (l - tb - nbl);
     phases.push_back(t);
     return true;
   }

@@ -827,13 +827,17 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
     const int t = T.t;
     const int B = 1 << t;
     const int nb_log = T.l - t;                            // global blocks per pole
-    const int64_t o = q >> T.rlog;
-    const int b = (int)(T.blk0 + (q & ((int64_t(1) << T.rlog) - 1)));
+    // a tile holds NB = T.R consecutive blocks (power of two; 0 / 1: one) of one
+    // pole: rows 0 .. NB 2^t, block boundaries (rb % 2^t == 0) read-only
+    const int nbl = (T.R > 1) ? __ffs(T.R) - 1 : 0;
+    const int NB = 1 << nbl;
+    const int64_t o = q >> (T.rlog - nbl);
+    const int b = (int)(T.blk0 + ((q & ((int64_t(1) << (T.rlog - nbl)) - 1)) << nbl));   // first block
     const int S = (int)T.S;
     const int n = (1 << T.l) - 1;
     const int i0 = b * B;                                  // pole index of local row 0
     const int rb_lo = (b == 0) ? 1 : 0;                    // row 0 of block 0 is the boundary
-    const int rb_hi = (b == (1 << nb_log) - 1) ? B - 1 : B;  // row 2^l is the boundary
+    const int rb_hi = (b + NB == (1 << nb_log)) ? NB * B - 1 : NB * B;  // row 2^l is the boundary
     const FDiv fS = T.fS;
     // global element of local e = rb*S + r is  gr[e]
     double *__restrict__ gr = T.grid + T.base + o * T.OS + (int64_t)(i0 - 1) * S;
@@ -847,9 +851,11 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
     }
     cp_async_wait_all();
     __syncthreads();
+    // level s of every block of the tile: the rows s (2 jj + 1), jj < NB 2^t / (2 s)
+    // (odd multiples of s < 2^t are never block boundaries)
     if (padded) {
       for (int s = B >> 1; s >= 1; s >>= 1) {              // block-local levels, coarse -> fine
-        const int cnt = (B / (2 * s)) * S;
+        const int cnt = (NB * B / (2 * s)) * S;
         const int sS = s * S;
         for (int k = threadIdx.x; k < cnt; k += kThreads) {
           const int jj = (int)fdiv((uint32_t)k, fS);
@@ -864,12 +870,14 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
         }
         __syncthreads();
       }
-      const int e1 = B * S;
-      for (int e = S + threadIdx.x; e < e1; e += kThreads) gr[e] = smem[e + (e >> 5)];
+      const int e1 = NB * B * S;
+      for (int e = S + threadIdx.x; e < e1; e += kThreads)
+        if (NB == 1 || (fdiv((uint32_t)e, fS) & (B - 1))) gr[e] = smem[e + (e >> 5)];
     } else if (!INV) {
-      const int e1 = B * S;
+      const int e1 = NB * B * S;
       for (int e = S + threadIdx.x; e < e1; e += kThreads) {
         const int rb = (int)fdiv((uint32_t)e, fS);
+        if ((rb & (B - 1)) == 0) continue;                 // a block boundary (NB > 1)
         const int i = i0 + rb;
         const int s = rb & -rb;                            // tz(i) = tz(rb) < t
         const int sS = s * S;
@@ -879,7 +887,7 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
       }
     } else {
       for (int s = B >> 1; s >= 1; s >>= 1) {              // block-local levels, coarse -> fine
-        const int cnt = (B / (2 * s)) * S;
+        const int cnt = (NB * B / (2 * s)) * S;
         const int sS = s * S;
         for (int k = threadIdx.x; k < cnt; k += kThreads) {
           const int jj = (int)fdiv((uint32_t)k, fS);
@@ -894,8 +902,9 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
         }
         __syncthreads();
       }
-      const int e1 = B * S;
-      for (int e = S + threadIdx.x; e < e1; e += kThreads) gr[e] = sm[e];
+      const int e1 = NB * B * S;
+      for (int e = S + threadIdx.x; e < e1; e += kThreads)
+        if (NB == 1 || (fdiv((uint32_t)e, fS) & (B - 1))) gr[e] = sm[e];
     }
     __syncthreads();
   });
@@ -1485,7 +1494,7 @@ size_t task_smem(const Task &t) {
       return (e + e / 32 + 2) * 8;
     }
     case KIND_FLAT_BLOCKS: {
-      const size_t e = size_t((int64_t(1) << t.t) + 1) * size_t(t.S);
+      const size_t e = size_t((int64_t(std::max(1, t.R)) << t.t) + 1) * size_t(t.S);
       return (e + e / 32 + 2) * 8;
     }
     case KIND_STRIDED: return size_t((int64_t(1) << t.t) + 1) * size_t(t.W + 2) * 8;

@@ -306,6 +306,7 @@ static bool plan_view_range(double *grid, int64_t O, int64_t OS, int64_t PS, int
     Task &k = one.back();
     k.rlog = T - t;                                   // the 2^{T-t} blocks of super-block r
     k.blk0 = r << (T - t);
+    if (k.kind == KIND_FLAT_BLOCKS) k.R = 1;          // one block per tile here
     k.tiles = (O << k.rlog) * (k.kind == KIND_STRIDED ? k.ncb : 1);
     phases.push_back(k);
     base += ((int64_t(1) << t) - 1) * PS;             // the lattice {i : 2^t | i}
