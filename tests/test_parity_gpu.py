@@ -449,11 +449,12 @@ def test_gather_closed_form_c5_subset(sgh):
     assert off == sp.numel()
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SGH_FUZZ_SEEDS", "6"))))
 def test_random_shapes_fuzz(sgh, seed, monkeypatch):
     """Planner fuzz: random level vectors (d = 1..6, up to ~2 M points) under every
     plan family -- automatic, whole-pole fusion only, per axis, forced two-blocked
-    -- hierarchize and dehierarchize, bitwise vs the oracle."""
+    -- hierarchize and dehierarchize, bitwise vs the oracle.  SGH_FUZZ_SEEDS
+    widens the seed range for ad-hoc runs."""
     rng = np.random.default_rng(1000 + seed)
     done = 0
     while done < 12:
@@ -471,4 +472,5 @@ def test_random_shapes_fuzz(sgh, seed, monkeypatch):
             assert_bitwise(gpu_transform(sgh, u, lv, inverse=True, fuse=fuse, guard=64), want_d)
         monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
         assert_bitwise(gpu_transform(sgh, u, lv, guard=64), want_h)
+        assert_bitwise(gpu_transform(sgh, u, lv, inverse=True, guard=64), want_d)
         monkeypatch.delenv("SGH_TWO_BLOCKED")
