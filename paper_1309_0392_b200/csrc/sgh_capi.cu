@@ -672,12 +672,12 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
         bool later = false;                          // transformed group axes after the blocked one
         for (int k = s + 1; k < j; ++k) later |= levels[k] > 1;
         // dehierarchization with later axes runs the lattice phases twice
-        // (split_inverse_lattice); not when they are lattices of the unit-stride
-        // axis, columns of isolated elements (C3: 77.9 vs 80.8 Gpoints/s)
-        if (inv && later && Sa == 1 && s == i) continue;
+        // (split_inverse_lattice); not when they are single-point lattices of the
+        // unit-stride axis, columns of isolated elements (C3: 77.9 vs 80.8 Gpoints/s)
         for (int W = (Sa == 1 ? 1 : fused_wmax()); W >= (Sa == 1 ? 1 : 8); W >>= 1) {
           std::vector<Task> bp;
           if (!plan_blocked_group(grid, levels, d, i, j, s, W, bp)) continue;
+          if (inv && later && Sa == 1 && s == i && bp.size() >= 2 && bp[1].gl[bp[1].bj] < 2) continue;
           if (inv && later) split_inverse_lattice(bp, s - i);
           const double cj = cost[i] + pass_cost(bp);
           if (cj < cost[j] - 1e-12) {
