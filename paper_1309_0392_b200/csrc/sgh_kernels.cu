@@ -1344,7 +1344,9 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
       }
     }
     fused_compute_store<INV, W>(s_task[STAGES == 2 ? (k & 1) : slot], fc, cur + fc.par);
+#ifndef SGH_DEBUG_NOSTOREWAIT   // timing experiment only (races: results wrong)
     if (W == 1 && SGH_BULK_STORE && threadIdx.x == 0) bulk_wait_read();   // bulk stores have read the stage
+#endif
     if (STAGES == 1 && newtask) cp_async_wait<0>();
     __syncthreads();                              // the stage is free for the next load
     if (!more) break;
