@@ -213,14 +213,20 @@ def main():
 def reference_arm(args, rank, world):
     if rank != 0:
         return 0
+    import sgh_inputs as si
     members, ids, desc = workload(args.workload)
+    total = sum(si.num_points(l) for l in members)
     rate, sample, cores, times, npts = oracle_rate(members, ids, target_cpu_s=4.0, max_points=200_000_000,
                                                    steps=args.steps, warmup=args.warmup)
     ms = 1e3 * sum(times) / len(times)
     out = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": desc, "sample_points_per_step": npts},
+           # the sgh arm's config keys (the same workload), plus the bounded sample timed per step
+           "config": {"workload": desc, "points": total, "bytes": 8 * total,
+                      "l2": "host memory (oracle on host cores)",
+                      "parallelism": f"oracle, one grid per host thread ({cores} threads), rank 0 only",
+                      "seed": si.SEED, "sample_points_per_step": npts},
            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "note": "the paper's comparison codes (SGpp, Buse et al.) and its own CPU code are not available; "
