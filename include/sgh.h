@@ -279,7 +279,11 @@ size_t sgh_combi_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_g
  *  grids:  host array of num_grids DEVICE pointers (hierarchical surpluses);
  *  levels: host int32[num_grids][d];  coeffs: host double[num_grids] (the
  *          combination coefficients (-1)^q C(d-1, q), or any weights);
- *  sparse: device array of sgh_sparse_num_points(d, n) doubles (written). */
+ *  sparse: device array of sgh_sparse_num_points(d, n) doubles (written).
+ *  Errors: SGH_ERR_INVALID_ARGUMENT (NULL arguments, invalid levels, a grid
+ *  whose level sum exceeds n or with N >= 2^31 points, unsupported (d, n) or
+ *  n - d > 30), SGH_ERR_WORKSPACE (workspace missing, misaligned or smaller
+ *  than sgh_combi_workspace_bytes), SGH_ERR_CUDA (launch failure). */
 sgh_status sgh_gather(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
                       int64_t num_grids, int32_t n, double *sparse, void *workspace, size_t ws_bytes, void *stream);
 
@@ -298,7 +302,10 @@ sgh_status sgh_gather(const double *const *grids, const int32_t *levels, const d
  *          gather: rank r owns grid block r and continues the
  *          partial sums received from rank r-1, pipelined over subspace
  *          ranges (paper_1309_0392_b200.gather_chain).
- *  The workspace of sgh_combi_workspace_bytes (full range) is sufficient. */
+ *  The workspace of sgh_combi_workspace_bytes (full range) is sufficient.
+ *  Errors: SGH_ERR_INVALID_ARGUMENT for a range out of bounds, unknown flags
+ *  or n - d > 30 (a subspace larger than any grid can hold); otherwise as
+ *  sgh_gather.  An empty range does nothing. */
 #define SGH_FLAG_ACCUMULATE 16u
 sgh_status sgh_gather_ex(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
                          int64_t num_grids, int32_t n, double *sparse, int64_t sub_begin, int64_t sub_end,

@@ -407,6 +407,9 @@ static sgh_status build_combi_plan(double *const *grids, const int32_t *levels, 
     P.prefix.push_back(acc);
     return SGH_OK;
   }
+  // a subspace has 2^{s-d} points, indexed in int32 by the gather kernel; no
+  // grid can hold a larger one anyway (N < 2^31 per grid)
+  if (n - d > 30) return invalid("gather: subspaces of more than 2^30 points (n - d > 30)");
   std::vector<int> lam(d);
   int64_t si = 0;                                  // subspace index in SG order
   for (int s = d; s <= n && si < sub_end; ++s) {   // subspaces in SG order

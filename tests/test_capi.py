@@ -223,3 +223,12 @@ def test_sparse_subspace_offsets(d, n):
     assert sgh.sparse_subspace_offset(d, n, nsub) == sgh.sparse_num_points(d, n)
     with pytest.raises(sgh.SGHError):
         sgh.sparse_subspace_offset(d, n, nsub + 1)
+
+
+def test_combi_workspace_rejects_oversized_subspaces():
+    """Gather plans are refused (workspace size 0) when a subspace would hold
+    more than 2^30 points (n - d > 30) -- more than any grid can hold."""
+    import ctypes
+    lv = (ctypes.c_int32 * 1)(20)
+    assert sgh.lib.sgh_combi_workspace_bytes(lv, 1, 1, 30, 0) > 0
+    assert sgh.lib.sgh_combi_workspace_bytes(lv, 1, 1, 32, 0) == 0
