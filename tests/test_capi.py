@@ -232,3 +232,20 @@ def test_combi_workspace_rejects_oversized_subspaces():
     lv = (ctypes.c_int32 * 1)(20)
     assert sgh.lib.sgh_combi_workspace_bytes(lv, 1, 1, 30, 0) > 0
     assert sgh.lib.sgh_combi_workspace_bytes(lv, 1, 1, 32, 0) == 0
+
+
+def test_plan_two_blocked_inverse_phase_order():
+    """Dehierarchization with two-blocked tiles (sgh_capi.cu plan_two_blocked):
+    the plan lists, in the order the runner reverses, (5) the coarse-a columns'
+    fine-b part (axis a skipped), (4) the tiles, (3) the b-lattice view, (2) the
+    fine-a view of the coarse-b rows, (1) the a-lattice: a view for the
+    coarse-b rows and the coarse-a-column tiles with axis b skipped."""
+    q = _plan_passes((14, 13), inverse=True)
+    assert len(q) == 1
+    ph = q[0]
+    kinds = [(k, a.get("skip"), a.get("bt2")) for k, a, _ in ph]
+    assert kinds[0][0] == "FUSED" and kinds[0][1] == "1"                  # (5)
+    assert kinds[1][0] == "FUSED" and kinds[1][1] == "0" and kinds[1][2] == "5"   # (4): the 257 x 33 tiles
+    assert kinds[-1][0] == "FUSED" and kinds[-1][1] == "2"                # (1), fine-b rows
+    assert all(k != "FUSED" for k, _, _ in kinds[2:-1])                   # (3), (2), (1) views
+    assert ph[0][2] == ph[-1][2]                                          # same coarse-a columns
