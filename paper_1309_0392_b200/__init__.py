@@ -141,6 +141,15 @@ def _stream(stream) -> ctypes.c_void_p:
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+def _keep_on(stream, *tensors):
+    """Tensors allocated on the current stream but used by kernels launched on
+    ``stream``: tell the caching allocator, so their blocks are not handed to
+    another tensor while those kernels may still run."""
+    if stream is not None and stream != torch.cuda.current_stream():
+        for t in tensors:
+            t.record_stream(stream)
+
+
 def _grid_ptr(t: torch.Tensor, levels) -> ctypes.c_void_p:
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError("grid must be a CUDA tensor (there is no CPU path)")
@@ -531,6 +540,7 @@ def gather(grids, levels_list, coeffs, n: int, sparse: torch.Tensor = None, stre
     with torch.cuda.device(dev):
         _check(lib.sgh_gather(ptrs, flat, c, d, len(grids), int(n), ctypes.c_void_p(sparse.data_ptr()),
                               ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
+    _keep_on(stream, ws, sparse)
     return sparse
 
 
@@ -561,6 +571,7 @@ def gather_ex(grids, levels_list, coeffs, n: int, sparse: torch.Tensor, sub_begi
         _check(lib.sgh_gather_ex(ptrs, flat, c, d, len(grids), int(n), ctypes.c_void_p(sparse.data_ptr()),
                                  int(sub_begin), int(sub_end), FLAG_ACCUMULATE if accumulate else 0,
                                  ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
+    _keep_on(stream, ws)
     return sparse
 
 
@@ -625,4 +636,5 @@ def scatter(sparse: torch.Tensor, grids, levels_list, n: int, stream=None):
     with torch.cuda.device(dev):
         _check(lib.sgh_scatter(ptrs, flat, d, len(grids), int(n), ctypes.c_void_p(sparse.data_ptr()),
                                ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
+    _keep_on(stream, ws)
     return grids

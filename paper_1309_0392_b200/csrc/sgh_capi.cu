@@ -853,6 +853,7 @@ struct Segment {
   size_t smem;        // max dynamic shared memory over the segment's tasks
   double points;      // points the segment transforms (profiling)
   int variant;        // task_variant of its tasks (3: mixed blocked / lattice)
+  bool pipe;          // runs on k_fpipe (pipe_task)
 };
 
 struct BatchedPlan {
@@ -892,7 +893,7 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
         if (j < per[g].size()) {
           const Task &t = per[g][j];
           groups[{t.kind, t.kind == KIND_REG ? t.l : 0, (t.kind == KIND_STRIDED || t.kind == KIND_FUSED) ? t.W : 0,
-                  split ? task_variant(t) : 0}]
+                  (split ? task_variant(t) : 0) * 2 + (pipe_task(t) ? 1 : 0)}]
               .push_back(&t);
         }
       for (auto &kv : groups) {
@@ -903,6 +904,7 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
         sg.task_off = P.tasks.size();
         sg.prefix_off = P.prefix.size();
         sg.ntasks = (int32_t)kv.second.size();
+        sg.pipe = (std::get<3>(kv.first) & 1) != 0;
         int64_t acc = 0;
         sg.smem = 0;
         sg.points = 0;
@@ -1011,7 +1013,7 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
   const int64_t *d_prefix = reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + prefix_base);
   for (const Segment &sg : P.segs) {
     cudaError_t e = launch_table(sg.kind, sg.l, sg.w, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off, sg.ntasks,
-                                 sg.tiles, sg.smem, sg.points, s, sg.variant);
+                                 sg.tiles, sg.smem, sg.points, s, sg.variant, sg.pipe);
     if (e != cudaSuccess) return cuda_fail(e, "grouped kernel launch");
     count_launch();
   }
@@ -1035,28 +1037,38 @@ int64_t sgh_num_points(const int32_t *levels, int32_t d) {
 }
 
 sgh_status sgh_hierarchize(double *grid, const int32_t *levels, int32_t d, void *stream) {
+  return guarded([&]() -> sgh_status {
   return transform_single(grid, levels, d, nullptr, 0u, SGH_FLAG_NONE, stream);
+});
 }
 
 sgh_status sgh_dehierarchize(double *grid, const int32_t *levels, int32_t d, void *stream) {
+  return guarded([&]() -> sgh_status {
   return transform_single(grid, levels, d, nullptr, 0u, SGH_FLAG_DEHIERARCHIZE, stream);
+});
 }
 
 sgh_status sgh_transform_ex(double *grid, const int32_t *levels, int32_t d, const int32_t *axis_order,
                             uint32_t axis_mask, uint32_t flags, void *stream) {
+  return guarded([&]() -> sgh_status {
   return transform_single(grid, levels, d, axis_order, axis_mask, flags, stream);
+});
 }
 
 size_t sgh_batched_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
+  return guarded_value<size_t>(0, [&]() -> size_t {
   if (validate_batch(nullptr, levels, d, num_grids, false) != SGH_OK || num_grids == 0) return 0;
   BatchedPlan P;
   build_batched_plan(nullptr, levels, d, num_grids, flags, P);
   return P.table_bytes();
+});
 }
 
 sgh_status sgh_hierarchize_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
                                    uint32_t flags, void *workspace, size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   return run_batched(grids, levels, d, num_grids, flags, workspace, ws_bytes, static_cast<cudaStream_t>(stream));
+});
 }
 
 sgh_status sgh_fill_uniform(double *grid, int64_t n, uint64_t seed, uint64_t grid_id, int64_t index_offset,
@@ -1095,6 +1107,7 @@ static sgh_status make_items(double *const *grids, const int64_t *sizes, const u
 sgh_status sgh_fill_uniform_batched(double *const *grids, const int64_t *sizes, const uint64_t *grid_ids,
                                     int64_t num_grids, uint64_t seed, void *workspace, size_t ws_bytes,
                                     void *stream) {
+  return guarded([&]() -> sgh_status {
   if (num_grids < 0) return invalid("num_grids < 0");
   if (num_grids == 0) return SGH_OK;
   if (!grids || !sizes) return invalid("grids/sizes is NULL");
@@ -1117,6 +1130,7 @@ sgh_status sgh_fill_uniform_batched(double *const *grids, const int64_t *sizes, 
   if (e != cudaSuccess) return cuda_fail(e, "batched fill launch");
   count_launch();
   return SGH_OK;
+});
 }
 
 sgh_status sgh_digest(const double *grid, int64_t n, int64_t index_offset, uint64_t *out_host, void *stream) {
@@ -1156,6 +1170,7 @@ sgh_status sgh_digest(const double *grid, int64_t n, int64_t index_offset, uint6
 
 sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_t num_grids, uint64_t *out_host,
                               void *workspace, size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   if (num_grids < 0) return invalid("num_grids < 0");
   if (num_grids == 0) return SGH_OK;
   if (!grids || !sizes || !out_host) return invalid("NULL argument");
@@ -1187,9 +1202,11 @@ sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize(digests)");
   return SGH_OK;
+});
 }
 
 int64_t sgh_plan_describe(const int32_t *levels, int32_t d, uint32_t flags, char *buf, size_t cap) {
+  return guarded_value<int64_t>(-1, [&]() -> int64_t {
   if (validate_levels(levels, d, nullptr) != SGH_OK || (flags & ~kKnownFlags)) return -1;
   std::vector<std::vector<Task>> passes;
   plan_grid(nullptr, levels, d, flags, passes);
@@ -1221,6 +1238,7 @@ int64_t sgh_plan_describe(const int32_t *levels, int32_t d, uint32_t flags, char
     buf[n] = 0;
   }
   return (int64_t)out.size();
+});
 }
 
 uint64_t sgh_launch_count(void) { return g_launches.load(); }

@@ -410,6 +410,14 @@ static sgh_status build_combi_plan(double *const *grids, const int32_t *levels, 
   // a subspace has 2^{s-d} points, indexed in int32 by the gather kernel; no
   // grid can hold a larger one anyway (N < 2^31 per grid)
   if (n - d > 30) return invalid("gather: subspaces of more than 2^30 points (n - d > 30)");
+  {                                                // refuse before listing: C(n, d) can be ~1e14
+    const int64_t total = binom_host(n, d);
+    const int64_t cnt = std::min(sub_end, total) - std::max<int64_t>(sub_begin, 0);
+    if (cnt >= (int64_t(1) << 31)) {
+      set_error("gather: too many subspaces in the requested range (>= 2^31)");
+      return SGH_ERR_CAPACITY;
+    }
+  }
   std::vector<int> lam(d);
   int64_t si = 0;                                  // subspace index in SG order
   for (int s = d; s <= n && si < sub_end; ++s) {   // subspaces in SG order
@@ -440,7 +448,6 @@ static sgh_status build_combi_plan(double *const *grids, const int32_t *levels, 
     } while (next_composition(lam.data(), d));
   }
   P.prefix.push_back(acc);
-  if (P.subs.size() >= (size_t(1) << 31)) return invalid("too many subspaces");
   return SGH_OK;
 }
 
@@ -554,34 +561,42 @@ int64_t sgh_sparse_subspace_offset(int32_t d, int32_t n, int64_t index) {
 }
 
 size_t sgh_combi_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, int32_t n, uint32_t flags) {
+  return guarded_value<size_t>(0, [&]() -> size_t {
   if (!levels || num_grids < 0) return 0;
   CombiPlan P;
   const bool gather = (flags & SGH_FLAG_SCATTER) == 0;
   if (build_combi_plan(nullptr, levels, nullptr, d, num_grids, n, gather, P) != SGH_OK) return 0;
   return P.bytes();
+});
 }
 
 sgh_status sgh_gather(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
                       int64_t num_grids, int32_t n, double *sparse, void *workspace, size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   return run_combi(const_cast<double *const *>(grids), levels, coeffs, d, num_grids, n, sparse, workspace, ws_bytes,
                    static_cast<cudaStream_t>(stream), true);
+});
 }
 
 sgh_status sgh_gather_ex(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
                          int64_t num_grids, int32_t n, double *sparse, int64_t sub_begin, int64_t sub_end,
                          uint32_t flags, void *workspace, size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   const int64_t nsub = sgh_sparse_num_subspaces(d, n);
   if (nsub < 0) return invalid("unsupported (d, n) for the sparse grid");
   if (sub_begin < 0 || sub_end < sub_begin || sub_end > nsub) return invalid("subspace range out of bounds");
   if (sub_begin == sub_end) return SGH_OK;
   return run_combi(const_cast<double *const *>(grids), levels, coeffs, d, num_grids, n, sparse, workspace, ws_bytes,
                    static_cast<cudaStream_t>(stream), true, sub_begin, sub_end, flags);
+});
 }
 
 sgh_status sgh_scatter(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, int32_t n,
                        const double *sparse, void *workspace, size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   return run_combi(grids, levels, nullptr, d, num_grids, n, const_cast<double *>(sparse), workspace, ws_bytes,
                    static_cast<cudaStream_t>(stream), false);
+});
 }
 
 }  // extern "C"

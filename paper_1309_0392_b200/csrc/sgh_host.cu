@@ -92,16 +92,19 @@ using namespace sgh;
 extern "C" {
 
 size_t sgh_batched_host_buffer_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
+  return guarded_value<size_t>(0, [&]() -> size_t {
   if (!levels || num_grids <= 0) return 0;
   HostLayout L;
   if (host_layout(levels, d, num_grids, flags, L) != SGH_OK)
     return 0;
   return L.total;
+});
 }
 
 sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *levels, int32_t d,
                                       int64_t num_grids, uint32_t flags, void *device_buffer,
                                       size_t device_buffer_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   if (flags & ~kKnownFlags) return invalid("unknown flags");
   if (num_grids < 0) return invalid("num_grids < 0");
   if (num_grids == 0) return SGH_OK;
@@ -184,6 +187,7 @@ sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "e2e batched");
   return SGH_OK;
+});
 }
 
 }  // extern "C"

@@ -28,11 +28,20 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "sgh_common.cuh"
 #include "sgh_plan.hpp"
 
 namespace sgh {
+
+// One term of an update with the oracle's rounding (oracle.c is built with
+// -ffp-contract=off): the product 0.5 e is rounded on its own, then the sum.
+// Written with explicit _rn intrinsics so nvcc cannot contract them into a
+// DFMA -- 0.5 e is exact for normal e, but not for subnormal e with an odd
+// last bit, where a fused multiply-add would round once instead of twice.
+__device__ __forceinline__ double hsub(double x, double e) { return __dsub_rn(x, __dmul_rn(0.5, e)); }
+__device__ __forceinline__ double hadd(double x, double e) { return __dadd_rn(x, __dmul_rn(0.5, e)); }
 
 // The hierarchization update of one point from its two predecessors, each
 // skipped if it lies on the boundary: x - 0.5 L, then
@@ -43,15 +52,15 @@ namespace sgh {
 #define HIER_UPDATE(x, cl, el, cr, er)           \
   do {                                           \
     const bool hl_ = (cl), hr_ = (cr);           \
-    if (hl_ && hr_) x = x - 0.5 * ((el) + (er)); \
-    else if (hl_) x = x - 0.5 * (el);            \
-    else if (hr_) x = x - 0.5 * (er);            \
+    if (hl_ && hr_) x = hsub(x, __dadd_rn((el), (er))); \
+    else if (hl_) x = hsub(x, (el));             \
+    else if (hr_) x = hsub(x, (er));             \
   } while (0)
 #else
 #define HIER_UPDATE(x, cl, el, cr, er) \
   do {                                 \
-    if (cl) x = x - 0.5 * (el);        \
-    if (cr) x = x - 0.5 * (er);        \
+    if (cl) x = hsub(x, (el));         \
+    if (cr) x = hsub(x, (er));         \
   } while (0)
 #endif
 
@@ -301,8 +310,8 @@ __global__ void __launch_bounds__(kThreads) k_strided(const __grid_constant__ Sr
           for (int u = 0; u < CPL; ++u) {
             const int c = lane + 32 * u;
             double x = xm[c];
-            if (i - s >= 1) x = x + 0.5 * xl[c];
-            if (i + s <= n) x = x + 0.5 * xr[c];
+            if (i - s >= 1) x = hadd(x, xl[c]);
+            if (i + s <= n) x = hadd(x, xr[c]);
             xm[c] = x;
           }
         }
@@ -413,8 +422,8 @@ __device__ __forceinline__ void pole_regs(double *p, int STR) {
 #pragma unroll
       for (int i = s; i <= n; i += 2 * s) {
         double x = v[i - 1];
-        if (i - s >= 1) x = x + 0.5 * v[i - s - 1];
-        if (i + s <= n) x = x + 0.5 * v[i + s - 1];
+        if (i - s >= 1) x = hadd(x, v[i - s - 1]);
+        if (i + s <= n) x = hadd(x, v[i + s - 1]);
         v[i - 1] = x;
       }
     }
@@ -456,8 +465,8 @@ __device__ __forceinline__ void block_fine(double *p0, int STR, bool lo_ok, bool
 #pragma unroll
       for (int r = s; r < B; r += 2 * s) {
         double x = v[r];
-        if (r - s > 0 || lo_ok) x = x + 0.5 * v[r - s];
-        if (r + s < B || hi_ok) x = x + 0.5 * v[r + s];
+        if (r - s > 0 || lo_ok) x = hadd(x, v[r - s]);
+        if (r + s < B || hi_ok) x = hadd(x, v[r + s]);
         v[r] = x;
       }
     }
@@ -547,6 +556,20 @@ struct HaloSkip {
   }
 };
 
+// The threads that transform a tile together, with their barrier: the whole
+// CTA (CtaSync, k_fused) or one consumer warp group of the warp-specialised
+// pipelined kernel (GroupSync: named barrier `id` over NT threads, k_fpipe).
+struct CtaSync {
+  __device__ __forceinline__ int tid() const { return (int)threadIdx.x; }
+  __device__ __forceinline__ void bar() const { __syncthreads(); }
+};
+template <int NT>
+struct GroupSync {
+  int t, id;
+  __device__ __forceinline__ int tid() const { return t; }
+  __device__ __forceinline__ void bar() const { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(NT) : "memory"); }
+};
+
 // One axis of a staged tile, all npoles poles of level l (pole p = (oo, rk, c)
 // at sm + (oo*n*R + rk)*RS + c, point stride R*RS), in parallel work items:
 // l <= 4: one register pole per thread; l >= 5: (pole, 2^kTB-block) items on
@@ -555,9 +578,9 @@ struct HaloSkip {
 // levels; hierarchization runs fine -> coarse, dehierarchization the reverse.
 // UNIT: the axis is the tile's first (R == 1): the point stride RS is a
 // compile-time constant (immediate SMEM offsets) and a pole index needs no division.
-template <bool INV, int W, bool UNIT = false, int NT = FT<W>::v>
+template <bool INV, int W, bool UNIT = false, int NT = FT<W>::v, class SY = CtaSync>
 __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv fR, int Ok,
-                                           const HaloSkip hs, const FDiv *fnp = nullptr) {
+                                           const HaloSkip hs, const FDiv *fnp = nullptr, const SY sy = SY()) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   if (UNIT) {
     RS = (W == 1) ? 1 : W + 1;
@@ -575,11 +598,11 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   };
   auto pole_base = [&](int p) -> double * { return sm + pole_row(p) * RS + (p & (W - 1)); };
   if (l <= 4) {
-    for (int p = threadIdx.x; p < npoles; p += NT) {
+    for (int p = sy.tid(); p < npoles; p += NT) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       pole_regs_rt<INV>(pole_base(p), l, STR);
     }
-    __syncthreads();
+    sy.bar();
     return;
   }
   // lattice levels visited: l, l-kTB, l-2kTB, ... (> 4), then the register lattice
@@ -588,7 +611,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
     levels[nlev++] = lf;
     lf -= kTB;
   }
-  const ItemWalk walk(npoles, (int)threadIdx.x, NT, fnp);
+  const ItemWalk walk(npoles, (int)sy.tid(), NT, fnp);
   auto block_phase = [&](int k) {                // k-th lattice level: stride 2^{kTB k}
     const int m = 1 << (kTB * k);
     const int nblk = 1 << (levels[k] - kTB);
@@ -597,17 +620,17 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
       if (hs.on && hs.skip(pole_row(p))) continue;
       block_item<INV>(pole_base(p) - STR, m * STR, b, nblk);
     }
-    __syncthreads();
+    sy.bar();
   };
   auto lattice_phase = [&]() {
     if (lf <= 1) return;                         // a single point: no update
     const int m = 1 << (kTB * nlev);
-    for (int p = threadIdx.x; p < npoles; p += NT) {
+    for (int p = sy.tid(); p < npoles; p += NT) {
       if (hs.on && hs.skip(pole_row(p))) continue;
       double *p0 = pole_base(p) - STR;           // virtual point 0
       pole_regs_rt<INV>(p0 + m * STR, lf, m * STR);
     }
-    __syncthreads();
+    sy.bar();
   };
   if (!INV) {
     for (int k = 0; k < nlev; ++k) block_phase(k);
@@ -678,10 +701,10 @@ __device__ __forceinline__ bool warp_rows_dispatch(double *sm, int nrows, int l)
 // skip_oe (dehierarchization of a two-blocked tile, axis a): poles in the
 // first / last outer row (oo = 0, Ok - 1: the second blocked axis' end rows,
 // final values) are left untouched.
-template <bool INV, int W, int NT = FT<W>::v>
+template <bool INV, int W, int NT = FT<W>::v, class SY = CtaSync>
 __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int R, const FDiv fR, int Ok,
                                                  bool lo_ok, bool hi_ok, const FDiv *fnp = nullptr,
-                                                 bool skip_oe = false) {
+                                                 bool skip_oe = false, const SY sy = SY()) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   const int ej = (1 << t) + 1;
   const int npoles = Ok * R * W;
@@ -695,7 +718,7 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
   };
   const int K = t / kTB;
   const int tr = t - kTB * K;
-  const ItemWalk walk(npoles, (int)threadIdx.x, NT, fnp);
+  const ItemWalk walk(npoles, (int)sy.tid(), NT, fnp);
   auto skip = [&](int p) -> bool {
     if (!skip_oe) return false;
     const int oo = (int)fdiv((uint32_t)(p >> LOGW), fR);
@@ -708,18 +731,18 @@ __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int 
       if (skip(p)) continue;
       block_item_ends<INV>(pole_base(p) + (b << kTB) * m * STR, m * STR, lo_ok || b > 0, hi_ok || b < nblk - 1);
     }
-    __syncthreads();
+    sy.bar();
   };
   auto top_phase = [&]() {
     if (tr == 0) return;                         // the top lattice is just the two ends
     const int m = 1 << (kTB * K);
-    for (int p = threadIdx.x; p < npoles; p += NT) {
+    for (int p = sy.tid(); p < npoles; p += NT) {
       if (skip(p)) continue;
       if (tr == 1) block_fine<1, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else if (tr == 2 || kTB <= 3) block_fine<2, INV>(pole_base(p), m * STR, lo_ok, hi_ok);
       else block_fine<(kTB > 3 ? 3 : 2), INV>(pole_base(p), m * STR, lo_ok, hi_ok);
     }
-    __syncthreads();
+    sy.bar();
   };
   if (!INV) {
     for (int k = 0; k < K; ++k) sub_phase(k);
@@ -771,8 +794,8 @@ __global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__
           const int i = s * (2 * j + 1);
           const int e = slab * nS + (i - 1) * S + r;
           double x = smem[e + (e >> 5)];
-          if (i - s >= 1) x = x + 0.5 * smem[(e - sS) + ((e - sS) >> 5)];
-          if (i + s <= n) x = x + 0.5 * smem[(e + sS) + ((e + sS) >> 5)];
+          if (i - s >= 1) x = hadd(x, smem[(e - sS) + ((e - sS) >> 5)]);
+          if (i + s <= n) x = hadd(x, smem[(e + sS) + ((e + sS) >> 5)]);
           smem[e + (e >> 5)] = x;
         }
         __syncthreads();
@@ -803,8 +826,8 @@ __global__ void __launch_bounds__(kThreads) k_flat_slabs(const __grid_constant__
           const int i = s * (2 * j + 1);
           const int e = slab * nS + (i - 1) * S + r;
           double x = sm[e];
-          if (i - s >= 1) x = x + 0.5 * sm[e - sS];
-          if (i + s <= n) x = x + 0.5 * sm[e + sS];
+          if (i - s >= 1) x = hadd(x, sm[e - sS]);
+          if (i + s <= n) x = hadd(x, sm[e + sS]);
           sm[e] = x;
         }
         __syncthreads();
@@ -864,8 +887,8 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
           const int e = rb * S + r;
           const int i = i0 + rb;
           double x = smem[e + (e >> 5)];
-          if (i - s >= 1) x = x + 0.5 * smem[(e - sS) + ((e - sS) >> 5)];
-          if (i + s <= n) x = x + 0.5 * smem[(e + sS) + ((e + sS) >> 5)];
+          if (i - s >= 1) x = hadd(x, smem[(e - sS) + ((e - sS) >> 5)]);
+          if (i + s <= n) x = hadd(x, smem[(e + sS) + ((e + sS) >> 5)]);
           smem[e + (e >> 5)] = x;
         }
         __syncthreads();
@@ -896,8 +919,8 @@ __global__ void __launch_bounds__(kThreads) k_flat_blocks(const __grid_constant_
           const int e = rb * S + r;
           const int i = i0 + rb;
           double x = sm[e];
-          if (i - s >= 1) x = x + 0.5 * sm[e - sS];
-          if (i + s <= n) x = x + 0.5 * sm[e + sS];
+          if (i - s >= 1) x = hadd(x, sm[e - sS]);
+          if (i + s <= n) x = hadd(x, sm[e + sS]);
           sm[e] = x;
         }
         __syncthreads();
@@ -1164,15 +1187,11 @@ __device__ __forceinline__ void fused_issue(const Task &T, const FusedTile &f, d
   else fused_load_rows<(W == 1 || W >= 64 ? 8 : W)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
 }
 
-// all axes of the group on a staged tile, then the store
-template <bool INV, int W>
-__device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTile &f, double *sm) {
+// all axes of the group on a staged tile (Alg. 1's axis loop, in SMEM)
+template <bool INV, int W, int NT = FT<W>::v, class SY = CtaSync>
+__device__ __forceinline__ void fused_compute(const Task &T, const FusedTile &f, double *sm, const SY sy = SY()) {
   constexpr int RS = (W == 1) ? 1 : W + 1;
-  const int P = T.P;
-  const int units = f.units, wc = f.wc;
-  const int64_t S = T.S;
-  double *gbase = f.g;
-  const int rows_total = units * P;
+  const int rows_total = f.units * T.P;
   const bool blocked = T.bj >= 0 && T.bt < T.gl[T.bj];
   HaloSkip hs;
   hs.on = false;
@@ -1194,13 +1213,14 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     const FDiv fnp = T.fNP[j];
     if (blocked && j == T.bj) {
       // dehierarchization of a two-blocked tile: the second axis' end rows are final
-      fused_axis_block<INV, W>(sm, RS, T.bt, R, fR, full ? T.gOk[j] : rows_total / (T.ej * R), f.lo_ok, f.hi_ok,
-                               full ? &fnp : nullptr, INV && T.bt2 >= 0);
+      fused_axis_block<INV, W, NT, SY>(sm, RS, T.bt, R, fR, full ? T.gOk[j] : rows_total / (T.ej * R), f.lo_ok,
+                                       f.hi_ok, full ? &fnp : nullptr, INV && T.bt2 >= 0, sy);
       continue;
     }
     if (T.bt2 >= 0 && j == T.bj + 1) {              // second blocked axis
-      fused_axis_block<INV, W>(sm, RS, T.bt2, R, fR, full ? T.gOk[j] : rows_total / (((1 << T.bt2) + 1) * R),
-                               f.lo2_ok, f.hi2_ok, full ? &fnp : nullptr);
+      fused_axis_block<INV, W, NT, SY>(sm, RS, T.bt2, R, fR,
+                                       full ? T.gOk[j] : rows_total / (((1 << T.bt2) + 1) * R), f.lo2_ok, f.hi2_ok,
+                                       full ? &fnp : nullptr, false, sy);
       continue;
     }
     const int n = (T.bj == j) ? T.ej : (1 << l) - 1;
@@ -1212,9 +1232,21 @@ __device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTi
     }
 #endif
     const int Ok = full ? T.gOk[j] : rows_total / (n * R);
-    if (R == 1) fused_axis<INV, W, true>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr);
-    else fused_axis<INV, W>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr);
+    if (R == 1) fused_axis<INV, W, true, NT, SY>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr, sy);
+    else fused_axis<INV, W, false, NT, SY>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr, sy);
   }
+}
+
+// all axes of the group on a staged tile, then the store
+template <bool INV, int W>
+__device__ __forceinline__ void fused_compute_store(const Task &T, const FusedTile &f, double *sm) {
+  constexpr int RS = (W == 1) ? 1 : W + 1;
+  const int P = T.P;
+  const int units = f.units, wc = f.wc;
+  const int64_t S = T.S;
+  double *gbase = f.g;
+  const int rows_total = units * P;
+  fused_compute<INV, W>(T, f, sm);
 #if defined(SGH_DEBUG_NOMEMORY) || defined(SGH_DEBUG_NOSTORE)
   return;                                         // timing experiments: compute only / no store
 #endif
@@ -1367,6 +1399,245 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
   if (W == 1 && SGH_BULK_STORE && threadIdx.x == 0) bulk_wait_all();
 }
 
+// ============================================= PIPELINED FUSED W == 1 (k_fpipe)
+// The same tiles as k_fused<W = 1> (whole poles of a run of axes, or a run
+// with one / two BLOCKED axes; contiguous global runs), run by a
+// warp-specialised persistent CTA, one per SM, over a ring of kPipeStages SMEM
+// stages:
+//   warp 0        producer: per tile, waits until its stage is free, copies the
+//                 task descriptor and tile geometry into SMEM, and issues the
+//                 tile's loads -- one cp.async.bulk (TMA bulk copy, SASS
+//                 UBLKCP) per contiguous run into the 16-byte aligned body,
+//                 completing on the stage's `full` mbarrier by transaction
+//                 count, plus 8-byte cp.async for the odd end elements of runs
+//                 at an 8-mod-16 phase (cp.async.mbarrier.arrive.noinc);
+//   warps 2..     consumers (kPipeGroups groups of kPipeCWarps warps, group g
+//                 takes tiles g, g + G, ..): wait for `full`, run the group's
+//                 axes in SMEM (fused_compute: the oracle's operation order,
+//                 bitwise), fence the generic-proxy writes for the async proxy
+//                 and arrive on `computed`;
+//   warp 1        storer: waits for `computed`, issues the bulk stores of the
+//                 tile's written runs (cp.async.bulk shared -> global) and its
+//                 8-byte ends, waits until the copies have READ the stage and
+//                 arrives on `empty`.
+// So the loads of tile k+1.. and the stores of tile k-1 stream while tile k is
+// transformed: the engine keeps HBM busy, the SM's issue slots go to the
+// transform.  Tasks whose SMEM phase does not follow the global one
+// (`aligned == 0`, lattice views with 8-byte copies) stay on k_fused.
+#ifndef SGH_PIPE_STAGES
+#define SGH_PIPE_STAGES 3
+#endif
+#ifndef SGH_PIPE_GROUPS
+#define SGH_PIPE_GROUPS 1
+#endif
+#ifndef SGH_PIPE_CWARPS
+#define SGH_PIPE_CWARPS 8
+#endif
+constexpr int kPipeStages = SGH_PIPE_STAGES;
+constexpr int kPipeGroups = SGH_PIPE_GROUPS;
+constexpr int kPipeCT = 32 * SGH_PIPE_CWARPS;          // threads per consumer group
+constexpr int kPipeThreads = 64 + kPipeGroups * kPipeCT;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t *b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mb_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// one arrival, triggered when all of this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void mb_arrive_cpasync(uint64_t *b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(double *sdst, const double *gsrc, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Contiguous runs of a W == 1 tile, for the loads (every existing row) or the
+// stores (the rows the tile writes; fused_segments).  Run i (i < count) covers
+// SMEM [lo(i), lo(i) + len) of the stage and global [g(i), g(i) + len).
+struct PipeRuns {
+  double *g0;
+  int64_t Gj, Gn;
+  int A, ej, y0, z0, nyw, len, count;
+  __device__ __forceinline__ PipeRuns(const Task &T, const FusedTile &f, bool store) {
+    if (T.bj < 0) {                                 // dense: one range of R units
+      g0 = f.g;
+      Gj = Gn = 0;
+      A = ej = 1;
+      y0 = z0 = 0;
+      nyw = 1;
+      len = f.units * T.P;
+      count = 1;
+      return;
+    }
+    const bool blocked = T.bt < T.gl[T.bj];
+    A = T.A;
+    ej = T.ej;
+    y0 = (store && blocked) ? 1 : f.ylo;
+    const int y1 = (store && blocked) ? ej - 2 : f.yhi;
+    const int ny = y1 - y0 + 1;
+    z0 = 0;
+    int nz = T.P / (A * ej);
+    if (T.bt2 >= 0) {
+      z0 = store ? 1 : f.zlo;
+      nz = (store ? nz - 2 : f.zhi) - z0 + 1;
+    }
+    Gj = T.Gj;
+    Gn = T.Gnext;
+    g0 = f.g;
+    const bool dense_y = (Gj == (int64_t)A);
+    len = dense_y ? ny * A : A;
+    nyw = dense_y ? 1 : ny;
+    count = (ny > 0 && nz > 0) ? nz * nyw : 0;
+  }
+  __device__ __forceinline__ int lo(int i) const {
+    const int z = i / nyw, yy = i - z * nyw;
+    return ((z0 + z) * ej + y0 + yy) * A;
+  }
+  __device__ __forceinline__ double *g(int i) const {
+    const int z = i / nyw, yy = i - z * nyw;
+    return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)(z0 + z) * Gn;
+  }
+};
+
+template <bool INV>
+__global__ void __launch_bounds__(kPipeThreads, 1) k_fpipe(const __grid_constant__ Src src) {
+  extern __shared__ __align__(128) double pipe_smem[];
+  __shared__ __align__(8) uint64_t bar_full[kPipeStages], bar_computed[kPipeStages], bar_empty[kPipeStages];
+  __shared__ __align__(16) Task s_task[kPipeStages];
+  __shared__ FusedTile s_tile[kPipeStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPipeStages; ++s) {
+      mb_init(&bar_full[s], 32);                    // one (cp.async-triggered) arrival per producer lane
+      mb_init(&bar_computed[s], 1);                 // the consumer group's leader
+      mb_init(&bar_empty[s], 1);                    // the storer's lane 0
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = src.total_tiles;
+  const int64_t q0 = blockIdx.x, qstep = gridDim.x;
+  const int sd = src.stage_doubles;
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    int idx = -1;
+    int64_t q = q0;
+    for (int k = 0; q < total; ++k, q += qstep) {
+      const int s = k % kPipeStages;
+      const int r = k / kPipeStages;
+      if (r > 0) mb_wait(&bar_empty[s], (r - 1) & 1);
+      const Task *Tg;
+      int64_t ql;
+      if (src.tasks) {
+        idx = (idx < 0) ? first_task(src, q) : advance_task(src, idx, q);
+        ql = q - __ldg(&src.prefix[idx]);
+        Tg = &src.tasks[idx];
+      } else {
+        Tg = &src.single;
+        ql = q;
+      }
+      {
+        const uint64_t *a = reinterpret_cast<const uint64_t *>(Tg);
+        uint64_t *b = reinterpret_cast<uint64_t *>(&s_task[s]);
+        for (int i = lane; i < (int)(sizeof(Task) / 8); i += 32) b[i] = a[i];
+      }
+      __syncwarp();
+      const Task &T = s_task[s];
+      const FusedTile f = fused_tile<1>(T, ql);
+      if (lane == 0) s_tile[s] = f;
+      double *stage = pipe_smem + (size_t)s * sd + f.par;
+      const PipeRuns runs(T, f, false);
+      // this lane's runs: i = lane, lane + 32, ..; bytes first (expect_tx before the copies)
+      uint32_t tx = 0;
+      for (int i = lane; i < runs.count; i += 32) {
+        const int head = phase8(runs.g(i));
+        tx += (uint32_t)((runs.len - head) >> 1) * 16u;
+      }
+      if (tx) mb_expect_tx(&bar_full[s], tx);
+      for (int i = lane; i < runs.count; i += 32) {
+        double *sp = stage + runs.lo(i);
+        const double *gp = runs.g(i);
+        const int len = runs.len;
+        const int head = phase8(gp);
+        const int pairs = (len - head) >> 1;
+        const int last = head + 2 * pairs;
+        if (head) cp_async8(sp, gp);
+        if (last < len) cp_async8(sp + last, gp + last);
+        if (pairs > 0) bulk_load(sp + head, gp + head, (uint32_t)pairs * 16u, &bar_full[s]);
+      }
+      mb_arrive_cpasync(&bar_full[s]);
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------------- storer
+    int64_t q = q0;
+    for (int k = 0; q < total; ++k, q += qstep) {
+      const int s = k % kPipeStages;
+      mb_wait(&bar_computed[s], (k / kPipeStages) & 1);
+      const Task &T = s_task[s];
+      const FusedTile f = s_tile[s];
+      const double *sm = pipe_smem + (size_t)s * sd + f.par;
+      const PipeRuns runs(T, f, true);
+      for (int i = lane; i < runs.count; i += 32) {
+        const double *sp = sm + runs.lo(i);
+        double *gp = runs.g(i);
+        const int len = runs.len;
+        const int head = phase8(gp);
+        const int pairs = (len - head) >> 1;
+        const int last = head + 2 * pairs;
+        if (head) __stcg(gp, sp[0]);
+        if (last < len) __stcg(gp + last, sp[last]);
+        if (pairs > 0)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gp + head),
+                       "r"(smem_u32(sp + head)), "r"(pairs * 16)
+                       : "memory");
+      }
+      bulk_commit();
+      bulk_wait_read();                             // this lane's copies have read the stage
+      __syncwarp();
+      if (lane == 0) mb_arrive(&bar_empty[s]);
+    }
+    bulk_wait_all();
+  } else {
+    // ----------------------------------------------------------- consumers
+    const int g = (warp - 2) / SGH_PIPE_CWARPS;
+    const GroupSync<kPipeCT> sy{(int)threadIdx.x - 64 - g * kPipeCT, 1 + g};
+    int64_t q = q0 + (int64_t)g * qstep;
+    for (int k = g; q < total; k += kPipeGroups, q += kPipeGroups * qstep) {
+      const int s = k % kPipeStages;
+      mb_wait(&bar_full[s], (k / kPipeStages) & 1);
+      const Task &T = s_task[s];
+      const FusedTile f = s_tile[s];
+      fused_compute<INV, 1, kPipeCT, GroupSync<kPipeCT>>(T, f, pipe_smem + (size_t)s * sd + f.par, sy);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // SMEM results -> the bulk stores
+      sy.bar();
+      if (sy.tid() == 0) mb_arrive(&bar_computed[s]);
+    }
+  }
+}
+
+// W == 1 FUSED tasks the pipelined kernel runs: dense ranges, or runs whose
+// SMEM 8-byte phase follows the global one (bulk copies need equal 16-byte phases)
+bool pipe_task(const Task &t) { return t.kind == KIND_FUSED && t.W == 1 && (t.bj < 0 || t.aligned); }
+
 // ----------------------------------------------------------------------- REG
 // One thread per column (o, r); the whole pole of n = 2^L - 1 points lives in
 // registers; the level structure is resolved at compile time.  Each thread
@@ -1418,8 +1689,8 @@ __global__ void __launch_bounds__(kThreads) k_reg(const __grid_constant__ Src sr
 #pragma unroll
           for (int i = s; i <= n; i += 2 * s) {
             double x = v[c][i - 1];
-            if (i - s >= 1) x = x + 0.5 * v[c][i - s - 1];
-            if (i + s <= n) x = x + 0.5 * v[c][i + s - 1];
+            if (i - s >= 1) x = hadd(x, v[c][i - s - 1]);
+            if (i + s <= n) x = hadd(x, v[c][i + s - 1]);
             v[c][i - 1] = x;
           }
         }
@@ -1513,6 +1784,8 @@ static int resident_ctas(KernelFn fn, size_t smem, int threads = kThreads) {
   struct Entry { KernelFn fn; int dev; size_t smem; int ctas; };
   static Entry cache[256];
   static int ncache = 0;
+  static std::mutex mu;                           // calls may come from several host threads
+  std::lock_guard<std::mutex> lk(mu);
   for (int i = 0; i < ncache; ++i)
     if (cache[i].fn == fn && cache[i].dev == dev && cache[i].smem == smem) return cache[i].ctas;
   // Opt in to large dynamic shared memory (FUSED / STRIDED tiles up to ~70 KB):
@@ -1538,7 +1811,8 @@ static int resident_ctas(KernelFn fn, size_t smem, int threads = kThreads) {
 
 // Launch one task (single grid).  Returns the CUDA error of the launch.
 cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
-  KernelFn fn = kernel_for(task.kind, task.l, task.W, inv);
+  const bool pipe = pipe_task(task);
+  KernelFn fn = pipe ? (inv ? k_fpipe<true> : k_fpipe<false>) : kernel_for(task.kind, task.l, task.W, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = nullptr;
@@ -1549,9 +1823,9 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
   size_t smem = task_smem(task);
   if (task.kind == KIND_FUSED) {                 // pipeline stages, 16-byte aligned
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
-    smem = size_t(fused_stages()) * src.stage_doubles * 8;
+    smem = size_t(pipe ? kPipeStages : fused_stages()) * src.stage_doubles * 8;
   }
-  const int nt = task.kind == KIND_FUSED ? (task.W == 1 ? FT<1>::v : FT<8>::v) : kThreads;
+  const int nt = pipe ? kPipeThreads : task.kind == KIND_FUSED ? (task.W == 1 ? FT<1>::v : FT<8>::v) : kThreads;
   const int64_t cap = resident_ctas(fn, smem, nt);
   const int64_t grid = task.tiles < cap ? task.tiles : cap;
   if (grid <= 0) return cudaSuccess;
@@ -1567,8 +1841,8 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
 // smem = max task_smem over the group.
 cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
                          int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream,
-                         int variant) {
-  KernelFn fn = kernel_for(kind, l, w, inv);
+                         int variant, bool pipe) {
+  KernelFn fn = pipe ? (inv ? k_fpipe<true> : k_fpipe<false>) : kernel_for(kind, l, w, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = d_tasks;
@@ -1577,9 +1851,9 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
   src.total_tiles = total_tiles;
   if (kind == KIND_FUSED) {
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
-    smem = size_t(fused_stages()) * src.stage_doubles * 8;
+    smem = size_t(pipe ? kPipeStages : fused_stages()) * src.stage_doubles * 8;
   }
-  const int nt = kind == KIND_FUSED ? (w == 1 ? FT<1>::v : FT<8>::v) : kThreads;
+  const int nt = pipe ? kPipeThreads : kind == KIND_FUSED ? (w == 1 ? FT<1>::v : FT<8>::v) : kThreads;
   const int64_t cap = resident_ctas(fn, smem, nt);
   const int64_t grid = total_tiles < cap ? total_tiles : cap;
   if (grid <= 0) return cudaSuccess;

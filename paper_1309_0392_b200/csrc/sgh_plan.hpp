@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <exception>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -15,7 +17,9 @@ namespace sgh {
 cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream);
 cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
                          int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream,
-                         int variant = 0);
+                         int variant = 0, bool pipe = false);
+// W == 1 FUSED tasks that run on the pipelined bulk-copy kernel k_fpipe (grouped separately)
+bool pipe_task(const Task &t);
 size_t task_smem(const Task &t);
 
 // per-launch profiling (sgh_profile.cu); a no-op unless sgh_profile_enable(1)
@@ -75,6 +79,40 @@ void plan_axis(double *grid, const int32_t *levels, int d, int k, std::vector<Ta
 // phase over all 2^{l-tb} blocks (rlog = l - tb, blk0 = 0).  False if no tile fits.
 bool plan_view_fine(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64_t base, int l, int tb,
                     std::vector<Task> &phases);
+
+// No C++ exception may cross the C ABI (sgh.h): every extern "C" entry point
+// that builds host containers runs its body through one of these.  Host
+// allocation failure -> SGH_ERR_CAPACITY, anything else -> INVALID_ARGUMENT,
+// with the detail in sgh_last_error().
+template <class F>
+sgh_status guarded(F &&body) {
+  try {
+    return body();
+  } catch (const std::bad_alloc &) {
+    set_error("host allocation failed (request too large)");
+    return SGH_ERR_CAPACITY;
+  } catch (const std::exception &e) {
+    set_error(std::string("internal error: ") + e.what());
+    return SGH_ERR_INVALID_ARGUMENT;
+  } catch (...) {
+    set_error("internal error");
+    return SGH_ERR_INVALID_ARGUMENT;
+  }
+}
+// the same for entry points that return a size / count (`fail` on error)
+template <class T, class F>
+T guarded_value(T fail, F &&body) {
+  try {
+    return body();
+  } catch (const std::bad_alloc &) {
+    set_error("host allocation failed (request too large)");
+  } catch (const std::exception &e) {
+    set_error(std::string("internal error: ") + e.what());
+  } catch (...) {
+    set_error("internal error");
+  }
+  return fail;
+}
 
 // helpers shared by the drivers (sgh_capi.cu)
 sgh_status cuda_fail(cudaError_t e, const char *where);

@@ -16,7 +16,7 @@
 namespace sgh {
 
 struct ProfRec {
-  int kind, l, inv, variant;
+  int kind, l, inv, variant, dev;
   double bytes;
   cudaEvent_t a, b;
 };
@@ -24,12 +24,17 @@ struct ProfRec {
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<ProfRec> g_recs;
-static std::vector<cudaEvent_t> g_pool;
+// free events, per device: an event may only be recorded on a stream of the
+// device that was current when it was created
+static std::vector<std::pair<int, cudaEvent_t>> g_pool;
 
 static cudaEvent_t take_event() {
-  if (!g_pool.empty()) {
-    cudaEvent_t e = g_pool.back();
-    g_pool.pop_back();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (size_t i = g_pool.size(); i-- > 0;) {
+    if (g_pool[i].first != dev) continue;
+    cudaEvent_t e = g_pool[i].second;
+    g_pool.erase(g_pool.begin() + i);
     return e;
   }
   cudaEvent_t e = nullptr;
@@ -50,7 +55,9 @@ void prof_end(ProfToken tok, int kind, int l, bool inv, double bytes, cudaStream
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t b = take_event();
   cudaEventRecord(b, s);
-  g_recs.push_back(ProfRec{kind, l, inv ? 1 : 0, variant, bytes, tok.start, b});
+  int dev = 0;
+  cudaGetDevice(&dev);
+  g_recs.push_back(ProfRec{kind, l, inv ? 1 : 0, variant, dev, bytes, tok.start, b});
 }
 
 }  // namespace sgh
@@ -62,8 +69,8 @@ extern "C" {
 sgh_status sgh_profile_enable(int32_t on) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   for (ProfRec &r : g_recs) {
-    g_pool.push_back(r.a);
-    g_pool.push_back(r.b);
+    g_pool.emplace_back(r.dev, r.a);
+    g_pool.emplace_back(r.dev, r.b);
   }
   g_recs.clear();
   g_prof_on = on != 0;

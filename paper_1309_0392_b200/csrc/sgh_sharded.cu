@@ -457,12 +457,15 @@ extern "C" {
 
 sgh_status sgh_shard_rows(const int32_t *levels, int32_t d, int32_t nranks, int32_t rank, int64_t *row_begin,
                           int64_t *row_end) {
+  return guarded([&]() -> sgh_status {
   if (!row_begin || !row_end) return invalid("NULL output pointer");
   return shard_rows_impl(levels, d, nranks, rank, row_begin, row_end);
+});
 }
 
 sgh_status sgh_shard_layout(const int32_t *levels, int32_t d, int32_t nranks, int64_t *row_begin, int64_t *rows,
                             int64_t *col_begin, int64_t *cols) {
+  return guarded([&]() -> sgh_status {
   if (!row_begin || !rows || !col_begin || !cols) return invalid("NULL output pointer");
   ShardGeom G;
   sgh_status st = validate_levels(levels, d, nullptr);
@@ -477,6 +480,7 @@ sgh_status sgh_shard_layout(const int32_t *levels, int32_t d, int32_t nranks, in
     cols[q] = G.cols[q];
   }
   return SGH_OK;
+});
 }
 
 sgh_status sgh_comm_unique_id(void *out) {
@@ -490,6 +494,7 @@ sgh_status sgh_comm_unique_id(void *out) {
 }
 
 sgh_status sgh_comm_create(void **comm, const void *nccl_unique_id, int32_t nranks, int32_t rank) {
+  return guarded([&]() -> sgh_status {
   if (!comm || !nccl_unique_id) return invalid("NULL argument");
   if (nranks < 1 || rank < 0 || rank >= nranks) return invalid("bad nranks/rank");
   ncclUniqueId id;
@@ -504,6 +509,7 @@ sgh_status sgh_comm_create(void **comm, const void *nccl_unique_id, int32_t nran
   }
   *comm = c;
   return SGH_OK;
+});
 }
 
 void sgh_comm_destroy(void *comm) {
@@ -514,49 +520,63 @@ void sgh_comm_destroy(void *comm) {
 }
 
 size_t sgh_sharded_workspace_bytes(const int32_t *levels, int32_t d, int32_t nranks) {
+  return guarded_value<size_t>(0, [&]() -> size_t {
   ShardGeom G;
   if (validate_levels(levels, d, nullptr) != SGH_OK) return 0;
   int64_t b, e;
   if (shard_rows_impl(levels, d, nranks, 0, &b, &e) != SGH_OK) return 0;
   if (make_geom(levels, d, nranks, 0, G) != SGH_OK) return 0;
   return size_t(2 * stage_elems(G) * 8);
+});
 }
 
 sgh_status sgh_hierarchize_sharded(double *shard, const int32_t *levels, int32_t d, void *comm, void *workspace,
                                    size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   return sharded_nccl(shard, levels, d, comm, workspace, ws_bytes, stream, false);
+});
 }
 
 sgh_status sgh_dehierarchize_sharded(double *shard, const int32_t *levels, int32_t d, void *comm, void *workspace,
                                      size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   return sharded_nccl(shard, levels, d, comm, workspace, ws_bytes, stream, true);
+});
 }
 
 size_t sgh_sharded_halo_workspace_bytes(const int32_t *levels, int32_t d, int32_t nranks) {
+  return guarded_value<size_t>(0, [&]() -> size_t {
   HaloGeom H;
   if (make_halo_geom(levels, d, nranks, H) != SGH_OK) return 0;
   return size_t(H.P * H.C * 8);
+});
 }
 
 sgh_status sgh_transform_sharded_halo(double *shard, const int32_t *levels, int32_t d, void *comm, uint32_t flags,
                                       void *workspace, size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
   return sharded_halo_nccl(shard, levels, d, comm, workspace, ws_bytes, stream, (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
+});
 }
 
 sgh_status sgh_transform_sharded_halo_loopback(double *const *shards, const int32_t *levels, int32_t d,
                                                int32_t nranks, uint32_t flags, void *workspace, size_t ws_bytes,
                                                void *stream) {
+  return guarded([&]() -> sgh_status {
   if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
   return sharded_halo_loopback(shards, levels, d, nranks, workspace, ws_bytes, stream,
                                (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
+});
 }
 
 sgh_status sgh_transform_sharded_loopback(double *const *shards, const int32_t *levels, int32_t d, int32_t nranks,
                                           uint32_t flags, void *workspace, size_t ws_bytes, void *stream) {
+  return guarded([&]() -> sgh_status {
   if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
   return sharded_loopback(shards, levels, d, nranks, workspace, ws_bytes, stream,
                           (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
+});
 }
 
 }  // extern "C"

@@ -183,6 +183,22 @@ def test_tent_only_root_surplus(levels):
     assert not np.any(f)
 
 
+def test_update_rounds_product_and_difference_separately():
+    """Alg. 1's update x <- x - 0.5*x_pred (reading R5/R8) is two
+    IEEE operations: RN(0.5*e) then RN(x - that).  With t = 2^-1074 (the
+    smallest subnormal), level-2 pole [3t, t, 0]: point 1's right predecessor
+    is the root t; RN(0.5 t) is a tie that rounds to even, i.e. +0, so
+    alpha_1 = 3t exactly (a single-rounding fma would give RN(2.5 t) = 2t).
+    The inverse: 3t + RN(0.5 t) = 3t as well."""
+    t = np.ldexp(1.0, -1074)
+    u = np.array([3 * t, t, 0.0])
+    a = oracle.hierarchize(u.copy(), (2,))
+    assert a[0] == 3 * t and a[1] == t and a[2] == 0.0
+    assert a[0] != 2 * t
+    v = oracle.dehierarchize(np.array([3 * t, t, 0.0]), (2,))
+    assert v[0] == 3 * t
+
+
 # ------------------------------------------------------------- invariants
 @pytest.mark.parametrize("levels", [(12, 3), (4, 5, 6), (2, 2, 2, 2, 2), (9,)], ids=str)
 def test_round_trip(levels):

@@ -99,6 +99,30 @@ def test_shape_sweep_bitwise(sgh, levels, inverse, fuse):
     assert_bitwise(got, want)
 
 
+SUBNORMAL_SHAPES = [(5,), (13,), (6, 6), (14, 3), (8, 8, 8), (6, 6, 5, 5), (10, 4, 4, 4), (2, 7, 11, 2), (9, 2, 8, 2),
+                    (3, 7, 7, 4), (12, 4, 5)]
+
+
+@pytest.mark.parametrize("levels", SUBNORMAL_SHAPES, ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+@pytest.mark.parametrize("fuse", FUSE_MODES, ids=FUSE_IDS)
+def test_subnormal_bitwise(sgh, levels, inverse, fuse):
+    """Subnormal and near-underflow inputs: 0.5*x is inexact for subnormal x
+    with an odd last bit, so a contracted FMA would round once where the
+    oracle (built with -ffp-contract=off) rounds the product and the sum
+    separately.  Every kernel kind must keep the two roundings (bitwise)."""
+    N = si.num_points(levels)
+    u = si.fill_uniform(N, grid_id=(N * 5 + 3) % 9973)
+    k = np.floor(u * 2.0 ** 52)                                # integers |k| < 2^52, many odd
+    sub = np.ldexp(k, -1074)                                   # subnormal multiples of 2^-1074
+    near = np.ldexp(u, -1020)                                  # normal, halving reaches subnormal
+    x = np.where(np.arange(N) % 3 == 0, near, sub)
+    want = x.copy()
+    (oracle.dehierarchize if inverse else oracle.hierarchize)(want, levels)
+    got = gpu_transform(sgh, x, levels, inverse=inverse, fuse=fuse)
+    assert_bitwise(got, want)
+
+
 @pytest.mark.parametrize("levels", [(5, 5), (3, 4, 2), (7, 6, 3), (2, 3, 2, 3)], ids=str)
 def test_axis_orders_and_masks(sgh, levels):
     """Other axis orders: bitwise vs the oracle run in the same order."""
