@@ -1221,10 +1221,12 @@ int64_t sgh_plan_describe(const int32_t *levels, int32_t d, uint32_t flags, char
         std::string lv;
         for (int j = 0; j < t.m; ++j) lv += (j ? "," : "") + std::to_string(int(t.gl[j]));
         std::snprintf(line, sizeof line,
-                      "  FUSED W=%d levels=(%s) special=%d bt=%d bt2=%d aligned=%d skip=%u points=%.0f\n", t.W,
-                      lv.c_str(), t.bj, t.bj >= 0 ? t.bt : -1, t.bj >= 0 ? t.bt2 : -1, t.bj >= 0 ? t.aligned : 1,
-                      t.skipmask,
-                      task_points(t));
+                      "  FUSED W=%d levels=(%s) special=%d bt=%d bt2=%d aligned=%d skip=%u P=%d R=%d A=%d ej=%d "
+                      "runlen=%lld tiles=%lld points=%.0f\n",
+                      t.W, lv.c_str(), t.bj, t.bj >= 0 ? t.bt : -1, t.bj >= 0 ? t.bt2 : -1,
+                      t.bj >= 0 ? t.aligned : 1, t.skipmask, t.P, t.R, t.bj >= 0 ? t.A : 0, t.bj >= 0 ? t.ej : 0,
+                      (long long)(t.W > 1 ? t.W : t.bj < 0 ? int64_t(t.R) * t.P : (t.Gj == t.A ? int64_t(t.A) * t.ej : t.A)),
+                      (long long)t.tiles, task_points(t));
       } else {
         std::snprintf(line, sizeof line, "  %s l=%d t=%d W=%d points=%.0f\n", names[t.kind], t.l, t.t, t.W,
                       task_points(t));

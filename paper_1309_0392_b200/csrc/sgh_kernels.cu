@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -87,6 +89,8 @@ struct Src {
   int32_t ntasks;
   int32_t stage_doubles;  // FUSED: SMEM doubles per pipeline stage (2 stages)
   int64_t total_tiles;
+  int32_t nstages;        // k_fpipe: stages of the SMEM ring
+  int32_t pad_;
   Task single;
 };
 
@@ -597,24 +601,40 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
     return oo * n * R + rk;
   };
   auto pole_base = [&](int p) -> double * { return sm + pole_row(p) * RS + (p & (W - 1)); };
-  if (l <= 4) {
+  // register poles of level L over all poles: the level dispatch is hoisted
+  // out of the pole loop
+  auto reg_poles = [&](auto LC, int off, int str) {
+    constexpr int L = decltype(LC)::value;
     for (int p = sy.tid(); p < npoles; p += NT) {
       if (hs.on && hs.skip(pole_row(p))) continue;
-      pole_regs_rt<INV>(pole_base(p), l, STR);
+      pole_regs<L, INV>(pole_base(p) + off, str);
     }
+  };
+  auto reg_poles_rt = [&](int L, int off, int str) {
+    switch (L) {
+      case 2: reg_poles(std::integral_constant<int, 2>(), off, str); break;
+      case 3: reg_poles(std::integral_constant<int, 3>(), off, str); break;
+      case 4: reg_poles(std::integral_constant<int, 4>(), off, str); break;
+      default: break;                            // L = 1: a single point, no update
+    }
+  };
+  if (l <= 4) {
+    reg_poles_rt(l, 0, STR);
     sy.bar();
     return;
   }
-  // lattice levels visited: l, l-kTB, l-2kTB, ... (> 4), then the register lattice
-  int levels[8], nlev = 0, lf = l;
+  // lattice levels visited: l, l-kTB, l-2kTB, ... (> 4), then the register
+  // lattice of level lf <= 4 (level k is l - kTB k: no array, which would
+  // live in local memory)
+  int nlev = 0, lf = l;
   while (lf > 4) {
-    levels[nlev++] = lf;
+    ++nlev;
     lf -= kTB;
   }
   const ItemWalk walk(npoles, (int)sy.tid(), NT, fnp);
   auto block_phase = [&](int k) {                // k-th lattice level: stride 2^{kTB k}
     const int m = 1 << (kTB * k);
-    const int nblk = 1 << (levels[k] - kTB);
+    const int nblk = 1 << (l - kTB * k - kTB);
     // items (b, p), p fastest: lanes run over poles (conflict-free SMEM)
     for (int b = walk.b0, p = walk.p0; b < nblk; walk.next(b, p)) {
       if (hs.on && hs.skip(pole_row(p))) continue;
@@ -625,11 +645,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   auto lattice_phase = [&]() {
     if (lf <= 1) return;                         // a single point: no update
     const int m = 1 << (kTB * nlev);
-    for (int p = sy.tid(); p < npoles; p += NT) {
-      if (hs.on && hs.skip(pole_row(p))) continue;
-      double *p0 = pole_base(p) - STR;           // virtual point 0
-      pole_regs_rt<INV>(p0 + m * STR, lf, m * STR);
-    }
+    reg_poles_rt(lf, (m - 1) * STR, m * STR);    // point j of the lattice at (j m - 1) STR
     sy.bar();
   };
   if (!INV) {
@@ -1402,16 +1418,20 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
 // ============================================= PIPELINED FUSED W == 1 (k_fpipe)
 // The same tiles as k_fused<W = 1> (whole poles of a run of axes, or a run
 // with one / two BLOCKED axes; contiguous global runs), run by a
-// warp-specialised persistent CTA, one per SM, over a ring of kPipeStages SMEM
-// stages:
-//   warp 0        producer: per tile, waits until its stage is free, copies the
-//                 task descriptor and tile geometry into SMEM, and issues the
-//                 tile's loads -- one cp.async.bulk (TMA bulk copy, SASS
-//                 UBLKCP) per contiguous run into the 16-byte aligned body,
-//                 completing on the stage's `full` mbarrier by transaction
-//                 count, plus 8-byte cp.async for the odd end elements of runs
-//                 at an 8-mod-16 phase (cp.async.mbarrier.arrive.noinc);
-//   warps 2..     consumers (kPipeGroups groups of kPipeCWarps warps, group g
+// warp-specialised persistent CTA, one per SM, over a ring of NS SMEM stages
+// (and NS + 3 descriptor slots):
+//   warp 2        descriptors: per tile, finds its task (prefix table) and
+//                 copies the task descriptor and the tile geometry into a
+//                 slot, up to NS + 3 tiles ahead (slot freed by the storer), so
+//                 these dependent global loads never sit on the load path;
+//   warp 0        producer: per tile, waits for its descriptor and a free
+//                 stage and issues the tile's loads -- one cp.async.bulk (TMA
+//                 bulk copy, SASS UBLKCP) per contiguous run into the 16-byte
+//                 aligned body, completing on the stage's `full` mbarrier by
+//                 transaction count, plus 8-byte cp.async for the odd end
+//                 elements of runs at an 8-mod-16 phase
+//                 (cp.async.mbarrier.arrive.noinc);
+//   warps 3..     consumers (CFG::groups groups of CFG::cwarps warps, group g
 //                 takes tiles g, g + G, ..): wait for `full`, run the group's
 //                 axes in SMEM (fused_compute: the oracle's operation order,
 //                 bitwise), fence the generic-proxy writes for the async proxy
@@ -1419,24 +1439,40 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
 //   warp 1        storer: waits for `computed`, issues the bulk stores of the
 //                 tile's written runs (cp.async.bulk shared -> global) and its
 //                 8-byte ends, waits until the copies have READ the stage and
-//                 arrives on `empty`.
+//                 arrives on `empty` (and frees the descriptor slot).
 // So the loads of tile k+1.. and the stores of tile k-1 stream while tile k is
 // transformed: the engine keeps HBM busy, the SM's issue slots go to the
 // transform.  Tasks whose SMEM phase does not follow the global one
 // (`aligned == 0`, lattice views with 8-byte copies) stay on k_fused.
-#ifndef SGH_PIPE_STAGES
-#define SGH_PIPE_STAGES 3
+// The ring holds as many stages as fit the SM's shared memory (chosen per
+// launch from the group's largest tile: 3 stages of the 8192-point tiles,
+// more for smaller tiles), at most kPipeMaxStages.
+constexpr int kPipeMaxStages = 6;
+constexpr int kPipeDescAhead = 3;                    // descriptor slots beyond the stages
+constexpr int kPipeMaxDesc = kPipeMaxStages + kPipeDescAhead;
+// Consumer configuration <groups, warps per group>: one task per launch (a
+// single big grid, every tile alike: C4's two-blocked tiles) -> one group of 8
+// warps (C4 281.7 vs 273.4 Gpoints/s with 2 x 6); a batched launch (every
+// tile a different task, short barrier phases: C5) -> two groups of 6 warps
+// that transform two tiles at once (C5 157.1 vs 147.9).
+template <int G, int CW>
+struct PipeCfg {
+  static constexpr int groups = G;
+  static constexpr int cwarps = CW;
+  static constexpr int ct = 32 * CW;              // threads per consumer group
+  static constexpr int threads = 96 + G * 32 * CW;
+};
+#ifndef SGH_PIPE_BG
+#define SGH_PIPE_BG 2
 #endif
-#ifndef SGH_PIPE_GROUPS
-#define SGH_PIPE_GROUPS 1
+#ifndef SGH_PIPE_BW
+#define SGH_PIPE_BW 6
 #endif
-#ifndef SGH_PIPE_CWARPS
-#define SGH_PIPE_CWARPS 8
+#ifndef SGH_PIPE_SW
+#define SGH_PIPE_SW 8
 #endif
-constexpr int kPipeStages = SGH_PIPE_STAGES;
-constexpr int kPipeGroups = SGH_PIPE_GROUPS;
-constexpr int kPipeCT = 32 * SGH_PIPE_CWARPS;          // threads per consumer group
-constexpr int kPipeThreads = 64 + kPipeGroups * kPipeCT;
+using PipeSingle = PipeCfg<1, SGH_PIPE_SW>;
+using PipeBatched = PipeCfg<SGH_PIPE_BG, SGH_PIPE_BW>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mb_init(uint64_t *b, uint32_t count) {
@@ -1518,18 +1554,74 @@ struct PipeRuns {
   }
 };
 
-template <bool INV>
-__global__ void __launch_bounds__(kPipeThreads, 1) k_fpipe(const __grid_constant__ Src src) {
+// Task owning tile q (the last t with prefix[t] <= q), searching forward from
+// idx (prefix[idx] <= q) with the whole warp: 32 probes per round trip at
+// stride 1, 32, 1024, .. (expanding while all probes are <= q, then refining).
+// The prefix is non-decreasing, so the probes that are <= q form a prefix of
+// the lanes.
+__device__ __forceinline__ int warp_find_task(const Src &src, int idx, int64_t q, int lane) {
+  int step = 1;
+  bool expanding = true;
+  for (;;) {
+    const int64_t p = (int64_t)idx + 1 + (int64_t)lane * step;
+    const bool le = p < src.ntasks && __ldg(&src.prefix[p]) <= q;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, le));
+    if (cnt == 32 && expanding) {                 // the answer is further on
+      idx += 1 + 31 * step;                       // the last probe, <= q
+      if (step < (1 << 20)) step *= 32;
+      continue;
+    }
+    if (cnt > 0) idx += 1 + (cnt - 1) * step;     // the last probe <= q
+    if (step == 1) return idx;                    // the next position is > q (or the end)
+    expanding = false;
+    step /= 32;                                   // the answer lies in (idx, idx + 32 step)
+  }
+}
+
+// -DSGH_PIPE_TRACE (diagnostic build only): %globaltimer stamps of the first
+// kTraceTiles tiles of every CTA of launches with >= g_ptrace_min tiles, read
+// back with sgh_debug_pipe_trace().  Events per tile: 0 descriptor published,
+// 1 producer starts issuing, 2 loads issued, 3 consumer starts waiting,
+// 4 data ready, 5 computed, 6 stores issued, 7 stores have read the stage.
+#ifdef SGH_PIPE_TRACE
+constexpr int kTraceTiles = 64;
+__device__ unsigned long long g_ptrace[160 * kTraceTiles * 8];
+__device__ long long g_ptrace_min = 1ll << 62;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PTRACE(k, ev)                                                                          \
+  do {                                                                                         \
+    if (trace_on && (k) < kTraceTiles && blockIdx.x < 160)                                     \
+      g_ptrace[((size_t)blockIdx.x * kTraceTiles + (k)) * 8 + (ev)] = gtime();                 \
+  } while (0)
+#else
+#define PTRACE(k, ev) \
+  do {                \
+  } while (0)
+#endif
+
+template <bool INV, class CFG>
+__global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant__ Src src) {
   extern __shared__ __align__(128) double pipe_smem[];
-  __shared__ __align__(8) uint64_t bar_full[kPipeStages], bar_computed[kPipeStages], bar_empty[kPipeStages];
-  __shared__ __align__(16) Task s_task[kPipeStages];
-  __shared__ FusedTile s_tile[kPipeStages];
+  __shared__ __align__(8) uint64_t bar_full[kPipeMaxStages], bar_computed[kPipeMaxStages],
+      bar_empty[kPipeMaxStages], bar_dfull[kPipeMaxDesc], bar_dfree[kPipeMaxDesc];
+  __shared__ __align__(16) Task s_task[kPipeMaxDesc];   // descriptor slot of tile k: k % ND
+  __shared__ FusedTile s_tile[kPipeMaxDesc];
+  const int NS = src.nstages;                     // stage of tile k: k % NS
+  const int ND = NS + kPipeDescAhead;             // descriptor slots
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kPipeStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mb_init(&bar_full[s], 32);                    // one (cp.async-triggered) arrival per producer lane
       mb_init(&bar_computed[s], 1);                 // the consumer group's leader
       mb_init(&bar_empty[s], 1);                    // the storer's lane 0
+    }
+    for (int s = 0; s < ND; ++s) {
+      mb_init(&bar_dfull[s], 32);                   // every lane of the descriptor warp
+      mb_init(&bar_dfree[s], 1);                    // the storer's lane 0 (the slot's last reader)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -1537,33 +1629,59 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_fpipe(const __grid_constant
   const int64_t total = src.total_tiles;
   const int64_t q0 = blockIdx.x, qstep = gridDim.x;
   const int sd = src.stage_doubles;
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    int idx = -1;
+#ifdef SGH_PIPE_TRACE
+  const bool trace_on = total >= g_ptrace_min;
+#endif
+  if (warp == 2) {
+    // ---------------------------------------------------------- descriptors
+    // Looks up the task of each tile (a chain of dependent global loads: the
+    // tile's task in the prefix table, then its descriptor) and publishes the
+    // descriptor and the tile geometry in a slot, up to ND tiles ahead of the
+    // storer, so the producer never waits for those loads.
+    constexpr int kTW = (int)(sizeof(Task) / 8);
+    static_assert(kTW <= 96, "Task descriptor must fit 3 words per lane");
+    int idx = 0;
     int64_t q = q0;
     for (int k = 0; q < total; ++k, q += qstep) {
-      const int s = k % kPipeStages;
-      const int r = k / kPipeStages;
-      if (r > 0) mb_wait(&bar_empty[s], (r - 1) & 1);
-      const Task *Tg;
+      const int ds = k % ND;
+      const int rr = k / ND;
       int64_t ql;
+      const uint64_t *a;
       if (src.tasks) {
-        idx = (idx < 0) ? first_task(src, q) : advance_task(src, idx, q);
+        idx = warp_find_task(src, idx, q, lane);
         ql = q - __ldg(&src.prefix[idx]);
-        Tg = &src.tasks[idx];
+        a = reinterpret_cast<const uint64_t *>(&src.tasks[idx]);
       } else {
-        Tg = &src.single;
         ql = q;
+        a = reinterpret_cast<const uint64_t *>(&src.single);
       }
-      {
-        const uint64_t *a = reinterpret_cast<const uint64_t *>(Tg);
-        uint64_t *b = reinterpret_cast<uint64_t *>(&s_task[s]);
-        for (int i = lane; i < (int)(sizeof(Task) / 8); i += 32) b[i] = a[i];
-      }
+      uint64_t dreg[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) dreg[u] = (lane + 32 * u < kTW) ? a[lane + 32 * u] : 0;
+      if (rr > 0) mb_wait(&bar_dfree[ds], (rr - 1) & 1);
+      uint64_t *b = reinterpret_cast<uint64_t *>(&s_task[ds]);
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+        if (lane + 32 * u < kTW) b[lane + 32 * u] = dreg[u];
       __syncwarp();
-      const Task &T = s_task[s];
-      const FusedTile f = fused_tile<1>(T, ql);
-      if (lane == 0) s_tile[s] = f;
+      const FusedTile f = fused_tile<1>(s_task[ds], ql);
+      if (lane == 0) s_tile[ds] = f;
+      __syncwarp();
+      if (lane == 0) PTRACE(k, 0);
+      mb_arrive(&bar_dfull[ds]);
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    int64_t q = q0;
+    for (int k = 0; q < total; ++k, q += qstep) {
+      const int s = k % NS;
+      const int r = k / NS;
+      const int ds = k % ND;
+      mb_wait(&bar_dfull[ds], (k / ND) & 1);
+      if (r > 0) mb_wait(&bar_empty[s], (r - 1) & 1);
+      if (lane == 0) PTRACE(k, 1);
+      const Task &T = s_task[ds];
+      const FusedTile f = s_tile[ds];
       double *stage = pipe_smem + (size_t)s * sd + f.par;
       const PipeRuns runs(T, f, false);
       // this lane's runs: i = lane, lane + 32, ..; bytes first (expect_tx before the copies)
@@ -1585,15 +1703,17 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_fpipe(const __grid_constant
         if (pairs > 0) bulk_load(sp + head, gp + head, (uint32_t)pairs * 16u, &bar_full[s]);
       }
       mb_arrive_cpasync(&bar_full[s]);
+      if (lane == 0) PTRACE(k, 2);
     }
   } else if (warp == 1) {
     // -------------------------------------------------------------- storer
     int64_t q = q0;
     for (int k = 0; q < total; ++k, q += qstep) {
-      const int s = k % kPipeStages;
-      mb_wait(&bar_computed[s], (k / kPipeStages) & 1);
-      const Task &T = s_task[s];
-      const FusedTile f = s_tile[s];
+      const int s = k % NS;
+      const int ds = k % ND;
+      mb_wait(&bar_computed[s], (k / NS) & 1);
+      const Task &T = s_task[ds];
+      const FusedTile f = s_tile[ds];
       const double *sm = pipe_smem + (size_t)s * sd + f.par;
       const PipeRuns runs(T, f, true);
       for (int i = lane; i < runs.count; i += 32) {
@@ -1611,25 +1731,37 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_fpipe(const __grid_constant
                        : "memory");
       }
       bulk_commit();
+      if (lane == 0) PTRACE(k, 6);
       bulk_wait_read();                             // this lane's copies have read the stage
       __syncwarp();
-      if (lane == 0) mb_arrive(&bar_empty[s]);
+      if (lane == 0) {
+        PTRACE(k, 7);
+        mb_arrive(&bar_empty[s]);
+        mb_arrive(&bar_dfree[ds]);
+      }
     }
     bulk_wait_all();
   } else {
     // ----------------------------------------------------------- consumers
-    const int g = (warp - 2) / SGH_PIPE_CWARPS;
-    const GroupSync<kPipeCT> sy{(int)threadIdx.x - 64 - g * kPipeCT, 1 + g};
+    constexpr int kPipeCT = CFG::ct;
+    constexpr int kPipeGroups = CFG::groups;
+    const int g = (warp - 3) / CFG::cwarps;
+    const GroupSync<kPipeCT> sy{(int)threadIdx.x - 96 - g * kPipeCT, 1 + g};
     int64_t q = q0 + (int64_t)g * qstep;
     for (int k = g; q < total; k += kPipeGroups, q += kPipeGroups * qstep) {
-      const int s = k % kPipeStages;
-      mb_wait(&bar_full[s], (k / kPipeStages) & 1);
-      const Task &T = s_task[s];
-      const FusedTile f = s_tile[s];
+      const int s = k % NS;
+      if (sy.tid() == 0) PTRACE(k, 3);
+      mb_wait(&bar_full[s], (k / NS) & 1);
+      if (sy.tid() == 0) PTRACE(k, 4);
+      const Task &T = s_task[k % ND];
+      const FusedTile f = s_tile[k % ND];
       fused_compute<INV, 1, kPipeCT, GroupSync<kPipeCT>>(T, f, pipe_smem + (size_t)s * sd + f.par, sy);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // SMEM results -> the bulk stores
       sy.bar();
-      if (sy.tid() == 0) mb_arrive(&bar_computed[s]);
+      if (sy.tid() == 0) {
+        PTRACE(k, 5);
+        mb_arrive(&bar_computed[s]);
+      }
     }
   }
 }
@@ -1809,10 +1941,25 @@ static int resident_ctas(KernelFn fn, size_t smem, int threads = kThreads) {
   return total;
 }
 
+// stages of k_fpipe's ring for a stage size: all that fit the per-block
+// shared memory next to the kernel's static part, 2 .. kPipeMaxStages
+static int pipe_stages(KernelFn fn, size_t stage_bytes) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  size_t stat = 0;
+  if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) stat = fa.sharedSizeBytes;
+  const size_t avail = size_t(optin) > stat + 1024 ? size_t(optin) - stat - 1024 : 0;
+  const int n = stage_bytes ? int(avail / stage_bytes) : kPipeMaxStages;
+  return std::max(2, std::min(kPipeMaxStages, n));
+}
+
 // Launch one task (single grid).  Returns the CUDA error of the launch.
 cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
   const bool pipe = pipe_task(task);
-  KernelFn fn = pipe ? (inv ? k_fpipe<true> : k_fpipe<false>) : kernel_for(task.kind, task.l, task.W, inv);
+  KernelFn fn = pipe ? (inv ? k_fpipe<true, PipeSingle> : k_fpipe<false, PipeSingle>)
+                     : kernel_for(task.kind, task.l, task.W, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = nullptr;
@@ -1823,9 +1970,10 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
   size_t smem = task_smem(task);
   if (task.kind == KIND_FUSED) {                 // pipeline stages, 16-byte aligned
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
-    smem = size_t(pipe ? kPipeStages : fused_stages()) * src.stage_doubles * 8;
+    if (pipe) src.nstages = pipe_stages(fn, size_t(src.stage_doubles) * 8);
+    smem = size_t(pipe ? src.nstages : fused_stages()) * src.stage_doubles * 8;
   }
-  const int nt = pipe ? kPipeThreads : task.kind == KIND_FUSED ? (task.W == 1 ? FT<1>::v : FT<8>::v) : kThreads;
+  const int nt = pipe ? PipeSingle::threads : task.kind == KIND_FUSED ? (task.W == 1 ? FT<1>::v : FT<8>::v) : kThreads;
   const int64_t cap = resident_ctas(fn, smem, nt);
   const int64_t grid = task.tiles < cap ? task.tiles : cap;
   if (grid <= 0) return cudaSuccess;
@@ -1842,7 +1990,7 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
 cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
                          int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream,
                          int variant, bool pipe) {
-  KernelFn fn = pipe ? (inv ? k_fpipe<true> : k_fpipe<false>) : kernel_for(kind, l, w, inv);
+  KernelFn fn = pipe ? (inv ? k_fpipe<true, PipeBatched> : k_fpipe<false, PipeBatched>) : kernel_for(kind, l, w, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = d_tasks;
@@ -1851,9 +1999,10 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
   src.total_tiles = total_tiles;
   if (kind == KIND_FUSED) {
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
-    smem = size_t(pipe ? kPipeStages : fused_stages()) * src.stage_doubles * 8;
+    if (pipe) src.nstages = pipe_stages(fn, size_t(src.stage_doubles) * 8);
+    smem = size_t(pipe ? src.nstages : fused_stages()) * src.stage_doubles * 8;
   }
-  const int nt = pipe ? kPipeThreads : kind == KIND_FUSED ? (w == 1 ? FT<1>::v : FT<8>::v) : kThreads;
+  const int nt = pipe ? PipeBatched::threads : kind == KIND_FUSED ? (w == 1 ? FT<1>::v : FT<8>::v) : kThreads;
   const int64_t cap = resident_ctas(fn, smem, nt);
   const int64_t grid = total_tiles < cap ? total_tiles : cap;
   if (grid <= 0) return cudaSuccess;
@@ -1865,3 +2014,19 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
 }
 
 }  // namespace sgh
+
+#ifdef SGH_PIPE_TRACE
+// diagnostic build only: out == NULL -> arm tracing for launches with >= min_tiles
+// tiles; else copy the trace (160 CTAs x kTraceTiles x 8 stamps) out.
+extern "C" int64_t sgh_debug_pipe_trace(int64_t min_tiles, unsigned long long *out, int64_t cap) {
+  const int64_t n = 160 * sgh::kTraceTiles * 8;
+  if (!out) {
+    long long m = min_tiles;
+    cudaMemcpyToSymbol(sgh::g_ptrace_min, &m, sizeof m);
+    return n;
+  }
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, sgh::g_ptrace, sizeof(unsigned long long) * (size_t)std::min(n, cap));
+  return n;
+}
+#endif
