@@ -1420,7 +1420,7 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
 // with one / two BLOCKED axes; contiguous global runs), run by a
 // warp-specialised persistent CTA, one per SM, over a ring of NS SMEM stages
 // (and NS + 3 descriptor slots):
-//   warp 2        descriptors: per tile, finds its task (prefix table) and
+//   warp 1        descriptors: per tile, finds its task (prefix table) and
 //                 copies the task descriptor and the tile geometry into a
 //                 slot, up to NS + 3 tiles ahead (slot freed by the storer), so
 //                 these dependent global loads never sit on the load path;
@@ -1431,12 +1431,13 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
 //                 transaction count, plus 8-byte cp.async for the odd end
 //                 elements of runs at an 8-mod-16 phase
 //                 (cp.async.mbarrier.arrive.noinc);
-//   warps 3..     consumers (CFG::groups groups of CFG::cwarps warps, group g
+//   warps 2+G..   consumers (CFG::groups groups of CFG::cwarps warps, group g
 //                 takes tiles g, g + G, ..): wait for `full`, run the group's
 //                 axes in SMEM (fused_compute: the oracle's operation order,
 //                 bitwise), fence the generic-proxy writes for the async proxy
 //                 and arrive on `computed`;
-//   warp 1        storer: waits for `computed`, issues the bulk stores of the
+//   warps 2..1+G  storers, one per consumer group (group g's tiles): wait for
+//                 `computed`, issue the bulk stores of the
 //                 tile's written runs (cp.async.bulk shared -> global) and its
 //                 8-byte ends, waits until the copies have READ the stage and
 //                 arrives on `empty` (and frees the descriptor slot).
@@ -1446,8 +1447,13 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
 // (`aligned == 0`, lattice views with 8-byte copies) stay on k_fused.
 // The ring holds as many stages as fit the SM's shared memory (chosen per
 // launch from the group's largest tile: 3 stages of the 8192-point tiles,
-// more for smaller tiles), at most kPipeMaxStages.
+// more for smaller tiles), at most kPipeMaxStages.  (A ring of variable-size
+// tiles, each taking only the space it needs -- up to 6 C5 tiles in flight
+// instead of 3 -- measured slower: C5 155.9 vs 163, C4 270.8 vs 278.)
 constexpr int kPipeMaxStages = 6;
+#ifndef SGH_WAIT_HINT_NS
+#define SGH_WAIT_HINT_NS 20000
+#endif
 constexpr int kPipeDescAhead = 3;                    // descriptor slots beyond the stages
 constexpr int kPipeMaxDesc = kPipeMaxStages + kPipeDescAhead;
 // Consumer configuration <groups, warps per group>: one task per launch (a
@@ -1460,7 +1466,8 @@ struct PipeCfg {
   static constexpr int groups = G;
   static constexpr int cwarps = CW;
   static constexpr int ct = 32 * CW;              // threads per consumer group
-  static constexpr int threads = 96 + G * 32 * CW;
+  static constexpr int roles = 2 + G;           // producer, descriptors, one storer per group
+  static constexpr int threads = 32 * roles + G * 32 * CW;
 };
 #ifndef SGH_PIPE_BG
 #define SGH_PIPE_BG 2
@@ -1478,13 +1485,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)_
 __device__ __forceinline__ void mb_init(uint64_t *b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
+// The waiting warp sleeps in hardware until the phase completes or the time
+// hint (ns) runs out, instead of re-issuing try_wait (a spinning consumer
+// takes issue slots from the other consumer group on its SM sub-partitions).
 __device__ __forceinline__ void mb_wait(uint64_t *b, uint32_t parity) {
   uint32_t done;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
+        : "r"(smem_u32(b)), "r"(parity), "n"(SGH_WAIT_HINT_NS)
         : "memory");
   } while (!done);
 }
@@ -1606,7 +1616,11 @@ __device__ __forceinline__ unsigned long long gtime() {
 template <bool INV, class CFG>
 __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant__ Src src) {
   extern __shared__ __align__(128) double pipe_smem[];
-  __shared__ __align__(8) uint64_t bar_full[kPipeMaxStages], bar_computed[kPipeMaxStages],
+  // `computed` is a ring per consumer group (its j-th tile: slot j % NS), so
+  // each storer waits for the phases of its barriers strictly in order (two
+  // storers on one barrier could wait for a phase two ahead of the current
+  // one, which the parity test cannot tell from the previous one)
+  __shared__ __align__(8) uint64_t bar_full[kPipeMaxStages], bar_computed[CFG::groups][kPipeMaxStages],
       bar_empty[kPipeMaxStages], bar_dfull[kPipeMaxDesc], bar_dfree[kPipeMaxDesc];
   __shared__ __align__(16) Task s_task[kPipeMaxDesc];   // descriptor slot of tile k: k % ND
   __shared__ FusedTile s_tile[kPipeMaxDesc];
@@ -1616,7 +1630,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mb_init(&bar_full[s], 32);                    // one (cp.async-triggered) arrival per producer lane
-      mb_init(&bar_computed[s], 1);                 // the consumer group's leader
+      for (int g = 0; g < CFG::groups; ++g) mb_init(&bar_computed[g][s], 1);   // the group's leader
       mb_init(&bar_empty[s], 1);                    // the storer's lane 0
     }
     for (int s = 0; s < ND; ++s) {
@@ -1632,7 +1646,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
 #ifdef SGH_PIPE_TRACE
   const bool trace_on = total >= g_ptrace_min;
 #endif
-  if (warp == 2) {
+  if (warp == 1) {
     // ---------------------------------------------------------- descriptors
     // Looks up the task of each tile (a chain of dependent global loads: the
     // tile's task in the prefix table, then its descriptor) and publishes the
@@ -1705,13 +1719,17 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       mb_arrive_cpasync(&bar_full[s]);
       if (lane == 0) PTRACE(k, 2);
     }
-  } else if (warp == 1) {
-    // -------------------------------------------------------------- storer
-    int64_t q = q0;
-    for (int k = 0; q < total; ++k, q += qstep) {
+  } else if (warp < CFG::roles) {
+    // ------------------------------------------------------------- storers
+    // storer g stores the tiles of consumer group g (k = g, g + G, ..), so a
+    // group's finished tile never waits behind the other group's
+    const int g = warp - 2;
+    int64_t q = q0 + (int64_t)g * qstep;
+    for (int k = g; q < total; k += CFG::groups, q += CFG::groups * qstep) {
       const int s = k % NS;
       const int ds = k % ND;
-      mb_wait(&bar_computed[s], (k / NS) & 1);
+      const int j = k / CFG::groups;                // the group's j-th tile
+      mb_wait(&bar_computed[g][j % NS], (j / NS) & 1);
       const Task &T = s_task[ds];
       const FusedTile f = s_tile[ds];
       const double *sm = pipe_smem + (size_t)s * sd + f.par;
@@ -1745,8 +1763,8 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
     // ----------------------------------------------------------- consumers
     constexpr int kPipeCT = CFG::ct;
     constexpr int kPipeGroups = CFG::groups;
-    const int g = (warp - 3) / CFG::cwarps;
-    const GroupSync<kPipeCT> sy{(int)threadIdx.x - 96 - g * kPipeCT, 1 + g};
+    const int g = (warp - CFG::roles) / CFG::cwarps;
+    const GroupSync<kPipeCT> sy{(int)threadIdx.x - 32 * CFG::roles - g * kPipeCT, 1 + g};
     int64_t q = q0 + (int64_t)g * qstep;
     for (int k = g; q < total; k += kPipeGroups, q += kPipeGroups * qstep) {
       const int s = k % NS;
@@ -1760,7 +1778,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       sy.bar();
       if (sy.tid() == 0) {
         PTRACE(k, 5);
-        mb_arrive(&bar_computed[s]);
+        mb_arrive(&bar_computed[g][(k / CFG::groups) % NS]);
       }
     }
   }
