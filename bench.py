@@ -72,6 +72,20 @@ def d_eff(levels):
     return sum(1 for l in levels if l > 1)
 
 
+def plan_passes(sgh, members, inverse, fuse):
+    """HBM round trips per point of the library's plans (sgh_plan_describe:
+    points each phase writes, summed over the phases, / grid points)."""
+    import re
+
+    import sgh_inputs as si
+    pts = tot = 0
+    for lv in members:
+        tot += si.num_points(lv)
+        for m in re.finditer(r"points=(\d+)", sgh.plan_describe(lv, inverse=inverse, fuse=fuse)):
+            pts += int(m.group(1))
+    return pts / tot if tot else None
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -200,14 +214,63 @@ def main():
                     help="write the kernel keys of one timed step's launches (in order) to this JSON file "
                          "(pairs the launches of an ncu launch list with the bench's kernel keys: "
                          "scripts/ncu_traffic.py)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU work: every rank prints its RANK / WORLD_SIZE / LOCAL_RANK and the path it would "
+                         "time (CPU test of the multi-rank launch)")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: launch one rank per GPU "
+            "(torchrun --nproc-per-node N, or bench.py --gpus N without WORLD_SIZE)")
+        return 2
+    if args.dry_run:
+        return dry_run(args, rank, world, local_rank)
     if args.impl == "reference":
         return reference_arm(args, rank, world)
     return sgh_arm(args, rank, world, local_rank)
+
+
+def self_launch(n):
+    """--gpus N without a torchrun environment: start N ranks of this script
+    (one per GPU, rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank, world, local_rank):
+    """The rank layout and the path each rank would time, without a GPU."""
+    import sgh_inputs as si
+    members, ids, desc = workload(args.workload)
+    sizes = [si.num_points(l) for l in members]
+    info = {"dry_run": True, "rank": rank, "world_size": world, "local_rank": local_rank,
+            "impl": args.impl, "workload": args.workload}
+    if args.impl == "reference":
+        info["path"] = "oracle on host cores (rank 0 only)" if rank == 0 else "idle (rank > 0)"
+    elif args.workload == "C5" and world > 1:
+        part = si.lpt_partition(sizes, world)[rank]
+        info.update(path="C5 grids LPT-balanced by point count, batched transform, no data-path collective",
+                    grids=len(part), points=sum(sizes[i] for i in part))
+    elif args.workload == "C4" and world > 1:
+        import paper_1309_0392_b200 as sgh
+        b, e = sgh.shard_rows(members[0], world, rank)
+        info.update(path=("C4 sharded along x_d: " + ("halo + coarse-lattice all-gather" if args.sharded == "halo"
+                                                       else "NCCL all-to-all re-shard")),
+                    rows=[b, e])
+    else:
+        info.update(path="replica of the single-grid workload" if world > 1 else "single GPU",
+                    grids=len(members), points=sum(sizes))
+    print(json.dumps(info), flush=True)
+    return 0
 
 
 def reference_arm(args, rank, world):
@@ -245,7 +308,11 @@ def sgh_arm(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        import datetime
+        # communicator lines (rank / nranks) in the log, and no indefinite hang
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=600))
     members, ids, desc = workload(args.workload)
     sizes = [si.num_points(l) for l in members]
     sharded = args.workload == "C4" and world > 1
@@ -307,49 +374,56 @@ def sgh_arm(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local_rank)
-    clocks.start()
-    time.sleep(0.3)
-    barrier()
-    torch.cuda.synchronize()
-    n0 = sgh.launch_count()
-    sgh.profile_enable(True)
     # working sets below 1 GB (C2, C3, S10) would otherwise keep part of the
     # grid in the 126 MB L2 between the in-place steps: flush it by writing a
     # 256 MB scratch buffer before every step and time each step alone
     flush_l2 = 8 * my_points < 1e9
-    if flush_l2:
-        scratch = torch.empty((256 << 20) // 8, dtype=torch.float64, device=dev)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        for i in range(args.steps):
-            scratch.fill_(float(i))
-            evs[i][0].record(stream)
-            step()
-            evs[i][1].record(stream)
-    else:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    scratch = torch.empty((256 << 20) // 8, dtype=torch.float64, device=dev) if flush_l2 else None
+
+    def timed(k):
+        """k steps bracketed by a barrier + synchronize; device ms (events on the work stream)."""
+        barrier()
+        torch.cuda.synchronize()
+        if flush_l2:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+            for i in range(k):
+                scratch.fill_(float(i))
+                evs[i][0].record(stream)
+                step()
+                evs[i][1].record(stream)
+        else:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            for _ in range(k):
+                step()
+            ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return sum(a.elapsed_time(b) for a, b in evs) if flush_l2 else ev0.elapsed_time(ev1)
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    n0 = sgh.launch_count()
+    ms = timed(args.steps)                       # the headline: no per-launch events inside
     launches = sgh.launch_count() - n0
+    clk = clocks.stop()
+    # the roofline pass: the same K steps again, every launch bracketed by
+    # events on its stream (kernel durations and shares of the step)
+    sgh.profile_enable(True)
+    ms_prof = timed(args.steps)
     recs = sgh.profile_read()
+    sgh.profile_enable(False)
     if args.dump_launch_keys and rank == 0:
         per_step = len(recs) // max(1, args.steps)
         with open(args.dump_launch_keys, "w") as f:
-            json.dump({"workload": args.workload, "launches_per_step": per_step,
+            json.dump({"workload": args.workload, "inverse": bool(args.inverse), "launches_per_step": per_step,
                        "warmup": args.warmup, "keys": [r["kernel"] for r in recs[:per_step]],
                        "algorithmic_bytes": [r["bytes"] for r in recs[:per_step]]}, f)
-    sgh.profile_enable(False)
-    clk = clocks.stop()
-    ms = sum(a.elapsed_time(b) for a, b in evs) if flush_l2 else ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, ms_prof], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, ms_prof = float(t[0].item()), float(t[1].item())
     ms_step = ms / args.steps
     value = total_points / (ms_step * 1e-3) / 1e9
 
@@ -363,7 +437,7 @@ def sgh_arm(args, rank, world, local_rank):
         a["bytes"] += r["bytes"]
         a["launches"] += 1
     kern_tab = {k: {"launches_per_step": v["launches"] / args.steps,
-                    "share_of_step": v["ms"] / ms if ms else None,
+                    "share_of_step": v["ms"] / ms_prof if ms_prof else None,
                     "GBps": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] > 0 else None}
                 for k, v in per.items()}
     roof = None
@@ -373,21 +447,32 @@ def sgh_arm(args, rank, world, local_rank):
         achieved = a["bytes"] / (a["ms"] * 1e-3) / 1e9
         traffic = None
         tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tf):
-            try:
-                t = json.load(open(tf)).get(args.workload, {}).get(dom)
+        tkey = args.workload + ("_dehier" if args.inverse else "") + ("_per_axis" if args.per_axis else "")
+        if os.path.exists(tf) and not sharded:
+            try:   # ncu DRAM bytes of this kernel key, captured for this workload AND direction
+                t = json.load(open(tf)).get(tkey, {}).get(dom)
                 traffic = t["traffic_bytes_per_launch"] if isinstance(t, dict) else t
             except Exception:
                 traffic = None
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": a["bytes"] / a["launches"],
-                "avg_launch_ms": a["ms"] / a["launches"], "peak_source": peak_src}
+                "avg_launch_ms": a["ms"] / a["launches"], "peak_source": peak_src,
+                "timing": "per-launch CUDA events on the launching stream over a second timed pass of the "
+                          "same K steps (the headline pass has no per-launch events)",
+                "traffic_source": f"profiles/ncu_traffic.json[{tkey}] (ncu dram__bytes_read+write per launch)"}
     step_s = ms_step * 1e-3
+    ppp = None if sharded else plan_passes(sgh, my_members, args.inverse, not args.per_axis)
     model = {"per_axis_GBps": 16.0 * deff_pts / step_s / 1e9 if not sharded else None,
              "fused_GBps": 16.0 * my_points / step_s / 1e9,
              "per_axis_frac": (16.0 * deff_pts / step_s / 1e9) / peak if not sharded else None,
-             "note": "rank-0 view: 16 B/point/axis (per-axis model) and 16 B/point (fused floor)"}
+             "fused_floor_frac": (16.0 * my_points / step_s / 1e9) / peak,
+             "passes_per_point": ppp,
+             "plan_GBps": 16.0 * ppp * my_points / step_s / 1e9 if ppp else None,
+             "plan_frac": (16.0 * ppp * my_points / step_s / 1e9) / peak if ppp else None,
+             "profiled_ms_per_step": ms_prof / args.steps,
+             "note": "rank-0 view: 16 B/point/axis (per-axis model), 16 B/point (fused floor), and "
+                     "16 B x points written by the plan's phases (plan: HBM round trips per point)"}
 
     # e2e through the C ABI with host buffers
     e2e = None
@@ -431,7 +516,8 @@ def run_e2e(sgh, members, ids, dev, steps, world, rank):
     import sgh_inputs as si
     sizes = [si.num_points(l) for l in members]
     nbytes = 8 * sum(sizes)
-    avail = psutil.virtual_memory().available
+    # ranks of this node pin their buffers at the same time: each takes its share of the host RAM
+    avail = psutil.virtual_memory().available // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
     sub_m, sub_i = members, ids
     note = "all grids of this rank"
     if nbytes * 1.3 > avail:

@@ -73,6 +73,15 @@ typedef enum {
                                      groups (an axis split into aligned 2^t blocks +
                                      end points, its coarse lattice a later phase;
                                      SURVEY 8(a) a3.iii/a4); results are bitwise identical */
+#define SGH_FLAG_TABLE_RESIDENT 64u /* batched calls: the caller asserts that `workspace` still
+                                     holds, unmodified, the task table the library wrote there
+                                     in its previous batched call with the same grids, levels,
+                                     flags and stream; the library then skips the table upload
+                                     if that call's plan last uploaded to this workspace */
+#define SGH_FLAG_TWO_BLOCKED 32u  /* take the two-blocked plan (two adjacent axes in aligned
+                                     blocks + cross phases) wherever one
+                                     exists, instead of the cost model's choice: selects a
+                                     plan family (tests); results are bitwise identical */
 
 /* ------------------------------------------------------------ geometry */
 
@@ -84,7 +93,8 @@ int64_t sgh_num_points(const int32_t *levels, int32_t d);
 
 /* Hierarchize one grid in place (Alg. 1), axes 1..d in order.
  * grid: device pointer to N doubles (layout above).  levels: host int32[d].
- * No workspace: uses only in-place per-axis kernels. */
+ * Needs no workspace: every pass the planner picks (fused multi-axis tiles,
+ * blocked and two-blocked groups, per-axis kernels) runs in place. */
 sgh_status sgh_hierarchize(double *grid, const int32_t *levels, int32_t d, void *stream);
 
 /* Dehierarchize one grid in place (inverse base change; reading R9). */
@@ -240,10 +250,12 @@ sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_
  * sgh_profile_enable(0) stops (and clears).  sgh_profile_read fills up to
  * `capacity` records (waiting for their events) and returns the number of
  * records; out may be NULL to query the count.  kind: 0 FLAT_SLABS,
- * 1 FLAT_BLOCKS, 2 STRIDED, 3 REG, 4 FUSED.  bytes = 16 x points transformed. */
+ * 1 FLAT_BLOCKS, 2 STRIDED, 3 REG, 4 FUSED (k_fused), 5 gather, 6 scatter,
+ * 7 FUSED contiguous-run tiles on the pipelined bulk-copy kernel (k_fpipe).
+ * bytes = 16 x points transformed (gather / scatter: their own byte model). */
 typedef struct {
     int32_t kind;
-    int32_t level;    /* REG: pole level; STRIDED / FUSED: tile width W; else the task's l */
+    int32_t level;    /* REG: pole level; STRIDED / FUSED / kind 7: tile width W; else the task's l */
     int32_t inverse;  /* 1 for dehierarchization */
     int32_t variant;  /* FUSED: 0 dense, 1 BLOCKED tiles, 2 coarse-lattice views, 3 both */
     double bytes;     /* algorithmic bytes (one read + one write per point) */

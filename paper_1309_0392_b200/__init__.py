@@ -36,6 +36,8 @@ LIB_PATH = os.environ.get("SGH_LIB_PATH") or os.path.join(_HERE, "lib", "libsgh.
 FLAG_DEHIERARCHIZE = 1
 FLAG_PER_AXIS = 2
 FLAG_WHOLE_POLES = 4
+FLAG_TWO_BLOCKED = 32
+FLAG_TABLE_RESIDENT = 64
 FLAG_SCATTER = 8
 FLAG_ACCUMULATE = 16
 STATUS = {0: "SGH_OK", 1: "SGH_ERR_INVALID_ARGUMENT", 2: "SGH_ERR_CAPACITY", 3: "SGH_ERR_CUDA",
@@ -170,15 +172,18 @@ def num_points(levels: Sequence[int]) -> int:
 
 def _flags(inverse: bool, fuse=True) -> int:
     """fuse: True (planner's choice, blocked groups allowed), "whole" (fused
-    groups of whole poles only) or False (one HBM round trip per axis)."""
+    groups of whole poles only), "two_blocked" (the two-blocked plan wherever
+    one exists) or False (one HBM round trip per axis)."""
     if fuse == "whole":
         f = FLAG_WHOLE_POLES
+    elif fuse == "two_blocked":
+        f = FLAG_TWO_BLOCKED
     elif fuse is True:
         f = 0
     elif fuse is False:
         f = FLAG_PER_AXIS
     else:
-        raise ValueError(f"fuse must be True, False or 'whole', not {fuse!r}")
+        raise ValueError(f"fuse must be True, False, 'whole' or 'two_blocked', not {fuse!r}")
     return (FLAG_DEHIERARCHIZE if inverse else 0) | f
 
 
@@ -256,7 +261,8 @@ class _LaunchRecord(ctypes.Structure):
                 ("variant", ctypes.c_int32), ("bytes", ctypes.c_double), ("ms", ctypes.c_double)]
 
 
-KIND_NAMES = {0: "flat_slabs", 1: "flat_blocks", 2: "strided", 3: "reg", 4: "fused", 5: "gather", 6: "scatter"}
+KIND_NAMES = {0: "flat_slabs", 1: "flat_blocks", 2: "strided", 3: "reg", 4: "fused", 5: "gather", 6: "scatter",
+              7: "fpipe"}
 
 
 def profile_enable(on: bool = True):
@@ -272,7 +278,7 @@ def profile_read():
     n = int(lib.sgh_profile_read(ctypes.cast(buf, ctypes.c_void_p), n))
     out = []
     for r in buf[:n]:
-        name = KIND_NAMES.get(r.kind, str(r.kind)) + (f"<{r.level}>" if r.kind in (2, 3, 4) else "")
+        name = KIND_NAMES.get(r.kind, str(r.kind)) + (f"<{r.level}>" if r.kind in (2, 3, 4, 7) else "")
         name += {1: "B", 2: "L", 3: "BL"}.get(r.variant, "")   # blocked tiles / lattice views
         out.append({"kernel": name, "level": r.level, "inverse": bool(r.inverse), "bytes": r.bytes, "ms": r.ms,
                     "variant": r.variant})
@@ -331,6 +337,7 @@ class GridBatch:
         ws = max([batched_workspace_bytes(self.levels, inv, fz) for inv in (False, True) for fz in (False, True)]
                  + [self._util_ws_bytes(), 256])
         self.workspace = torch.empty((ws + 7) // 8, dtype=torch.float64, device=self.device)
+        self._table_key = None     # (flags, stream) of the task table the workspace holds
 
     def _util_ws_bytes(self):
         G = len(self.levels)
@@ -346,9 +353,17 @@ class GridBatch:
         if not self.levels:
             return self
         ws, wsb = self._ws()
+        st = _stream(stream)
+        key = (_flags(inverse, fuse), st.value)
+        # the workspace is this batch's own and only the library writes it: when
+        # the previous call used the same plan and stream, its task table is
+        # still there (fill / digest calls reuse the workspace and reset this)
+        flags = key[0] | (FLAG_TABLE_RESIDENT if key == self._table_key else 0)
+        self._table_key = None
         with torch.cuda.device(self.device):
             _check(lib.sgh_hierarchize_batched(self._ptrs, self._flat, self.d, len(self.levels),
-                                               _flags(inverse, fuse), ws, wsb, _stream(stream)))
+                                               flags, ws, wsb, st))
+        self._table_key = key
         return self
 
     def hierarchize(self, stream=None, fuse: bool = True):
@@ -361,6 +376,7 @@ class GridBatch:
         if not self.levels:
             return self
         ws, wsb = self._ws()
+        self._table_key = None                       # the fill's item list overwrites the workspace
         with torch.cuda.device(self.device):
             _check(lib.sgh_fill_uniform_batched(self._ptrs, self._sizes, self._ids, len(self.levels),
                                                 ctypes.c_uint64(seed), ws, wsb, _stream(stream)))
@@ -372,6 +388,7 @@ class GridBatch:
             return []
         out = (ctypes.c_uint64 * G)()
         ws, wsb = self._ws()
+        self._table_key = None                       # the digest's item list overwrites the workspace
         with torch.cuda.device(self.device):
             _check(lib.sgh_digest_batched(self._ptrs, self._sizes, G, out, ws, wsb, _stream(stream)))
         return [int(x) for x in out]

@@ -121,13 +121,13 @@ void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64
   // DRAM pages open), rows = 2^t + 1 within the SMEM budget
   static int wpref = -1;
   if (wpref < 0) {
-    const char *e = getenv("SGH_STRIDED_W");  // tuning experiment override
+    const char *e = tuning_env("SGH_STRIDED_W");  // tuning experiment override
     wpref = e ? atoi(e) : 256;
     if (wpref != 32 && wpref != 64 && wpref != 128 && wpref != 256) wpref = 128;
   }
   static int64_t tile_budget = -1;
   if (tile_budget < 0) {
-    const char *e = getenv("SGH_STRIDED_TILE");  // tuning experiment override (doubles)
+    const char *e = tuning_env("SGH_STRIDED_TILE");  // tuning experiment override (doubles)
     tile_budget = e ? atoll(e) : kStridedTileDoubles;
     if (tile_budget < 1024 || tile_budget > 13000) tile_budget = kStridedTileDoubles;
   }
@@ -170,7 +170,7 @@ void plan_axis(double *grid, const int32_t *levels, int d, int k, std::vector<Ta
 static int fused_budget() {
   static int T = -1;
   if (T < 0) {
-    const char *e = getenv("SGH_FUSED_T");  // tuning experiment override
+    const char *e = tuning_env("SGH_FUSED_T");  // tuning experiment override
     T = e ? atoi(e) : kFusedT;
     if (T < 1024 || T > 14336) T = kFusedT;
   }
@@ -182,7 +182,7 @@ static int fused_budget() {
 static int fused_budget_w1() {
   static int T = -1;
   if (T < 0) {
-    const char *e = getenv("SGH_FUSED_T1");
+    const char *e = tuning_env("SGH_FUSED_T1");
     T = e ? atoi(e) : kFusedT1;
     if (T < 1024 || T > 14336) T = kFusedT1;
   }
@@ -192,7 +192,7 @@ static int fused_budget_w1() {
 static int fused_wmax() {
   static int wmax = -1;
   if (wmax < 0) {
-    const char *e = getenv("SGH_FUSED_W");  // tuning experiment override (8..128)
+    const char *e = tuning_env("SGH_FUSED_W");  // tuning experiment override (8..128)
     wmax = e ? atoi(e) : 128;
     if (wmax != 8 && wmax != 16 && wmax != 32 && wmax != 64 && wmax != 128) wmax = 128;
   }
@@ -636,7 +636,7 @@ static double pass_cost(const std::vector<Task> &phases) {
 void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::vector<std::vector<Task>> &passes) {
   passes.clear();
   const bool fuse = (flags & SGH_FLAG_PER_AXIS) == 0;
-  const bool blocked_ok = fuse && (flags & SGH_FLAG_WHOLE_POLES) == 0 && getenv("SGH_NO_BLOCKED") == nullptr;
+  const bool blocked_ok = fuse && (flags & SGH_FLAG_WHOLE_POLES) == 0 && tuning_env("SGH_NO_BLOCKED") == nullptr;
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   const double kInf = 1e30;
   std::vector<double> cost(d + 1, kInf);
@@ -692,12 +692,11 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
   // two-blocked plan (grids with exactly two adjacent non-trivial axes)
   if (blocked_ok) {
     std::vector<Task> bestp;
-    // SGH_TWO_BLOCKED=force: take a two-blocked plan whenever one exists (tests)
-    const char *tb = getenv("SGH_TWO_BLOCKED");
-    double bc = (tb && std::strcmp(tb, "force") == 0) ? 1e30 : cost[d];
+    // SGH_FLAG_TWO_BLOCKED: take a two-blocked plan whenever one exists (tests)
+    double bc = (flags & SGH_FLAG_TWO_BLOCKED) ? 1e30 : cost[d];
     // SGH_TWO_BLOCKED_T=t1,t2 (experiments): only that pair of block levels
     int ft1 = -1, ft2 = -1;
-    if (const char *e = getenv("SGH_TWO_BLOCKED_T")) std::sscanf(e, "%d,%d", &ft1, &ft2);
+    if (const char *e = tuning_env("SGH_TWO_BLOCKED_T")) std::sscanf(e, "%d,%d", &ft1, &ft2);
     for (int a = 0; a + 1 < d; ++a)
       for (int t1 = 2; t1 < levels[a]; ++t1)
         for (int t2 = 2; t2 < levels[a + 1]; ++t2) {
@@ -821,7 +820,7 @@ static sgh_status transform_single(double *grid, const int32_t *levels, int32_t 
       if (inv) std::reverse(phases.begin(), phases.end());   // coarse lattice first (H2)
       for (const Task &t : phases) {
         cudaError_t e = launch_single(t, inv, s);
-        if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+        if (e != cudaSuccess) return cuda_fail(e, pipe_task(t) ? "kernel launch (k_fpipe)" : "kernel launch");
         count_launch();
       }
     }
@@ -861,6 +860,7 @@ struct BatchedPlan {
   std::vector<int64_t> prefix;
   std::vector<Segment> segs;
   std::vector<unsigned char> image;   // the device table image (built once per cached plan)
+  void *resident_ws = nullptr;        // the workspace this plan's table was last uploaded to
   size_t table_bytes() const {
     return (tasks.size() * sizeof(Task) + 255) / 256 * 256 + prefix.size() * sizeof(int64_t);
   }
@@ -887,7 +887,7 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
     for (size_t j = 0; j < maxp; ++j) {
       // group phase j of all grids by kernel instance (kind, and l for REG)
       // SGH_SPLIT_VARIANTS=1 (profiling): dense / blocked / lattice FUSED tasks in separate launches
-      static const bool split = getenv("SGH_SPLIT_VARIANTS") != nullptr;
+      static const bool split = tuning_env("SGH_SPLIT_VARIANTS") != nullptr;
       std::map<std::tuple<int, int, int, int>, std::vector<const Task *>> groups;
       for (int64_t g = 0; g < num_grids; ++g)
         if (j < per[g].size()) {
@@ -928,9 +928,23 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
 
 size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
                            uint32_t flags) {
+  // the size depends on the levels and flags only: cached (the e2e host path
+  // asks for every transfer chunk on every call)
+  static std::mutex mu;
+  static std::map<std::pair<std::vector<int32_t>, uint32_t>, size_t> memo;
+  auto key = std::make_pair(std::vector<int32_t>(levels, levels + num_grids * d), (flags & kPlanFlags) | (uint32_t(d) << 24));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
   BatchedPlan P;
-  build_batched_plan(grids, levels, d, num_grids, flags, P);
-  return P.segs.empty() ? 0 : P.table_bytes();
+  build_batched_plan(grids, levels, d, num_grids, flags & kPlanFlags, P);
+  const size_t b = P.segs.empty() ? 0 : P.table_bytes();
+  std::lock_guard<std::mutex> lk(mu);
+  if (memo.size() > 4096) memo.clear();
+  memo.emplace(std::move(key), b);
+  return b;
 }
 
 static sgh_status validate_batch(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
@@ -956,8 +970,12 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   // Plan cache: the combination grids are transformed every iteration of the
   // combination technique with the same pointers and levels, and planning
-  // 4,255 grids takes tens of ms of host time -- reuse the plan (the table is
-  // still uploaded on every call, so the workspace contract is unchanged).
+  // 4,255 grids takes tens of ms of host time -- reuse the plan.  The table is
+  // uploaded on every call unless SGH_FLAG_TABLE_RESIDENT says the workspace
+  // still holds it.  Up to kCacheMax plans (the e2e host path runs one plan
+  // per transfer chunk: ~640 for C5).
+  const uint32_t pflags = flags & kPlanFlags;
+  constexpr size_t kCacheMax = 2048;
   struct CacheEntry {
     std::vector<int32_t> levels;
     std::vector<double *> grids;
@@ -972,7 +990,7 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
     std::lock_guard<std::mutex> lk(cache_mu);
     for (size_t i = 0; i < cache.size(); ++i) {
       const CacheEntry &c = cache[i];
-      if (c.flags == flags && c.d == d && c.grids.size() == size_t(num_grids) &&
+      if (c.flags == pflags && c.d == d && c.grids.size() == size_t(num_grids) &&
           std::equal(c.grids.begin(), c.grids.end(), grids) &&
           std::equal(c.levels.begin(), c.levels.end(), levels)) {
         plan = c.plan;
@@ -982,16 +1000,16 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
   }
   if (!plan) {
     plan = std::make_shared<BatchedPlan>();
-    build_batched_plan(grids, levels, d, num_grids, flags, *plan);
+    build_batched_plan(grids, levels, d, num_grids, pflags, *plan);
     CacheEntry c;
     c.levels.assign(levels, levels + num_grids * d);
     c.grids.assign(grids, grids + num_grids);
-    c.flags = flags;
+    c.flags = pflags;
     c.d = d;
     c.plan = plan;
     std::lock_guard<std::mutex> lk(cache_mu);
     cache.push_back(std::move(c));
-    if (cache.size() > 4) cache.erase(cache.begin());
+    if (cache.size() > kCacheMax) cache.erase(cache.begin());
   }
   const BatchedPlan &P = *plan;
   if (P.segs.empty()) return SGH_OK;
@@ -1007,14 +1025,22 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
     std::memcpy(host.data(), P.tasks.data(), P.tasks.size() * sizeof(Task));
     std::memcpy(host.data() + prefix_base, P.prefix.data(), P.prefix.size() * sizeof(int64_t));
   }
-  st = staged_upload(workspace, plan->image.data(), bytes, s);
-  if (st != SGH_OK) return st;
+  if (!((flags & SGH_FLAG_TABLE_RESIDENT) && plan->resident_ws == workspace)) {
+    st = staged_upload(workspace, plan->image.data(), bytes, s);
+    if (st != SGH_OK) return st;
+    plan->resident_ws = workspace;
+  }
   const Task *d_tasks = reinterpret_cast<const Task *>(workspace);
   const int64_t *d_prefix = reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + prefix_base);
   for (const Segment &sg : P.segs) {
     cudaError_t e = launch_table(sg.kind, sg.l, sg.w, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off, sg.ntasks,
                                  sg.tiles, sg.smem, sg.points, s, sg.variant, sg.pipe);
-    if (e != cudaSuccess) return cuda_fail(e, "grouped kernel launch");
+    if (e != cudaSuccess) {
+      char where[160];
+      std::snprintf(where, sizeof where, "grouped kernel launch (kind %d, W %d, l %d, variant %d, %s, %d tasks)",
+                    sg.kind, sg.w, sg.l, sg.variant, sg.pipe ? "k_fpipe" : "k_fused/per-axis", sg.ntasks);
+      return cuda_fail(e, where);
+    }
     count_launch();
   }
   return SGH_OK;

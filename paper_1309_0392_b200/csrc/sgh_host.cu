@@ -23,7 +23,7 @@ namespace sgh {
 static size_t chunk_bytes() {
   static size_t b = 0;
   if (!b) {
-    const char *e = getenv("SGH_E2E_CHUNK_MB");
+    const char *e = tuning_env("SGH_E2E_CHUNK_MB");
     const long mb = e ? atol(e) : 64;   // measured on C5: 64 MB 5.36, 128 MB 5.23, 512 MB 5.14, 2 GB 4.63 Gpoints/s
     b = size_t(mb >= 16 && mb <= 8192 ? mb : 64) << 20;
   }

@@ -1203,9 +1203,41 @@ __device__ __forceinline__ void fused_issue(const Task &T, const FusedTile &f, d
   else fused_load_rows<(W == 1 || W >= 64 ? 8 : W)>(stage + f.par, f.g, T.S, f.par, T.P, f.wc);
 }
 
+// -DSGH_PIPE_TRACE (diagnostic build only): %globaltimer stamps of the first
+// kTraceTiles tiles of every CTA of launches with >= g_ptrace_min tiles, read
+// back with sgh_debug_pipe_trace().  Events per tile: 0 descriptor published,
+// 1 producer starts issuing, 2 loads issued, 3 consumer starts waiting,
+// 4 data ready, 5 computed, 6 stores issued, 7 stores have read the stage,
+// 8 + j: axis j of the group transformed (j < 8); words 16..23 describe the
+// tile (m, levels packed 8 bits each, bj, bt, bt2, P, units, W).
+#ifdef SGH_PIPE_TRACE
+constexpr int kTraceTiles = 64;
+__device__ unsigned long long g_ptrace[160 * kTraceTiles * 24];
+__device__ long long g_ptrace_min = 1ll << 62;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PTRACE(k, ev) PTRACE_IF(trace_on, k, ev)
+#define PTRACE_IF(on, k, ev)                                                                   \
+  do {                                                                                         \
+    if ((on) && (k) < kTraceTiles && blockIdx.x < 160)                                         \
+      g_ptrace[((size_t)blockIdx.x * kTraceTiles + (k)) * 24 + (ev)] = gtime();                \
+  } while (0)
+#else
+#define PTRACE(k, ev) \
+  do {                \
+  } while (0)
+#define PTRACE_IF(on, k, ev) \
+  do {                       \
+  } while (0)
+#endif
+
 // all axes of the group on a staged tile (Alg. 1's axis loop, in SMEM)
 template <bool INV, int W, int NT = FT<W>::v, class SY = CtaSync>
-__device__ __forceinline__ void fused_compute(const Task &T, const FusedTile &f, double *sm, const SY sy = SY()) {
+__device__ __forceinline__ void fused_compute(const Task &T, const FusedTile &f, double *sm, const SY sy = SY(),
+                                              int trace_k = -1) {
   constexpr int RS = (W == 1) ? 1 : W + 1;
   const int rows_total = f.units * T.P;
   const bool blocked = T.bj >= 0 && T.bt < T.gl[T.bj];
@@ -1231,12 +1263,14 @@ __device__ __forceinline__ void fused_compute(const Task &T, const FusedTile &f,
       // dehierarchization of a two-blocked tile: the second axis' end rows are final
       fused_axis_block<INV, W, NT, SY>(sm, RS, T.bt, R, fR, full ? T.gOk[j] : rows_total / (T.ej * R), f.lo_ok,
                                        f.hi_ok, full ? &fnp : nullptr, INV && T.bt2 >= 0, sy);
+      if (sy.tid() == 0 && j < 8) PTRACE_IF(trace_k >= 0, trace_k, 8 + j);
       continue;
     }
     if (T.bt2 >= 0 && j == T.bj + 1) {              // second blocked axis
       fused_axis_block<INV, W, NT, SY>(sm, RS, T.bt2, R, fR,
                                        full ? T.gOk[j] : rows_total / (((1 << T.bt2) + 1) * R), f.lo2_ok, f.hi2_ok,
                                        full ? &fnp : nullptr, false, sy);
+      if (sy.tid() == 0 && j < 8) PTRACE_IF(trace_k >= 0, trace_k, 8 + j);
       continue;
     }
     const int n = (T.bj == j) ? T.ej : (1 << l) - 1;
@@ -1250,6 +1284,7 @@ __device__ __forceinline__ void fused_compute(const Task &T, const FusedTile &f,
     const int Ok = full ? T.gOk[j] : rows_total / (n * R);
     if (R == 1) fused_axis<INV, W, true, NT, SY>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr, sy);
     else fused_axis<INV, W, false, NT, SY>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr, sy);
+    if (sy.tid() == 0 && j < 8) PTRACE_IF(trace_k >= 0, trace_k, 8 + j);
   }
 }
 
@@ -1451,6 +1486,7 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
 // tiles, each taking only the space it needs -- up to 6 C5 tiles in flight
 // instead of 3 -- measured slower: C5 155.9 vs 163, C4 270.8 vs 278.)
 constexpr int kPipeMaxStages = 6;
+
 #ifndef SGH_WAIT_HINT_NS
 #define SGH_WAIT_HINT_NS 20000
 #endif
@@ -1588,31 +1624,6 @@ __device__ __forceinline__ int warp_find_task(const Src &src, int idx, int64_t q
   }
 }
 
-// -DSGH_PIPE_TRACE (diagnostic build only): %globaltimer stamps of the first
-// kTraceTiles tiles of every CTA of launches with >= g_ptrace_min tiles, read
-// back with sgh_debug_pipe_trace().  Events per tile: 0 descriptor published,
-// 1 producer starts issuing, 2 loads issued, 3 consumer starts waiting,
-// 4 data ready, 5 computed, 6 stores issued, 7 stores have read the stage.
-#ifdef SGH_PIPE_TRACE
-constexpr int kTraceTiles = 64;
-__device__ unsigned long long g_ptrace[160 * kTraceTiles * 8];
-__device__ long long g_ptrace_min = 1ll << 62;
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define PTRACE(k, ev)                                                                          \
-  do {                                                                                         \
-    if (trace_on && (k) < kTraceTiles && blockIdx.x < 160)                                     \
-      g_ptrace[((size_t)blockIdx.x * kTraceTiles + (k)) * 8 + (ev)] = gtime();                 \
-  } while (0)
-#else
-#define PTRACE(k, ev) \
-  do {                \
-  } while (0)
-#endif
-
 template <bool INV, class CFG>
 __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant__ Src src) {
   extern __shared__ __align__(128) double pipe_smem[];
@@ -1682,6 +1693,16 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       if (lane == 0) s_tile[ds] = f;
       __syncwarp();
       if (lane == 0) PTRACE(k, 0);
+#ifdef SGH_PIPE_TRACE
+      if (lane == 0 && trace_on && k < kTraceTiles && blockIdx.x < 160) {
+        unsigned long long *w = &g_ptrace[((size_t)blockIdx.x * kTraceTiles + k) * 24 + 16];
+        const Task &TT = s_task[ds];
+        unsigned long long lv = 0;
+        for (int j = 0; j < TT.m && j < 8; ++j) lv |= (unsigned long long)(uint8_t)TT.gl[j] << (8 * j);
+        w[0] = TT.m; w[1] = lv; w[2] = (unsigned long long)(long long)TT.bj; w[3] = (unsigned long long)(long long)TT.bt;
+        w[4] = (unsigned long long)(long long)TT.bt2; w[5] = TT.P; w[6] = f.units; w[7] = TT.skipmask;
+      }
+#endif
       mb_arrive(&bar_dfull[ds]);
     }
   } else if (warp == 0) {
@@ -1719,6 +1740,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       mb_arrive_cpasync(&bar_full[s]);
       if (lane == 0) PTRACE(k, 2);
     }
+    cp_async_wait<0>();                            // no cp.async outstanding when the warp exits
   } else if (warp < CFG::roles) {
     // ------------------------------------------------------------- storers
     // storer g stores the tiles of consumer group g (k = g, g + G, ..), so a
@@ -1734,24 +1756,26 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       const FusedTile f = s_tile[ds];
       const double *sm = pipe_smem + (size_t)s * sd + f.par;
       const PipeRuns runs(T, f, true);
-      for (int i = lane; i < runs.count; i += 32) {
-        const double *sp = sm + runs.lo(i);
-        double *gp = runs.g(i);
-        const int len = runs.len;
-        const int head = phase8(gp);
-        const int pairs = (len - head) >> 1;
-        const int last = head + 2 * pairs;
-        if (head) __stcg(gp, sp[0]);
-        if (last < len) __stcg(gp + last, sp[last]);
-        if (pairs > 0)
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gp + head),
-                       "r"(smem_u32(sp + head)), "r"(pairs * 16)
-                       : "memory");
+      {
+        for (int i = lane; i < runs.count; i += 32) {
+          const double *sp = sm + runs.lo(i);
+          double *gp = runs.g(i);
+          const int len = runs.len;
+          const int head = phase8(gp);
+          const int pairs = (len - head) >> 1;
+          const int last = head + 2 * pairs;
+          if (head) __stcg(gp, sp[0]);
+          if (last < len) __stcg(gp + last, sp[last]);
+          if (pairs > 0)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gp + head),
+                         "r"(smem_u32(sp + head)), "r"(pairs * 16)
+                         : "memory");
+        }
+        bulk_commit();
+        if (lane == 0) PTRACE(k, 6);
+        bulk_wait_read();                           // this lane's copies have read the stage
+        __syncwarp();
       }
-      bulk_commit();
-      if (lane == 0) PTRACE(k, 6);
-      bulk_wait_read();                             // this lane's copies have read the stage
-      __syncwarp();
       if (lane == 0) {
         PTRACE(k, 7);
         mb_arrive(&bar_empty[s]);
@@ -1773,7 +1797,12 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       if (sy.tid() == 0) PTRACE(k, 4);
       const Task &T = s_task[k % ND];
       const FusedTile f = s_tile[k % ND];
-      fused_compute<INV, 1, kPipeCT, GroupSync<kPipeCT>>(T, f, pipe_smem + (size_t)s * sd + f.par, sy);
+#ifdef SGH_PIPE_TRACE
+      const int tk = trace_on ? k : -1;
+#else
+      const int tk = -1;
+#endif
+      fused_compute<INV, 1, kPipeCT, GroupSync<kPipeCT>>(T, f, pipe_smem + (size_t)s * sd + f.par, sy, tk);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // SMEM results -> the bulk stores
       sy.bar();
       if (sy.tid() == 0) {
@@ -1853,12 +1882,13 @@ __global__ void __launch_bounds__(kThreads) k_reg(const __grid_constant__ Src sr
 
 // ------------------------------------------------------------ host launchers
 using KernelFn = void (*)(Src);
+constexpr int kProfKindPipe = 7;                 // sgh_launch_record.kind of k_fpipe launches
 
 // FUSED pipeline depth: 1 (default) or 2 stages (tuning override SGH_FUSED_STAGES)
 int fused_stages() {
   static int st = -1;
   if (st < 0) {
-    const char *e = getenv("SGH_FUSED_STAGES");
+    const char *e = tuning_env("SGH_FUSED_STAGES");
     st = (e && atoi(e) == 2) ? 2 : 1;
   }
   return st;
@@ -1998,8 +2028,8 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
   ProfToken tok = prof_begin(stream);
   fn<<<(unsigned)grid, nt, smem, stream>>>(src);
   cudaError_t e = cudaGetLastError();
-  prof_end(tok, task.kind, task.kind == KIND_FUSED || task.kind == KIND_STRIDED ? task.W : task.l, inv,
-           16.0 * task_points(task), stream, task_variant(task));
+  prof_end(tok, pipe ? kProfKindPipe : task.kind, task.kind == KIND_FUSED || task.kind == KIND_STRIDED ? task.W : task.l,
+           inv, 16.0 * task_points(task), stream, task_variant(task));
   return e;
 }
 
@@ -2027,7 +2057,8 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
   ProfToken tok = prof_begin(stream);
   fn<<<(unsigned)grid, nt, smem, stream>>>(src);
   cudaError_t e = cudaGetLastError();
-  prof_end(tok, kind, kind == KIND_FUSED || kind == KIND_STRIDED ? w : l, inv, 16.0 * points, stream, variant);
+  prof_end(tok, pipe ? kProfKindPipe : kind, kind == KIND_FUSED || kind == KIND_STRIDED ? w : l, inv, 16.0 * points,
+           stream, variant);
   return e;
 }
 
@@ -2035,9 +2066,9 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
 
 #ifdef SGH_PIPE_TRACE
 // diagnostic build only: out == NULL -> arm tracing for launches with >= min_tiles
-// tiles; else copy the trace (160 CTAs x kTraceTiles x 8 stamps) out.
+// tiles; else copy the trace (160 CTAs x kTraceTiles x 24 words) out.
 extern "C" int64_t sgh_debug_pipe_trace(int64_t min_tiles, unsigned long long *out, int64_t cap) {
-  const int64_t n = 160 * sgh::kTraceTiles * 8;
+  const int64_t n = 160 * sgh::kTraceTiles * 24;
   if (!out) {
     long long m = min_tiles;
     cudaMemcpyToSymbol(sgh::g_ptrace_min, &m, sizeof m);

@@ -126,6 +126,19 @@ size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t 
                            uint32_t flags);
 // flags: SGH_FLAG_DEHIERARCHIZE / SGH_FLAG_PER_AXIS / SGH_FLAG_WHOLE_POLES (sgh.h)
 void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::vector<std::vector<Task>> &passes);
-constexpr uint32_t kKnownFlags = SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS | SGH_FLAG_WHOLE_POLES;
+constexpr uint32_t kKnownFlags =
+    SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS | SGH_FLAG_WHOLE_POLES | SGH_FLAG_TWO_BLOCKED | SGH_FLAG_TABLE_RESIDENT;
+// flags that select the plan (the plan cache key)
+constexpr uint32_t kPlanFlags = kKnownFlags & ~uint32_t(SGH_FLAG_TABLE_RESIDENT);
+
+// Tuning knobs (experiments only): read from the environment in a -DSGH_TUNING
+// build, compile-time defaults otherwise -- the default library reads no
+// environment variable.
+#ifdef SGH_TUNING
+#include <cstdlib>
+inline const char *tuning_env(const char *name) { return std::getenv(name); }
+#else
+inline const char *tuning_env(const char *) { return nullptr; }
+#endif
 
 }  // namespace sgh

@@ -4,7 +4,7 @@ roofline "traffic" field (profiles/ncu_traffic.json).
   python scripts/ncu_traffic.py launches.csv keys.json [profiles/ncu_traffic.json]
 
 launches.csv: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
---csv --log-file launches.csv -k regex:"k_(fused|flat|strided|reg)" -s <warmup x launches/step>
+--csv --log-file launches.csv -k regex:"k_(fused|flat|strided|reg|fpipe)" -s <warmup x launches/step>
 -c <launches/step> python bench.py ...` (one step's transform launches, in order);
 keys.json: `python bench.py ... --dump-launch-keys keys.json` (the same step's kernel keys, in order).
 Each key gets the average dram read + write bytes per launch."""
@@ -58,7 +58,7 @@ def main():
             db = json.load(open(dst))
         except Exception:  # noqa: BLE001
             db = {}
-        db[K["workload"]] = res
+        db[K["workload"] + ("_dehier" if K.get("inverse") else "")] = res
         json.dump(db, open(dst, "w"), indent=1, sort_keys=True)
 
 

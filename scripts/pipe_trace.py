@@ -30,7 +30,10 @@ run()
 torch.cuda.synchronize()
 buf = np.zeros(n, dtype=np.uint64)
 f(0, buf.ctypes.data, n)
-T = buf.reshape(160, 64, 8).astype(np.float64)
+R = buf.reshape(160, 64, 24)
+T = R[:, :, :8].astype(np.float64)
+A = R[:, :, 8:16].astype(np.float64)
+I = R[:, :, 16:24]
 ok = (T > 0).all(axis=2)
 print("traced tiles:", int(ok.sum()))
 T = T[:, 8:56]                     # skip ramp-up / tail
@@ -47,3 +50,32 @@ for name, a, b2 in rows:
 # per-CTA tile period
 per = np.diff(T[:, :, 2], axis=1)[ok[:, 1:] & ok[:, :-1]] / 1000.0
 print(f"{'tile period (producer issue to issue)':42s} median {np.median(per):7.2f} us")
+
+# per-axis transform time by (axis level, role) over the traced tiles
+from collections import defaultdict  # noqa: E402
+acc = defaultdict(list)
+tiles = defaultdict(list)
+T = R[:, :, :8].astype(np.float64)
+for c in range(160):
+    for k in range(8, 56):
+        if not (R[c, k, :8] > 0).all():
+            continue
+        m = int(I[c, k, 0])
+        lv = [(int(I[c, k, 1]) >> (8 * j)) & 255 for j in range(m)]
+        bj, bt, bt2 = (np.int64(I[c, k, 2]), np.int64(I[c, k, 3]), np.int64(I[c, k, 4]))
+        P, units = int(I[c, k, 5]), int(I[c, k, 6])
+        t_prev = T[c, k, 4]
+        key = (tuple(lv), int(bj), int(bt), int(bt2))
+        tiles[key].append((T[c, k, 5] - T[c, k, 4]) / 1000.0)
+        for j in range(m):
+            if A[c, k, j] > 0:
+                role = "blocked" if (j == bj and bt < lv[j]) or (bt2 >= 0 and j == bj + 1) else "whole"
+                acc[(lv[j], role)].append((A[c, k, j] - t_prev) / 1000.0)
+                t_prev = A[c, k, j]
+print("per-axis time (us) by (level, role): median, count")
+for key in sorted(acc):
+    x = np.array(acc[key])
+    print(f"  l={key[0]:2d} {key[1]:8s} median {np.median(x):6.2f}  n={len(x)}")
+print("tile compute (us) by task shape (levels, bj, bt, bt2): top 12 by count")
+for key, v in sorted(tiles.items(), key=lambda kv: -len(kv[1]))[:12]:
+    print(f"  {key}  median {np.median(v):6.2f}  n={len(v)}")

@@ -186,16 +186,32 @@ def test_plan_two_blocked_available():
     assert N <= sum(x for _, _, x in q[0]) < 1.06 * N
 
 
-def test_plan_two_blocked_forced(monkeypatch):
-    """SGH_TWO_BLOCKED=force selects the two-blocked plan wherever one exists
-    (how the GPU parity tests exercise it)."""
-    monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
+def test_plan_two_blocked_forced():
+    """SGH_FLAG_TWO_BLOCKED (fuse="two_blocked") selects the two-blocked plan
+    wherever one exists (how the GPU parity tests exercise it)."""
     for lv in [(14, 13), (10, 10), (11, 8), (1, 1, 11, 9)]:
-        p = _plan_passes(lv)
+        p = _plan_passes(lv, fuse="two_blocked")
         assert len(p) == 1 and int(p[0][0][1]["bt2"]) >= 2, lv
         N = si.num_points(lv)
         assert p[0][0][2] < N <= sum(x for _, _, x in p[0])
-    assert len(_plan_passes((14, 13), inverse=True)) == 1
+    assert len(_plan_passes((14, 13), inverse=True, fuse="two_blocked")) == 1
+
+
+def test_library_reads_no_environment():
+    """the default library reads no environment variable.  The only
+    getenv in csrc/ is tuning_env()'s, compiled in a -DSGH_TUNING build only
+    (experiments); the default build's tuning_env returns NULL.  (The
+    statically linked CUDA runtime's own getenv calls are not ours.)"""
+    import glob
+    import re
+    hits = []
+    for path in glob.glob(os.path.join(os.path.dirname(sgh.__file__), "csrc", "*")):
+        src = open(path).read()
+        for m in re.finditer(r"\bgetenv\s*\(", src):
+            hits.append((os.path.basename(path), src[:m.start()]))
+    assert len(hits) == 1 and hits[0][0] == "sgh_plan.hpp", [h[0] for h in hits]
+    before = hits[0][1]
+    assert before.rfind("#ifdef SGH_TUNING") > before.rfind("#endif"), "getenv outside #ifdef SGH_TUNING"
 
 
 @pytest.mark.parametrize("d,n", [(1, 9), (2, 7), (3, 8), (4, 22), (5, 9)])

@@ -234,38 +234,36 @@ TWO_BLOCKED_SHAPES = [(10, 10), (11, 8), (13, 6), (12, 7), (1, 1, 11, 9), (12, 1
 
 
 @pytest.mark.parametrize("levels", TWO_BLOCKED_SHAPES, ids=str)
-def test_two_blocked_bitwise(sgh, levels, monkeypatch):
+def test_two_blocked_bitwise(sgh, levels):
     """The two-blocked plan (SURVEY 8(a) a4 block scheme: tiles fine along both
     axes, then the cross phases) forced on 2-D grids: bitwise vs the oracle."""
-    monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
     N = si.num_points(levels)
     u = si.fill_uniform(N, grid_id=N % 977)
     want = oracle.hierarchize(u.copy(), levels)
-    assert_bitwise(gpu_transform(sgh, u, levels), want)
+    assert_bitwise(gpu_transform(sgh, u, levels, fuse="two_blocked"), want)
 
 
 @pytest.mark.parametrize("levels", TWO_BLOCKED_SHAPES, ids=str)
-def test_two_blocked_dehier_bitwise(sgh, levels, monkeypatch):
+def test_two_blocked_dehier_bitwise(sgh, levels):
     """Dehierarchization with the two-blocked plan (a-lattice of every row,
     fine-a of the coarse-b rows, b-lattice, the tiles with their b-end rows
     untouched, fine-b of the coarse-a columns) forced on 2-D grids: bitwise vs
     the oracle, also for the round trip (the oracle's own round trip, which
     is not the identity bit for bit)."""
-    monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
     N = si.num_points(levels)
     a = si.fill_uniform(N, grid_id=N % 983)
     want = oracle.dehierarchize(a.copy(), levels)
-    assert_bitwise(gpu_transform(sgh, a, levels, inverse=True), want)
+    assert_bitwise(gpu_transform(sgh, a, levels, inverse=True, fuse="two_blocked"), want)
     h = oracle.hierarchize(a.copy(), levels)
-    assert_bitwise(gpu_transform(sgh, h, levels, inverse=True), oracle.dehierarchize(h.copy(), levels))
+    assert_bitwise(gpu_transform(sgh, h, levels, inverse=True, fuse="two_blocked"),
+                   oracle.dehierarchize(h.copy(), levels))
 
 
-def test_two_blocked_c4_golden(sgh, monkeypatch):
-    monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
+def test_two_blocked_c4_golden(sgh):
     c = SD["configs"]["C4"]
     g = torch.empty(si.num_points(c["levels"]), dtype=torch.float64, device="cuda")
     sgh.fill_uniform(g, SD["seed"], c["grid_id"])
-    sgh.hierarchize(g, c["levels"])
+    sgh.transform(g, c["levels"], fuse="two_blocked")
     assert sgh.digest(g) == int(c["hierarchized"], 16)
 
 
@@ -291,6 +289,30 @@ def _batch_check(sgh, members, ids, inverse=False, fuse=True):
         want = oracle.fill_uniform(si.num_points(lv), SD["seed"], gid)
         (oracle.dehierarchize if inverse else oracle.hierarchize)(want, lv)
         assert_bitwise(v.cpu().numpy(), want)
+
+
+def test_batched_table_resident_sequences(sgh):
+    """Repeated batched calls skip the task-table upload when the batch's own
+    workspace still holds the same plan's table (SGH_FLAG_TABLE_RESIDENT):
+    hier, hier (resident), dehier, dehier (resident), a digest (reuses the
+    workspace), hier, whole-pole hier -- every step bitwise vs the oracle
+    applying the same sequence."""
+    members = [(3, 4, 2), (6, 5, 1), (2, 2, 2), (7, 3, 3), (1, 9, 2), (5, 5, 5)]
+    ids = list(range(len(members)))
+    b = sgh.GridBatch(members, grid_ids=ids)
+    b.fill_uniform(SD["seed"])
+    want = [oracle.fill_uniform(si.num_points(lv), SD["seed"], g) for lv, g in zip(members, ids)]
+    for op, fuse in [("h", True), ("h", True), ("d", True), ("d", True), ("digest", None), ("h", True),
+                     ("h", "whole"), ("d", "whole")]:
+        if op == "digest":
+            b.digests()
+            continue
+        b.transform(op == "d", fuse=fuse)
+        torch.cuda.synchronize()
+        for w, lv in zip(want, members):
+            (oracle.dehierarchize if op == "d" else oracle.hierarchize)(w, lv)
+        for v, w in zip(b.views, want):
+            assert_bitwise(v.cpu().numpy(), w)
 
 
 @pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
@@ -474,7 +496,7 @@ def test_gather_closed_form_c5_subset(sgh):
 
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("SGH_FUZZ_SEEDS", "6"))))
-def test_random_shapes_fuzz(sgh, seed, monkeypatch):
+def test_random_shapes_fuzz(sgh, seed):
     """Planner fuzz: random level vectors (d = 1..6, up to ~2 M points) under every
     plan family -- automatic, whole-pole fusion only, per axis, forced two-blocked
     -- hierarchize and dehierarchize, bitwise vs the oracle.  SGH_FUZZ_SEEDS
@@ -494,7 +516,5 @@ def test_random_shapes_fuzz(sgh, seed, monkeypatch):
         for fuse in (True, "whole", False):
             assert_bitwise(gpu_transform(sgh, u, lv, fuse=fuse, guard=64), want_h)
             assert_bitwise(gpu_transform(sgh, u, lv, inverse=True, fuse=fuse, guard=64), want_d)
-        monkeypatch.setenv("SGH_TWO_BLOCKED", "force")
-        assert_bitwise(gpu_transform(sgh, u, lv, guard=64), want_h)
-        assert_bitwise(gpu_transform(sgh, u, lv, inverse=True, guard=64), want_d)
-        monkeypatch.delenv("SGH_TWO_BLOCKED")
+        assert_bitwise(gpu_transform(sgh, u, lv, guard=64, fuse="two_blocked"), want_h)
+        assert_bitwise(gpu_transform(sgh, u, lv, inverse=True, guard=64, fuse="two_blocked"), want_d)
