@@ -1486,6 +1486,10 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
 // tiles, each taking only the space it needs -- up to 6 C5 tiles in flight
 // instead of 3 -- measured slower: C5 155.9 vs 163, C4 270.8 vs 278.)
 constexpr int kPipeMaxStages = 6;
+#ifndef SGH_PIPE_PARTS
+#define SGH_PIPE_PARTS 1
+#endif
+constexpr int kPipeParts = SGH_PIPE_PARTS;            // a stage frees in this many parts (<= 4)
 
 #ifndef SGH_WAIT_HINT_NS
 #define SGH_WAIT_HINT_NS 20000
@@ -1550,6 +1554,28 @@ __device__ __forceinline__ void bulk_load(double *sdst, const double *gsrc, uint
           smem_u32(sdst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// The part of run i of a tile that lies in part h of its stage (the stage's
+// kPipeParts parts free separately): stage-relative offset o and length len
+// (len <= 0: none); returns the part's global address.  Part boundaries are
+// even offsets, so a part starting at one keeps the run's 16-byte phase.
+template <class R>
+__device__ __forceinline__ const double *pipe_piece(const R &runs, int i, int par, int sd, int h, int &o, int &len) {
+  const int unit = (sd / kPipeParts) & ~1;
+  const int b0 = h * unit, b1 = (h + 1 == kPipeParts) ? sd : (h + 1) * unit;
+  const int ro = par + runs.lo(i);
+  o = max(ro, b0);
+  len = min(ro + runs.len, b1) - o;
+  return runs.g(i) + (o - ro);
+}
+__device__ __forceinline__ void bulk_wait_read_n(int n) {   // wait until at most n bulk groups are unread
+  switch (n) {
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 3;\n" ::: "memory"); break;
+  }
 }
 
 // Contiguous runs of a W == 1 tile, for the loads (every existing row) or the
@@ -1631,8 +1657,15 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
   // each storer waits for the phases of its barriers strictly in order (two
   // storers on one barrier could wait for a phase two ahead of the current
   // one, which the parity test cannot tell from the previous one)
-  __shared__ __align__(8) uint64_t bar_full[kPipeMaxStages], bar_computed[CFG::groups][kPipeMaxStages],
-      bar_empty[kPipeMaxStages], bar_dfull[kPipeMaxDesc], bar_dfree[kPipeMaxDesc];
+  // `full` and `computed` are rings per consumer group, indexed by the group's
+  // own tile count j (slot j % NS): each barrier's phases then belong to ONE
+  // group's tiles, which that group (and its storer) waits for strictly in
+  // order.  (With the stage's barrier shared by the groups, group A could
+  // wait for its tile k while the stage's previous tile k - NS -- the other
+  // group's, whose copies may still be landing -- had not completed its
+  // phase: the parity test reads that incomplete phase as done.)
+  __shared__ __align__(8) uint64_t bar_full[CFG::groups][kPipeMaxStages], bar_computed[CFG::groups][kPipeMaxStages],
+      bar_empty[kPipeMaxStages * kPipeParts], bar_dfull[kPipeMaxDesc], bar_dfree[kPipeMaxDesc];
   __shared__ __align__(16) Task s_task[kPipeMaxDesc];   // descriptor slot of tile k: k % ND
   __shared__ FusedTile s_tile[kPipeMaxDesc];
   const int NS = src.nstages;                     // stage of tile k: k % NS
@@ -1640,9 +1673,9 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mb_init(&bar_full[s], 32);                    // one (cp.async-triggered) arrival per producer lane
+      for (int g = 0; g < CFG::groups; ++g) mb_init(&bar_full[g][s], 32);   // one (cp.async) arrival per producer lane
       for (int g = 0; g < CFG::groups; ++g) mb_init(&bar_computed[g][s], 1);   // the group's leader
-      mb_init(&bar_empty[s], 1);                    // the storer's lane 0
+      for (int h = 0; h < kPipeParts; ++h) mb_init(&bar_empty[s * kPipeParts + h], 1);   // the storer's lane 0
     }
     for (int s = 0; s < ND; ++s) {
       mb_init(&bar_dfull[s], 32);                   // every lane of the descriptor warp
@@ -1713,31 +1746,43 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       const int r = k / NS;
       const int ds = k % ND;
       mb_wait(&bar_dfull[ds], (k / ND) & 1);
-      if (r > 0) mb_wait(&bar_empty[s], (r - 1) & 1);
-      if (lane == 0) PTRACE(k, 1);
+      uint64_t *const fb = &bar_full[k % CFG::groups][(k / CFG::groups) % NS];   // the consuming group's ring
       const Task &T = s_task[ds];
       const FusedTile f = s_tile[ds];
-      double *stage = pipe_smem + (size_t)s * sd + f.par;
+      double *const sbase = pipe_smem + (size_t)s * sd;   // stage start; tile data from f.par
       const PipeRuns runs(T, f, false);
       // this lane's runs: i = lane, lane + 32, ..; bytes first (expect_tx before the copies)
       uint32_t tx = 0;
-      for (int i = lane; i < runs.count; i += 32) {
-        const int head = phase8(runs.g(i));
-        tx += (uint32_t)((runs.len - head) >> 1) * 16u;
+      for (int h = 0; h < kPipeParts; ++h)
+        for (int i = lane; i < runs.count; i += 32) {
+          int o, len;
+          const double *gp = pipe_piece(runs, i, f.par, sd, h, o, len);
+          if (len > 0) tx += (uint32_t)((len - phase8(gp)) >> 1) * 16u;
+        }
+      // the stage's parts free one by one (the storer releases each part once
+      // the copy engine has read it): load into each part as soon as it is free
+      for (int h = 0; h < kPipeParts; ++h) {
+        if (r > 0) mb_wait(&bar_empty[s * kPipeParts + h], (r - 1) & 1);
+        if (h == 0) {
+          // only now is the stage's previous tile consumed, i.e. the previous
+          // phase of `full` complete: the expected bytes count for THIS tile
+          if (tx) mb_expect_tx(fb, tx);
+          if (lane == 0) PTRACE(k, 1);
+        }
+        for (int i = lane; i < runs.count; i += 32) {
+          int o, len;
+          const double *gp = pipe_piece(runs, i, f.par, sd, h, o, len);
+          if (len <= 0) continue;
+          double *sp = sbase + o;
+          const int head = phase8(gp);
+          const int pairs = (len - head) >> 1;
+          const int last = head + 2 * pairs;
+          if (head) cp_async8(sp, gp);
+          if (last < len) cp_async8(sp + last, gp + last);
+          if (pairs > 0) bulk_load(sp + head, gp + head, (uint32_t)pairs * 16u, fb);
+        }
       }
-      if (tx) mb_expect_tx(&bar_full[s], tx);
-      for (int i = lane; i < runs.count; i += 32) {
-        double *sp = stage + runs.lo(i);
-        const double *gp = runs.g(i);
-        const int len = runs.len;
-        const int head = phase8(gp);
-        const int pairs = (len - head) >> 1;
-        const int last = head + 2 * pairs;
-        if (head) cp_async8(sp, gp);
-        if (last < len) cp_async8(sp + last, gp + last);
-        if (pairs > 0) bulk_load(sp + head, gp + head, (uint32_t)pairs * 16u, &bar_full[s]);
-      }
-      mb_arrive_cpasync(&bar_full[s]);
+      mb_arrive_cpasync(fb);
       if (lane == 0) PTRACE(k, 2);
     }
     cp_async_wait<0>();                            // no cp.async outstanding when the warp exits
@@ -1754,13 +1799,14 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       mb_wait(&bar_computed[g][j % NS], (j / NS) & 1);
       const Task &T = s_task[ds];
       const FusedTile f = s_tile[ds];
-      const double *sm = pipe_smem + (size_t)s * sd + f.par;
+      const double *const sbase = pipe_smem + (size_t)s * sd;
       const PipeRuns runs(T, f, true);
-      {
+      for (int h = 0; h < kPipeParts; ++h) {          // one bulk group per part of the stage
         for (int i = lane; i < runs.count; i += 32) {
-          const double *sp = sm + runs.lo(i);
-          double *gp = runs.g(i);
-          const int len = runs.len;
+          int o, len;
+          double *gp = const_cast<double *>(pipe_piece(runs, i, f.par, sd, h, o, len));
+          if (len <= 0) continue;
+          const double *sp = sbase + o;
           const int head = phase8(gp);
           const int pairs = (len - head) >> 1;
           const int last = head + 2 * pairs;
@@ -1772,13 +1818,15 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
                          : "memory");
         }
         bulk_commit();
-        if (lane == 0) PTRACE(k, 6);
-        bulk_wait_read();                           // this lane's copies have read the stage
+      }
+      if (lane == 0) PTRACE(k, 6);
+      for (int h = 0; h < kPipeParts; ++h) {          // release each part once it has been read
+        bulk_wait_read_n(kPipeParts - 1 - h);
         __syncwarp();
+        if (lane == 0) mb_arrive(&bar_empty[s * kPipeParts + h]);
       }
       if (lane == 0) {
         PTRACE(k, 7);
-        mb_arrive(&bar_empty[s]);
         mb_arrive(&bar_dfree[ds]);
       }
     }
@@ -1793,7 +1841,8 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
     for (int k = g; q < total; k += kPipeGroups, q += kPipeGroups * qstep) {
       const int s = k % NS;
       if (sy.tid() == 0) PTRACE(k, 3);
-      mb_wait(&bar_full[s], (k / NS) & 1);
+      const int jg = k / kPipeGroups;                // the group's jg-th tile
+      mb_wait(&bar_full[g][jg % NS], (jg / NS) & 1);
       if (sy.tid() == 0) PTRACE(k, 4);
       const Task &T = s_task[k % ND];
       const FusedTile f = s_tile[k % ND];
