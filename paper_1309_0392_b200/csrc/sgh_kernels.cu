@@ -1486,6 +1486,14 @@ __global__ void __launch_bounds__(FT<W>::v, (STAGES == 1 ? (W == 1 ? FUSED_MINB_
 // tiles, each taking only the space it needs -- up to 6 C5 tiles in flight
 // instead of 3 -- measured slower: C5 155.9 vs 163, C4 270.8 vs 278.)
 constexpr int kPipeMaxStages = 6;
+#ifndef SGH_PIPE_MINW
+#define SGH_PIPE_MINW 999
+#endif
+#ifndef SGH_PIPE_MINRUN
+#define SGH_PIPE_MINRUN 128
+#endif
+constexpr int kPipeMinRun = SGH_PIPE_MINRUN;        // W == 1 tiles whose runs are shorter stay on k_fused
+constexpr int kPipeMinW = SGH_PIPE_MINW;            // W > 1 column tiles this wide or wider run on k_fpipe
 #ifndef SGH_PIPE_PARTS
 #define SGH_PIPE_PARTS 1
 #endif
@@ -1626,6 +1634,65 @@ struct PipeRuns {
   }
 };
 
+// Runs of a W > 1 column tile: every tile row is one run of wc doubles
+// (SMEM row r at r (W + 1), odd stride: its 8-byte phase follows the global
+// row's, as in fused_load_rows).  Dense: rows r = 0..P-1 at g + r S.  With a
+// special axis: row r = x + A (y + ej z) at g + x S + y Gj + z Gnext, loaded
+// if y is a grid row, stored if y is a row the tile writes (fused_rows_special).
+template <int W>
+struct PipeRunsW {
+  double *g0;
+  int64_t S, Gj, Gn;
+  int A, ej, y0, ny, len, count;
+  FDiv fA;
+  bool special;
+  __device__ __forceinline__ PipeRunsW(const Task &T, const FusedTile &f, bool store) {
+    g0 = f.g;
+    S = T.S;
+    len = f.wc;
+    special = T.bj >= 0;
+    if (!special) {
+      count = T.P;
+      A = 1;
+      ej = 1;
+      y0 = 0;
+      ny = 1;
+      Gj = Gn = 0;
+      return;
+    }
+    const bool blocked = T.bt < T.gl[T.bj];
+    A = T.A;
+    ej = T.ej;
+    fA = T.fA;
+    Gj = T.Gj;
+    Gn = T.Gnext;
+    y0 = (store && blocked) ? 1 : f.ylo;
+    const int y1 = (store && blocked) ? ej - 2 : f.yhi;
+    ny = y1 - y0 + 1;
+    const int nz = T.P / (A * ej);
+    count = (ny > 0) ? A * ny * nz : 0;
+  }
+  // run i -> (x, y, z): x fastest, then the existing / written rows y, then z
+  __device__ __forceinline__ void xyz(int i, int &x, int &y, int &z) const {
+    const int q = (int)fdiv((uint32_t)i, fA);
+    x = i - q * A;
+    z = q / ny;
+    y = y0 + (q - z * ny);
+  }
+  __device__ __forceinline__ int lo(int i) const {
+    if (!special) return i * (W + 1);
+    int x, y, z;
+    xyz(i, x, y, z);
+    return (x + A * (y + ej * z)) * (W + 1);
+  }
+  __device__ __forceinline__ double *g(int i) const {
+    if (!special) return g0 + (int64_t)i * S;
+    int x, y, z;
+    xyz(i, x, y, z);
+    return g0 + (int64_t)x * S + (int64_t)y * Gj + (int64_t)z * Gn;
+  }
+};
+
 // Task owning tile q (the last t with prefix[t] <= q), searching forward from
 // idx (prefix[idx] <= q) with the whole warp: 32 probes per round trip at
 // stride 1, 32, 1024, .. (expanding while all probes are <= q, then refining).
@@ -1650,8 +1717,9 @@ __device__ __forceinline__ int warp_find_task(const Src &src, int idx, int64_t q
   }
 }
 
-template <bool INV, class CFG>
+template <bool INV, class CFG, int W>
 __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant__ Src src) {
+  using Runs = typename std::conditional<W == 1, PipeRuns, PipeRunsW<W>>::type;
   extern __shared__ __align__(128) double pipe_smem[];
   // `computed` is a ring per consumer group (its j-th tile: slot j % NS), so
   // each storer waits for the phases of its barriers strictly in order (two
@@ -1722,7 +1790,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       for (int u = 0; u < 3; ++u)
         if (lane + 32 * u < kTW) b[lane + 32 * u] = dreg[u];
       __syncwarp();
-      const FusedTile f = fused_tile<1>(s_task[ds], ql);
+      const FusedTile f = fused_tile<W>(s_task[ds], ql);
       if (lane == 0) s_tile[ds] = f;
       __syncwarp();
       if (lane == 0) PTRACE(k, 0);
@@ -1750,7 +1818,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       const Task &T = s_task[ds];
       const FusedTile f = s_tile[ds];
       double *const sbase = pipe_smem + (size_t)s * sd;   // stage start; tile data from f.par
-      const PipeRuns runs(T, f, false);
+      const Runs runs(T, f, false);
       // this lane's runs: i = lane, lane + 32, ..; bytes first (expect_tx before the copies)
       uint32_t tx = 0;
       for (int h = 0; h < kPipeParts; ++h)
@@ -1800,7 +1868,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       const Task &T = s_task[ds];
       const FusedTile f = s_tile[ds];
       const double *const sbase = pipe_smem + (size_t)s * sd;
-      const PipeRuns runs(T, f, true);
+      const Runs runs(T, f, true);
       for (int h = 0; h < kPipeParts; ++h) {          // one bulk group per part of the stage
         for (int i = lane; i < runs.count; i += 32) {
           int o, len;
@@ -1851,7 +1919,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
 #else
       const int tk = -1;
 #endif
-      fused_compute<INV, 1, kPipeCT, GroupSync<kPipeCT>>(T, f, pipe_smem + (size_t)s * sd + f.par, sy, tk);
+      fused_compute<INV, W, kPipeCT, GroupSync<kPipeCT>>(T, f, pipe_smem + (size_t)s * sd + f.par, sy, tk);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // SMEM results -> the bulk stores
       sy.bar();
       if (sy.tid() == 0) {
@@ -1864,7 +1932,19 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
 
 // W == 1 FUSED tasks the pipelined kernel runs: dense ranges, or runs whose
 // SMEM 8-byte phase follows the global one (bulk copies need equal 16-byte phases)
-bool pipe_task(const Task &t) { return t.kind == KIND_FUSED && t.W == 1 && (t.bj < 0 || t.aligned); }
+// (runs shorter than kPipeMinRun doubles -- e.g. C3's 33-point blocks of the
+// contiguous axis, 225 runs per tile -- make the copy engine slow: one bulk
+// copy per short run measured 0.26 of the copy peak on C3 vs 0.49 on k_fused's
+// LDGSTS; W > 1 column tiles, one run per 128-1024 B row, likewise: C5 146 vs
+// 167, so they stay on k_fused by default)
+bool pipe_task(const Task &t) {
+  if (t.kind != KIND_FUSED || (t.bj >= 0 && !t.aligned)) return false;
+  if (t.W > 1) return t.W >= kPipeMinW;
+  if (t.bj < 0) return true;                      // dense: one range per tile
+  const int64_t run = (t.Gj == t.A) ? int64_t(t.A) * t.ej : t.A;
+  return run >= kPipeMinRun;
+}
+
 
 // ----------------------------------------------------------------------- REG
 // One thread per column (o, r); the whole pole of n = 2^L - 1 points lives in
@@ -1932,6 +2012,20 @@ __global__ void __launch_bounds__(kThreads) k_reg(const __grid_constant__ Src sr
 // ------------------------------------------------------------ host launchers
 using KernelFn = void (*)(Src);
 constexpr int kProfKindPipe = 7;                 // sgh_launch_record.kind of k_fpipe launches
+
+// the k_fpipe instance for a tile width
+template <class CFG>
+static KernelFn fpipe_for(int w, bool inv) {
+  switch (w) {
+    case 1: return inv ? k_fpipe<true, CFG, 1> : k_fpipe<false, CFG, 1>;
+    case 8: return inv ? k_fpipe<true, CFG, 8> : k_fpipe<false, CFG, 8>;
+    case 16: return inv ? k_fpipe<true, CFG, 16> : k_fpipe<false, CFG, 16>;
+    case 32: return inv ? k_fpipe<true, CFG, 32> : k_fpipe<false, CFG, 32>;
+    case 64: return inv ? k_fpipe<true, CFG, 64> : k_fpipe<false, CFG, 64>;
+    case 128: return inv ? k_fpipe<true, CFG, 128> : k_fpipe<false, CFG, 128>;
+    default: return nullptr;
+  }
+}
 
 // FUSED pipeline depth: 1 (default) or 2 stages (tuning override SGH_FUSED_STAGES)
 int fused_stages() {
@@ -2055,8 +2149,7 @@ static int pipe_stages(KernelFn fn, size_t stage_bytes) {
 // Launch one task (single grid).  Returns the CUDA error of the launch.
 cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
   const bool pipe = pipe_task(task);
-  KernelFn fn = pipe ? (inv ? k_fpipe<true, PipeSingle> : k_fpipe<false, PipeSingle>)
-                     : kernel_for(task.kind, task.l, task.W, inv);
+  KernelFn fn = pipe ? fpipe_for<PipeSingle>(task.W, inv) : kernel_for(task.kind, task.l, task.W, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = nullptr;
@@ -2087,7 +2180,7 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
 cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
                          int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream,
                          int variant, bool pipe) {
-  KernelFn fn = pipe ? (inv ? k_fpipe<true, PipeBatched> : k_fpipe<false, PipeBatched>) : kernel_for(kind, l, w, inv);
+  KernelFn fn = pipe ? fpipe_for<PipeBatched>(w, inv) : kernel_for(kind, l, w, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = d_tasks;
