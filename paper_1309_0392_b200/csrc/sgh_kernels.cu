@@ -1494,10 +1494,6 @@ constexpr int kPipeMaxStages = 6;
 #endif
 constexpr int kPipeMinRun = SGH_PIPE_MINRUN;        // W == 1 tiles whose runs are shorter stay on k_fused
 constexpr int kPipeMinW = SGH_PIPE_MINW;            // W > 1 column tiles this wide or wider run on k_fpipe
-#ifndef SGH_PIPE_PARTS
-#define SGH_PIPE_PARTS 1
-#endif
-constexpr int kPipeParts = SGH_PIPE_PARTS;            // a stage frees in this many parts (<= 4)
 
 #ifndef SGH_WAIT_HINT_NS
 #define SGH_WAIT_HINT_NS 20000
@@ -1562,28 +1558,6 @@ __device__ __forceinline__ void bulk_load(double *sdst, const double *gsrc, uint
           smem_u32(sdst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
-}
-
-// The part of run i of a tile that lies in part h of its stage (the stage's
-// kPipeParts parts free separately): stage-relative offset o and length len
-// (len <= 0: none); returns the part's global address.  Part boundaries are
-// even offsets, so a part starting at one keeps the run's 16-byte phase.
-template <class R>
-__device__ __forceinline__ const double *pipe_piece(const R &runs, int i, int par, int sd, int h, int &o, int &len) {
-  const int unit = (sd / kPipeParts) & ~1;
-  const int b0 = h * unit, b1 = (h + 1 == kPipeParts) ? sd : (h + 1) * unit;
-  const int ro = par + runs.lo(i);
-  o = max(ro, b0);
-  len = min(ro + runs.len, b1) - o;
-  return runs.g(i) + (o - ro);
-}
-__device__ __forceinline__ void bulk_wait_read_n(int n) {   // wait until at most n bulk groups are unread
-  switch (n) {
-    case 0: asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); break;
-    case 1: asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); break;
-    case 2: asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory"); break;
-    default: asm volatile("cp.async.bulk.wait_group.read 3;\n" ::: "memory"); break;
-  }
 }
 
 // Contiguous runs of a W == 1 tile, for the loads (every existing row) or the
@@ -1733,7 +1707,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
   // group's, whose copies may still be landing -- had not completed its
   // phase: the parity test reads that incomplete phase as done.)
   __shared__ __align__(8) uint64_t bar_full[CFG::groups][kPipeMaxStages], bar_computed[CFG::groups][kPipeMaxStages],
-      bar_empty[kPipeMaxStages * kPipeParts], bar_dfull[kPipeMaxDesc], bar_dfree[kPipeMaxDesc];
+      bar_empty[kPipeMaxStages], bar_dfull[kPipeMaxDesc], bar_dfree[kPipeMaxDesc];
   __shared__ __align__(16) Task s_task[kPipeMaxDesc];   // descriptor slot of tile k: k % ND
   __shared__ FusedTile s_tile[kPipeMaxDesc];
   const int NS = src.nstages;                     // stage of tile k: k % NS
@@ -1743,7 +1717,7 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
     for (int s = 0; s < NS; ++s) {
       for (int g = 0; g < CFG::groups; ++g) mb_init(&bar_full[g][s], 32);   // one (cp.async) arrival per producer lane
       for (int g = 0; g < CFG::groups; ++g) mb_init(&bar_computed[g][s], 1);   // the group's leader
-      for (int h = 0; h < kPipeParts; ++h) mb_init(&bar_empty[s * kPipeParts + h], 1);   // the storer's lane 0
+      mb_init(&bar_empty[s], 1);                    // the storer's lane 0
     }
     for (int s = 0; s < ND; ++s) {
       mb_init(&bar_dfull[s], 32);                   // every lane of the descriptor warp
@@ -1819,36 +1793,24 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       const FusedTile f = s_tile[ds];
       double *const sbase = pipe_smem + (size_t)s * sd;   // stage start; tile data from f.par
       const Runs runs(T, f, false);
-      // this lane's runs: i = lane, lane + 32, ..; bytes first (expect_tx before the copies)
+      // one bulk copy (copy engine) per run; bytes first: expect_tx before the copies
       uint32_t tx = 0;
-      for (int h = 0; h < kPipeParts; ++h)
-        for (int i = lane; i < runs.count; i += 32) {
-          int o, len;
-          const double *gp = pipe_piece(runs, i, f.par, sd, h, o, len);
-          if (len > 0) tx += (uint32_t)((len - phase8(gp)) >> 1) * 16u;
-        }
-      // the stage's parts free one by one (the storer releases each part once
-      // the copy engine has read it): load into each part as soon as it is free
-      for (int h = 0; h < kPipeParts; ++h) {
-        if (r > 0) mb_wait(&bar_empty[s * kPipeParts + h], (r - 1) & 1);
-        if (h == 0) {
-          // only now is the stage's previous tile consumed, i.e. the previous
-          // phase of `full` complete: the expected bytes count for THIS tile
-          if (tx) mb_expect_tx(fb, tx);
-          if (lane == 0) PTRACE(k, 1);
-        }
-        for (int i = lane; i < runs.count; i += 32) {
-          int o, len;
-          const double *gp = pipe_piece(runs, i, f.par, sd, h, o, len);
-          if (len <= 0) continue;
-          double *sp = sbase + o;
-          const int head = phase8(gp);
-          const int pairs = (len - head) >> 1;
-          const int last = head + 2 * pairs;
-          if (head) cp_async8(sp, gp);
-          if (last < len) cp_async8(sp + last, gp + last);
-          if (pairs > 0) bulk_load(sp + head, gp + head, (uint32_t)pairs * 16u, fb);
-        }
+      for (int i = lane; i < runs.count; i += 32) tx += (uint32_t)((runs.len - phase8(runs.g(i))) >> 1) * 16u;
+      if (r > 0) mb_wait(&bar_empty[s], (r - 1) & 1);
+      // only now is the stage's previous tile consumed, i.e. the previous phase
+      // of this `full` barrier complete: the expected bytes count for THIS tile
+      if (tx) mb_expect_tx(fb, tx);
+      if (lane == 0) PTRACE(k, 1);
+      for (int i = lane; i < runs.count; i += 32) {
+        double *sp = sbase + f.par + runs.lo(i);
+        const double *gp = runs.g(i);
+        const int len = runs.len;
+        const int head = phase8(gp);
+        const int pairs = (len - head) >> 1;
+        const int last = head + 2 * pairs;
+        if (head) cp_async8(sp, gp);
+        if (last < len) cp_async8(sp + last, gp + last);
+        if (pairs > 0) bulk_load(sp + head, gp + head, (uint32_t)pairs * 16u, fb);
       }
       mb_arrive_cpasync(fb);
       if (lane == 0) PTRACE(k, 2);
@@ -1869,30 +1831,25 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
       const FusedTile f = s_tile[ds];
       const double *const sbase = pipe_smem + (size_t)s * sd;
       const Runs runs(T, f, true);
-      for (int h = 0; h < kPipeParts; ++h) {          // one bulk group per part of the stage
-        for (int i = lane; i < runs.count; i += 32) {
-          int o, len;
-          double *gp = const_cast<double *>(pipe_piece(runs, i, f.par, sd, h, o, len));
-          if (len <= 0) continue;
-          const double *sp = sbase + o;
-          const int head = phase8(gp);
-          const int pairs = (len - head) >> 1;
-          const int last = head + 2 * pairs;
-          if (head) __stcg(gp, sp[0]);
-          if (last < len) __stcg(gp + last, sp[last]);
-          if (pairs > 0)
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gp + head),
-                         "r"(smem_u32(sp + head)), "r"(pairs * 16)
-                         : "memory");
-        }
-        bulk_commit();
+      for (int i = lane; i < runs.count; i += 32) {
+        const double *sp = sbase + f.par + runs.lo(i);
+        double *gp = runs.g(i);
+        const int len = runs.len;
+        const int head = phase8(gp);
+        const int pairs = (len - head) >> 1;
+        const int last = head + 2 * pairs;
+        if (head) __stcg(gp, sp[0]);
+        if (last < len) __stcg(gp + last, sp[last]);
+        if (pairs > 0)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gp + head),
+                       "r"(smem_u32(sp + head)), "r"(pairs * 16)
+                       : "memory");
       }
+      bulk_commit();
       if (lane == 0) PTRACE(k, 6);
-      for (int h = 0; h < kPipeParts; ++h) {          // release each part once it has been read
-        bulk_wait_read_n(kPipeParts - 1 - h);
-        __syncwarp();
-        if (lane == 0) mb_arrive(&bar_empty[s * kPipeParts + h]);
-      }
+      bulk_wait_read();                             // this lane's copies have read the stage
+      __syncwarp();
+      if (lane == 0) mb_arrive(&bar_empty[s]);
       if (lane == 0) {
         PTRACE(k, 7);
         mb_arrive(&bar_dfree[ds]);
@@ -1935,8 +1892,10 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
 // (runs shorter than kPipeMinRun doubles -- e.g. C3's 33-point blocks of the
 // contiguous axis, 225 runs per tile -- make the copy engine slow: one bulk
 // copy per short run measured 0.26 of the copy peak on C3 vs 0.49 on k_fused's
-// LDGSTS; W > 1 column tiles, one run per 128-1024 B row, likewise: C5 146 vs
-// 167, so they stay on k_fused by default)
+// LDGSTS from all threads; W > 1 column tiles, one run per 128-1024 B row,
+// likewise: C5 146 vs 167.  Loading short runs with 16-byte cp.async from the
+// producer warp instead was slower still (C3 0.11, C5 101-145): one warp
+// cannot issue a tile's worth of small copies in time.  Both stay on k_fused.)
 bool pipe_task(const Task &t) {
   if (t.kind != KIND_FUSED || (t.bj >= 0 && !t.aligned)) return false;
   if (t.W > 1) return t.W >= kPipeMinW;
