@@ -269,7 +269,10 @@ def dry_run(args, rank, world, local_rank):
     else:
         info.update(path="replica of the single-grid workload" if world > 1 else "single GPU",
                     grids=len(members), points=sum(sizes))
-    print(json.dumps(info), flush=True)
+    # one write(2) per rank: the ranks share stdout, and a single short write
+    # to a pipe is atomic (print may split the line from its newline)
+    sys.stdout.flush()
+    os.write(1, (json.dumps(info) + "\n").encode())
     return 0
 
 

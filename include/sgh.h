@@ -140,7 +140,12 @@ size_t sgh_batched_host_buffer_bytes(const int32_t *levels, int32_t d, int64_t n
  * Grids are copied in, transformed and copied back in chunks of ~64 MB; the
  * copies run on two library-owned streams overlapped with the transform, and
  * `stream` waits for the last copy-out, so after synchronising `stream` every
- * host grid holds its result.  Asynchronous w.r.t. the host. */
+ * host grid holds its result.  Mostly asynchronous w.r.t. the host: each
+ * chunk's task table goes through a 4-slot pinned staging ring, so with more
+ * than 4 chunks the call waits on the host until an earlier chunk's table
+ * upload has completed (the call returns while the last chunks are still in
+ * flight).  Grids whose host memory is contiguous move with one copy per run
+ * in each direction. */
 sgh_status sgh_transform_batched_host(double *const *host_grids, const int32_t *levels, int32_t d,
                                       int64_t num_grids, uint32_t flags,
                                       void *device_buffer, size_t device_buffer_bytes,

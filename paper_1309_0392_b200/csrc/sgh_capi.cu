@@ -585,6 +585,18 @@ static double kind_bw(const Task &t) {
       // contiguous axis) touch one 32-byte sector per point and write partial
       // sectors (measured ~0.3 TB/s algorithmic on C3's (5,4,4) lattice)
       if (t.bj >= 0 && !t.aligned) bw = std::min(bw, run <= 1 ? 0.35 : 1.5);
+#ifndef SGH_COST_R1
+      // round 2: tasks on the pipelined bulk-copy kernel k_fpipe run at its
+      // measured rates (profiles/r02: C5's contiguous-run tiles 5.3 TB/s, C4's
+      // 257 x 33 two-blocked tiles 5.8, C2's 255 x 33 blocked tiles 4.4);
+      // W = 1 tiles with runs shorter than 128 doubles stay on k_fused (2.85)
+      if (pipe_task(t)) {
+        if (t.bt2 >= 0 && t.bt < t.gl[t.bj]) bw = t.ej >= 257 ? 5.6 : 4.5;
+        else bw = 5.3;
+      } else if (t.W == 1 && t.aligned && run < 128) {
+        bw = std::min(bw, 2.9);
+      }
+#endif
       return bw;
     }
     default: return 4.0;

@@ -1498,6 +1498,9 @@ constexpr int kPipeMinW = SGH_PIPE_MINW;            // W > 1 column tiles this w
 #ifndef SGH_WAIT_HINT_NS
 #define SGH_WAIT_HINT_NS 20000
 #endif
+#ifndef SGH_WAIT_SLEEP_NS
+#define SGH_WAIT_SLEEP_NS 0
+#endif
 constexpr int kPipeDescAhead = 3;                    // descriptor slots beyond the stages
 constexpr int kPipeMaxDesc = kPipeMaxStages + kPipeDescAhead;
 // Consumer configuration <groups, warps per group>: one task per launch (a
@@ -1534,13 +1537,21 @@ __device__ __forceinline__ void mb_init(uint64_t *b, uint32_t count) {
 // takes issue slots from the other consumer group on its SM sub-partitions).
 __device__ __forceinline__ void mb_wait(uint64_t *b, uint32_t parity) {
   uint32_t done;
-  do {
+#if SGH_WAIT_SLEEP_NS > 0
+  int sleep_ns = 32;
+#endif
+  for (;;) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(smem_u32(b)), "r"(parity), "n"(SGH_WAIT_HINT_NS)
         : "memory");
-  } while (!done);
+    if (done) break;
+#if SGH_WAIT_SLEEP_NS > 0
+    __nanosleep(sleep_ns);                         // back off: fewer issue slots taken while waiting
+    if (sleep_ns < SGH_WAIT_SLEEP_NS) sleep_ns *= 2;
+#endif
+  }
 }
 __device__ __forceinline__ void mb_arrive(uint64_t *b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");

@@ -11,9 +11,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _run(env_extra):
     env = dict(os.environ, **env_extra)
+    gpus = env_extra.get("WORLD_SIZE", "1")       # the driver passes --gpus N with N ranks
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "C2",
-                        "--steps", "1", "--warmup", "1"], capture_output=True, text=True, env=env, cwd=ROOT,
-                       timeout=600)
+                        "--steps", "1", "--warmup", "1", "--gpus", gpus], capture_output=True, text=True, env=env,
+                       cwd=ROOT, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     return [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
 

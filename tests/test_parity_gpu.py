@@ -370,6 +370,31 @@ def test_batched_host_e2e(sgh):
         assert_bitwise(h.numpy(), want)
 
 
+def test_batched_host_e2e_multichunk_contiguous(sgh):
+    """The e2e host path with many ~64 MB transfer chunks (more than the
+    4-slot staging ring) and grids that are views of ONE pinned buffer (the
+    contiguous-run placement: one copy per run of host-contiguous grids, the
+    next chunk's grids copied in while the previous chunk is transformed);
+    run twice (the second call hits the plan cache), bitwise vs the oracle."""
+    cs = si.combination_set(4, 17)                       # ~520 MB: ~8 chunks of 64 MB
+    sizes = [si.num_points(lv) for lv in cs]
+    host = torch.empty(sum(sizes), dtype=torch.float64).pin_memory()
+    views, off = [], 0
+    for n in sizes:
+        views.append(host[off:off + n])
+        off += n
+    fills = [si.fill_uniform(n, SD["seed"], g) for g, n in enumerate(sizes)]
+    buf = torch.empty(sgh.batched_host_buffer_bytes(cs) // 8 + 64, dtype=torch.float64, device="cuda")
+    pick = sorted(set(range(0, len(cs), 37)) | {0, len(cs) - 1})
+    for rep in range(2):
+        for v, f in zip(views, fills):
+            v.copy_(torch.from_numpy(f))
+        sgh.transform_batched_host(views, cs, buf)
+        torch.cuda.synchronize()
+        for g in pick:
+            assert_bitwise(views[g].numpy(), oracle.hierarchize(fills[g].copy(), cs[g]))
+
+
 # --------------------------------------------------------------- sharded
 @pytest.mark.parametrize("levels,P", [((6, 5), 2), ((6, 5), 4), ((5, 4, 6), 8), ((3, 7), 8), ((8, 2, 3, 4), 4),
                                       ((14, 13), 8)], ids=str)
