@@ -865,6 +865,7 @@ struct Segment {
   double points;      // points the segment transforms (profiling)
   int variant;        // task_variant of its tasks (3: mixed blocked / lattice)
   bool pipe;          // runs on k_fpipe (pipe_task)
+  int stage;          // (round, phase) index: segments of one stage touch disjoint grids
 };
 
 struct BatchedPlan {
@@ -888,6 +889,7 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
     rounds = std::max(rounds, all[g].size());
   }
   std::vector<std::vector<Task>> per(num_grids);
+  int stage = 0;
   for (size_t k = 0; k < rounds; ++k) {
     size_t maxp = 0;
     for (int64_t g = 0; g < num_grids; ++g) {
@@ -896,7 +898,7 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
       if (inv) std::reverse(per[g].begin(), per[g].end());
       maxp = std::max(maxp, per[g].size());
     }
-    for (size_t j = 0; j < maxp; ++j) {
+    for (size_t j = 0; j < maxp; ++j, ++stage) {
       // group phase j of all grids by kernel instance (kind, and l for REG)
       // SGH_SPLIT_VARIANTS=1 (profiling): dense / blocked / lattice FUSED tasks in separate launches
       static const bool split = tuning_env("SGH_SPLIT_VARIANTS") != nullptr;
@@ -917,6 +919,7 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
         sg.prefix_off = P.prefix.size();
         sg.ntasks = (int32_t)kv.second.size();
         sg.pipe = (std::get<3>(kv.first) & 1) != 0;
+        sg.stage = stage;
         int64_t acc = 0;
         sg.smem = 0;
         sg.points = 0;
@@ -970,6 +973,38 @@ static sgh_status validate_batch(double *const *grids, const int32_t *levels, in
     if (st != SGH_OK) return st;
     if (need_grids && !grids[g]) return invalid("grids[g] is NULL");
   }
+  return SGH_OK;
+}
+
+#ifndef SGH_CONCURRENT
+#define SGH_CONCURRENT 0
+#endif
+constexpr bool kConcurrent = SGH_CONCURRENT != 0;
+
+// library-owned streams and events for the concurrent launch of a stage's
+// segments (per device, created once)
+struct ConcStreams {
+  static constexpr size_t kN = 4;
+  cudaStream_t st[kN] = {};
+  cudaEvent_t fork = nullptr, join[kN] = {};
+};
+static std::mutex g_conc_mu;
+static std::map<int, ConcStreams> g_conc;
+
+static sgh_status conc_streams(ConcStreams *&out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_conc_mu);
+  ConcStreams &c = g_conc[dev];
+  if (!c.fork) {
+    for (size_t i = 0; i < ConcStreams::kN; ++i) {
+      if ((e = cudaStreamCreateWithFlags(&c.st[i], cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+      if ((e = cudaEventCreateWithFlags(&c.join[i], cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+    }
+    if ((e = cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e, "event");
+  }
+  out = &c;
   return SGH_OK;
 }
 
@@ -1044,16 +1079,41 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
   }
   const Task *d_tasks = reinterpret_cast<const Task *>(workspace);
   const int64_t *d_prefix = reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + prefix_base);
-  for (const Segment &sg : P.segs) {
-    cudaError_t e = launch_table(sg.kind, sg.l, sg.w, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off, sg.ntasks,
-                                 sg.tiles, sg.smem, sg.points, s, sg.variant, sg.pipe);
-    if (e != cudaSuccess) {
-      char where[160];
-      std::snprintf(where, sizeof where, "grouped kernel launch (kind %d, W %d, l %d, variant %d, %s, %d tasks)",
-                    sg.kind, sg.w, sg.l, sg.variant, sg.pipe ? "k_fpipe" : "k_fused/per-axis", sg.ntasks);
-      return cuda_fail(e, where);
+  // The segments of one (round, phase) stage touch disjoint grids: with
+  // kConcurrent (-DSGH_CONCURRENT=1), a stage's launches go to library
+  // streams forked from and joined back into `s`, so one kernel's tail
+  // overlaps the next ones.  Measured slower on C5 (169.2 vs 170-171, dehier
+  // 152.9 vs 155.0: the overlapping kernels compete), so off by default.
+  ConcStreams *cs = nullptr;
+  if (kConcurrent && (st = conc_streams(cs)) != SGH_OK) return st;
+  for (size_t a = 0; a < P.segs.size();) {
+    size_t b = a + 1;
+    while (b < P.segs.size() && P.segs[b].stage == P.segs[a].stage) ++b;
+    const bool fork = kConcurrent && b - a > 1;
+    if (fork) {
+      cudaEventRecord(cs->fork, s);
+      for (size_t i = 0; i < b - a && i < ConcStreams::kN; ++i) cudaStreamWaitEvent(cs->st[i], cs->fork, 0);
     }
-    count_launch();
+    for (size_t i = a; i < b; ++i) {
+      const Segment &sg = P.segs[i];
+      cudaStream_t ls = fork ? cs->st[(i - a) % ConcStreams::kN] : s;
+      cudaError_t e = launch_table(sg.kind, sg.l, sg.w, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off,
+                                   sg.ntasks, sg.tiles, sg.smem, sg.points, ls, sg.variant, sg.pipe);
+      if (e != cudaSuccess) {
+        char where[160];
+        std::snprintf(where, sizeof where, "grouped kernel launch (kind %d, W %d, l %d, variant %d, %s, %d tasks)",
+                      sg.kind, sg.w, sg.l, sg.variant, sg.pipe ? "k_fpipe" : "k_fused/per-axis", sg.ntasks);
+        return cuda_fail(e, where);
+      }
+      count_launch();
+    }
+    if (fork) {
+      for (size_t i = 0; i < b - a && i < ConcStreams::kN; ++i) {
+        cudaEventRecord(cs->join[i], cs->st[i]);
+        cudaStreamWaitEvent(s, cs->join[i], 0);
+      }
+    }
+    a = b;
   }
   return SGH_OK;
 }
