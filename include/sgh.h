@@ -249,6 +249,23 @@ sgh_status sgh_digest(const double *grid, int64_t n, int64_t index_offset, uint6
 sgh_status sgh_digest_batched(double *const *grids, const int64_t *sizes, int64_t num_grids,
                               uint64_t *out_host, void *workspace, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------ ablation (report only)
+ * the paper's BFS data layout of a 1-D pole (Fig.
+ * fig:hierDehier: points in breadth-first order of the binary hierarchy --
+ * root first, level by level, left to right; natural 1-based point
+ * i = (2 j + 1) 2^{l - lam} at BFS position 2^{lam-1} - 1 + j).  Not the
+ * product layout; timed against the row-major kernels by
+ * scripts/ablation_bfs.py.  Device pointers to 2^l - 1 doubles, stream-ordered.
+ *  permute: to_bfs != 0: dst[BFS(p)] = src[natural]; else the inverse.
+ *  hierarchize: out of place (one-pass stencil of the entering values; in and
+ *               out must not alias); dehierarchize: in place, one launch per
+ *               level, coarse -> fine.  Bitwise equal to Alg. 1 on the
+ *               permuted data.  Errors: INVALID_ARGUMENT (NULL / aliased / l
+ *               outside 1..SGH_MAX_LEVEL), CUDA. */
+sgh_status sgh_ablation_bfs_permute_1d(const double *src, double *dst, int32_t l, int32_t to_bfs, void *stream);
+sgh_status sgh_ablation_bfs_hierarchize_1d(const double *in, double *out, int32_t l, void *stream);
+sgh_status sgh_ablation_bfs_dehierarchize_1d(double *grid, int32_t l, void *stream);
+
 /* Optional per-launch timing of the transform kernels (process-wide).
  * sgh_profile_enable(1) clears the record list and starts recording: every
  * transform kernel launch is bracketed by two CUDA events on its own stream.

@@ -100,6 +100,9 @@ def _load():
                                ctypes.c_int32, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
         "sgh_sparse_num_subspaces": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
         "sgh_sparse_subspace_offset": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]),
+        "sgh_ablation_bfs_permute_1d": (st, [vp, vp, ctypes.c_int32, ctypes.c_int32, vp]),
+        "sgh_ablation_bfs_hierarchize_1d": (st, [vp, vp, ctypes.c_int32, vp]),
+        "sgh_ablation_bfs_dehierarchize_1d": (st, [vp, ctypes.c_int32, vp]),
         "sgh_profile_enable": (st, [ctypes.c_int32]),
         "sgh_profile_read": (ctypes.c_int64, [ctypes.c_void_p, ctypes.c_int64]),
         "sgh_status_string": (ctypes.c_char_p, [st]),
@@ -123,7 +126,8 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
             "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_sparse_num_points",
             "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter", "sgh_gather_ex",
-            "sgh_sparse_num_subspaces", "sgh_sparse_subspace_offset",
+            "sgh_sparse_num_subspaces", "sgh_sparse_subspace_offset", "sgh_ablation_bfs_permute_1d",
+            "sgh_ablation_bfs_hierarchize_1d", "sgh_ablation_bfs_dehierarchize_1d",
             "sgh_status_string", "sgh_last_error", "sgh_version")
 
 
@@ -655,3 +659,28 @@ def scatter(sparse: torch.Tensor, grids, levels_list, n: int, stream=None):
                                ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
     _keep_on(stream, ws)
     return grids
+
+
+# ------------------------------------------------------ ablation (report only)
+def bfs_permute_1d(src: torch.Tensor, dst: torch.Tensor, level: int, to_bfs: bool = True, stream=None):
+    """Natural <-> BFS order of a 1-D pole (sgh.h ablation section)."""
+    with torch.cuda.device(src.device):
+        _check(lib.sgh_ablation_bfs_permute_1d(_grid_ptr(src, [level]), _grid_ptr(dst, [level]), int(level),
+                                                1 if to_bfs else 0, _stream(stream)))
+    return dst
+
+
+def bfs_hierarchize_1d(src: torch.Tensor, dst: torch.Tensor, level: int, stream=None):
+    """Hierarchization of a BFS-ordered 1-D pole, out of place (ablation)."""
+    with torch.cuda.device(src.device):
+        _check(lib.sgh_ablation_bfs_hierarchize_1d(_grid_ptr(src, [level]), _grid_ptr(dst, [level]), int(level),
+                                                    _stream(stream)))
+    return dst
+
+
+def bfs_dehierarchize_1d(grid: torch.Tensor, level: int, stream=None):
+    """Dehierarchization of a BFS-ordered 1-D pole, in place (ablation)."""
+    with torch.cuda.device(grid.device):
+        _check(lib.sgh_ablation_bfs_dehierarchize_1d(_grid_ptr(grid, [level]), int(level), _stream(stream)))
+    return grid
+

@@ -543,3 +543,65 @@ def test_random_shapes_fuzz(sgh, seed):
             assert_bitwise(gpu_transform(sgh, u, lv, inverse=True, fuse=fuse, guard=64), want_d)
         assert_bitwise(gpu_transform(sgh, u, lv, guard=64, fuse="two_blocked"), want_h)
         assert_bitwise(gpu_transform(sgh, u, lv, inverse=True, guard=64, fuse="two_blocked"), want_d)
+
+
+# --------------------------------------------- ablation: BFS layout (report only)
+@pytest.mark.parametrize("l", [1, 2, 3, 5, 9, 13, 20], ids=str)
+def test_bfs_layout_ablation_bitwise(sgh, l):
+    """the paper's BFS layout of a 1-D pole.  The
+    fill permuted into BFS order, hierarchized there (out of place) and
+    permuted back is Alg. 1's result bitwise; the same for the in-place BFS
+    dehierarchization; and the permutation round trip is the identity."""
+    N = (1 << l) - 1
+    u = si.fill_uniform(N, grid_id=l)
+    nat = torch.from_numpy(u).cuda()
+    bfs = torch.empty_like(nat)
+    out = torch.empty_like(nat)
+    back = torch.empty_like(nat)
+    sgh.bfs_permute_1d(nat, bfs, l, to_bfs=True)
+    sgh.bfs_permute_1d(bfs, back, l, to_bfs=False)
+    torch.cuda.synchronize()
+    assert_bitwise(back.cpu().numpy(), u)
+    if l > 1:                                       # the root sits first in BFS order
+        assert float(bfs[0]) == u[(1 << (l - 1)) - 1]
+    sgh.bfs_hierarchize_1d(bfs, out, l)
+    sgh.bfs_permute_1d(out, back, l, to_bfs=False)
+    torch.cuda.synchronize()
+    assert_bitwise(back.cpu().numpy(), oracle.hierarchize(u.copy(), (l,)))
+    sgh.bfs_dehierarchize_1d(bfs, l)
+    sgh.bfs_permute_1d(bfs, back, l, to_bfs=False)
+    torch.cuda.synchronize()
+    assert_bitwise(back.cpu().numpy(), oracle.dehierarchize(u.copy(), (l,)))
+
+
+# ------------------------------------------- ablation: reduced-op (report only)
+REDOP_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1309_0392_b200", "lib",
+                         "libsgh_redop.so")
+
+
+@pytest.mark.skipif(not os.path.exists(REDOP_LIB), reason="libsgh_redop.so not built (__graft_entry__.build())")
+def test_reduced_op_ablation_normwise(sgh):
+    """the paper's reduced-op update x - 0.5 (L + R),
+    built as a second library (-DSGH_REDUCED_OP, every update site through one
+    macro).  It rounds differently from Alg. 1's two subtractions (reading
+    R5), so it is NOT bitwise equal to the oracle, but within the normwise
+    1e-13 of reading R10 on every kernel kind the shapes reach."""
+    import ctypes
+    L = ctypes.CDLL(REDOP_LIB)
+    L.sgh_hierarchize.restype = ctypes.c_int
+    L.sgh_hierarchize.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.c_void_p]
+    differs = 0
+    for levels in [(5, 5), (12,), (8, 8, 8), (6, 6, 5, 5), (10, 4, 4, 4), (14, 3), (2, 7, 11, 2)]:
+        N = si.num_points(levels)
+        u = si.fill_uniform(N, grid_id=N % 991)
+        g = torch.from_numpy(u).cuda()
+        lv = (ctypes.c_int32 * len(levels))(*levels)
+        assert L.sgh_hierarchize(ctypes.c_void_p(g.data_ptr()), lv, len(levels),
+                                 ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+        torch.cuda.synchronize()
+        got = g.cpu().numpy()
+        want = oracle.hierarchize(u.copy(), levels)
+        assert np.max(np.abs(got - want)) / np.max(np.abs(want)) <= 1e-13, levels
+        differs += int(np.count_nonzero(_bits(got) != _bits(want)))
+    assert differs > 0, "the reduced-op build should round differently from Alg. 1"
+
