@@ -337,7 +337,9 @@ def test_batched_c5_sample_vs_oracle(sgh, fuse, inverse):
 
 def test_batched_c5_full_golden(sgh):
     """The whole C5 set (4,255 grids, 41 GB) in one batched call: per-grid
-    digests summed == survey golden sums; four members == golden digests."""
+    digests summed == survey golden sums; four members == golden digests;
+    then dehierarchization (of the hierarchized set, and of the fill) over the
+    whole set against the oracle's digest sums."""
     cs = si.combination_set(4, 22)
     free, _ = torch.cuda.mem_get_info()
     if free < 46e9:
@@ -356,6 +358,15 @@ def test_batched_c5_full_golden(sgh):
     for gid in (0, 1, 834, 2000, 4254):                # round trip, normwise (reading R10)
         u = torch.from_numpy(oracle.fill_uniform(si.num_points(cs[gid]), SD["seed"], gid)).cuda()
         assert float((b.views[gid] - u).abs().max() / u.abs().max()) <= 1e-13
+    # the round trip over the WHOLE set, bitwise: the sum of the per-grid digests
+    # equals the oracle's (tests/golden/c5_oracle_digests.json, written by
+    # scripts/golden/c5_oracle_digests.py from oracle/ only)
+    od = json.load(open(os.path.join(GOLD, "c5_oracle_digests.json")))
+    assert sum(b.digests()) % (1 << 64) == int(od["sum_round_trip"], 16)
+    # dehierarchization of the fill over the whole set, bitwise
+    b.fill_uniform(SD["seed"])
+    b.dehierarchize()
+    assert sum(b.digests()) % (1 << 64) == int(od["sum_dehierarchized_fill"], 16)
 
 
 def test_batched_host_e2e(sgh):
