@@ -72,6 +72,16 @@ def d_eff(levels):
     return sum(1 for l in levels if l > 1)
 
 
+def c5_partition(sgh, members, nparts, inverse=False):
+    """Grids over ranks: LPT by the planner's estimated time per grid
+    (sgh_plan_cost: bytes per pass over each kernel's measured rate), not by
+    points -- grids of equal size differ in passes and kernels (a one-GPU
+    projection of N = 8, scripts/scale_projection.py, had rank times 3.87 to
+    4.17 ms with points balanced to 4e-5)."""
+    import sgh_inputs as si
+    return si.lpt_partition([sgh.plan_cost(lv, inverse=inverse) for lv in members], nparts)
+
+
 def plan_passes(sgh, members, inverse, fuse):
     """HBM round trips per point of the library's plans (sgh_plan_describe:
     points each phase writes, summed over the phases, / grid points)."""
@@ -257,9 +267,11 @@ def dry_run(args, rank, world, local_rank):
     if args.impl == "reference":
         info["path"] = "oracle on host cores (rank 0 only)" if rank == 0 else "idle (rank > 0)"
     elif args.workload == "C5" and world > 1:
-        part = si.lpt_partition(sizes, world)[rank]
-        info.update(path="C5 grids LPT-balanced by point count, batched transform, no data-path collective",
-                    grids=len(part), points=sum(sizes[i] for i in part))
+        import paper_1309_0392_b200 as sgh
+        part = c5_partition(sgh, members, world, args.inverse)[rank]
+        info.update(path="C5 grids LPT-balanced by planned time, batched transform, no data-path collective",
+                    grids=len(part), points=sum(sizes[i] for i in part),
+                    planned_ns=sum(sgh.plan_cost(members[i], inverse=args.inverse) for i in part))
     elif args.workload == "C4" and world > 1:
         import paper_1309_0392_b200 as sgh
         b, e = sgh.shard_rows(members[0], world, rank)
@@ -320,7 +332,7 @@ def sgh_arm(args, rank, world, local_rank):
     sizes = [si.num_points(l) for l in members]
     sharded = args.workload == "C4" and world > 1
     if args.workload == "C5" and world > 1:
-        part = si.lpt_partition(sizes, world)[rank]
+        part = c5_partition(sgh, members, world, args.inverse)[rank]
         my_members, my_ids = [members[i] for i in part], [ids[i] for i in part]
     elif args.workload == "C5cycle" and world > 1:   # the gather chain needs contiguous grid blocks
         b0, b1 = si.contiguous_partition(sizes, world)[rank]
@@ -496,7 +508,7 @@ def sgh_arm(args, rank, world, local_rank):
                "config": {"workload": desc, "points": total_points, "bytes": 8 * total_points,
                           "l2": ("L2 flushed before every step (256 MB write, outside the per-step events)"
                                  if flush_l2 else "inputs larger than L2 (no flush needed)"),
-                          "parallelism": (f"grids LPT-balanced over {world} ranks" if args.workload == "C5" else
+                          "parallelism": (f"grids LPT-balanced by planned time over {world} ranks" if args.workload == "C5" else
                                           f"contiguous grid blocks over {world} ranks, gather chain + broadcast"
                                           if args.workload == "C5cycle"
                                           else ((f"sharded along x_d, {'halo + coarse-lattice all-gather' if args.sharded == 'halo' else 'NCCL all-to-all'}")

@@ -266,6 +266,12 @@ sgh_status sgh_ablation_bfs_permute_1d(const double *src, double *dst, int32_t l
 sgh_status sgh_ablation_bfs_hierarchize_1d(const double *in, double *out, int32_t l, void *stream);
 sgh_status sgh_ablation_bfs_dehierarchize_1d(double *grid, int32_t l, void *stream);
 
+/* The planner's estimate of a grid's transform time in ns (its cost model:
+ * 16 B per point and pass over each kernel kind's measured B200 rate), host
+ * only; -1 on invalid arguments.  Used to balance grids over ranks by time
+ * rather than points (bench.py, C5 with N > 1). */
+double sgh_plan_cost(const int32_t *levels, int32_t d, uint32_t flags);
+
 /* Optional per-launch timing of the transform kernels (process-wide).
  * sgh_profile_enable(1) clears the record list and starts recording: every
  * transform kernel launch is bracketed by two CUDA events on its own stream.

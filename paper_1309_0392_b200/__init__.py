@@ -91,6 +91,7 @@ def _load():
         "sgh_digest_batched": (st, [vpp, i64p, ctypes.c_int64, u64p, vp, sz, vp]),
         "sgh_launch_count": (ctypes.c_uint64, []),
         "sgh_plan_describe": (ctypes.c_int64, [i32p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_char_p, sz]),
+        "sgh_plan_cost": (ctypes.c_double, [i32p, ctypes.c_int32, ctypes.c_uint32]),
         "sgh_sparse_num_points": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
         "sgh_combi_workspace_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32]),
         "sgh_gather": (st, [vpp, i32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64,
@@ -124,7 +125,7 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_sharded_halo_workspace_bytes",
             "sgh_transform_sharded_halo", "sgh_transform_sharded_halo_loopback", "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
-            "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_sparse_num_points",
+            "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_plan_cost", "sgh_sparse_num_points",
             "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter", "sgh_gather_ex",
             "sgh_sparse_num_subspaces", "sgh_sparse_subspace_offset", "sgh_ablation_bfs_permute_1d",
             "sgh_ablation_bfs_hierarchize_1d", "sgh_ablation_bfs_dehierarchize_1d",
@@ -201,6 +202,15 @@ def plan_describe(levels: Sequence[int], inverse: bool = False, fuse=True) -> st
     buf = ctypes.create_string_buffer(n + 1)
     lib.sgh_plan_describe(a, d, fl, buf, n + 1)
     return buf.value.decode()
+
+
+def plan_cost(levels: Sequence[int], inverse: bool = False, fuse=True) -> float:
+    """The planner's estimated transform time of one grid, ns (host-only)."""
+    a, d = _levels_arr(levels)
+    c = float(lib.sgh_plan_cost(a, d, ctypes.c_uint32(_flags(inverse, fuse))))
+    if c < 0:
+        raise ValueError(f"invalid levels {tuple(levels)}")
+    return c
 
 
 def transform(grid: torch.Tensor, levels: Sequence[int], *, inverse: bool = False, axis_order=None,

@@ -1341,6 +1341,18 @@ int64_t sgh_plan_describe(const int32_t *levels, int32_t d, uint32_t flags, char
 });
 }
 
+double sgh_plan_cost(const int32_t *levels, int32_t d, uint32_t flags) {
+  return guarded_value<double>(-1.0, [&]() -> double {
+  int64_t N = 0;
+  if (validate_levels(levels, d, &N) != SGH_OK || (flags & ~kKnownFlags)) return -1.0;
+  std::vector<std::vector<Task>> passes;
+  plan_grid(nullptr, levels, d, flags & kPlanFlags, passes);
+  double c = 0;
+  for (const auto &ph : passes) c += pass_cost(ph);
+  return c * double(N) * 16e-3;                       // 16 B per point and pass / (TB/s) -> ns
+});
+}
+
 uint64_t sgh_launch_count(void) { return g_launches.load(); }
 
 const char *sgh_status_string(sgh_status s) {
