@@ -874,6 +874,14 @@ struct BatchedPlan {
   std::vector<Segment> segs;
   std::vector<unsigned char> image;   // the device table image (built once per cached plan)
   void *resident_ws = nullptr;        // the workspace this plan's table was last uploaded to
+  // the plan's launches captured into a CUDA graph for `graph_ws` on `graph_dev`
+  cudaGraphExec_t gexec = nullptr;
+  void *graph_ws = nullptr;
+  int graph_dev = -1;
+  std::mutex graph_mu;
+  ~BatchedPlan() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
   size_t table_bytes() const {
     return (tasks.size() * sizeof(Task) + 255) / 256 * 256 + prefix.size() * sizeof(int64_t);
   }
@@ -991,6 +999,24 @@ struct ConcStreams {
 static std::mutex g_conc_mu;
 static std::map<int, ConcStreams> g_conc;
 
+#ifndef SGH_GRAPHS
+#define SGH_GRAPHS 1
+#endif
+constexpr bool kGraphs = SGH_GRAPHS != 0;
+static std::map<int, cudaStream_t> g_capture;
+
+// a private stream per device to capture a plan's launches on
+static sgh_status capture_stream(cudaStream_t &out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_conc_mu);
+  cudaStream_t &c = g_capture[dev];
+  if (!c && (e = cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+  out = c;
+  return SGH_OK;
+}
+
 static sgh_status conc_streams(ConcStreams *&out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -1072,50 +1098,94 @@ sgh_status run_batched(double *const *grids, const int32_t *levels, int32_t d, i
     std::memcpy(host.data(), P.tasks.data(), P.tasks.size() * sizeof(Task));
     std::memcpy(host.data() + prefix_base, P.prefix.data(), P.prefix.size() * sizeof(int64_t));
   }
+  bool uploaded = false;
   if (!((flags & SGH_FLAG_TABLE_RESIDENT) && plan->resident_ws == workspace)) {
     st = staged_upload(workspace, plan->image.data(), bytes, s);
     if (st != SGH_OK) return st;
     plan->resident_ws = workspace;
+    uploaded = true;
   }
   const Task *d_tasks = reinterpret_cast<const Task *>(workspace);
   const int64_t *d_prefix = reinterpret_cast<const int64_t *>(static_cast<unsigned char *>(workspace) + prefix_base);
-  // The segments of one (round, phase) stage touch disjoint grids: with
-  // kConcurrent (-DSGH_CONCURRENT=1), a stage's launches go to library
-  // streams forked from and joined back into `s`, so one kernel's tail
-  // overlaps the next ones.  Measured slower on C5 (169.2 vs 170-171, dehier
-  // 152.9 vs 155.0: the overlapping kernels compete), so off by default.
-  ConcStreams *cs = nullptr;
-  if (kConcurrent && (st = conc_streams(cs)) != SGH_OK) return st;
-  for (size_t a = 0; a < P.segs.size();) {
-    size_t b = a + 1;
-    while (b < P.segs.size() && P.segs[b].stage == P.segs[a].stage) ++b;
-    const bool fork = kConcurrent && b - a > 1;
-    if (fork) {
-      cudaEventRecord(cs->fork, s);
-      for (size_t i = 0; i < b - a && i < ConcStreams::kN; ++i) cudaStreamWaitEvent(cs->st[i], cs->fork, 0);
-    }
-    for (size_t i = a; i < b; ++i) {
-      const Segment &sg = P.segs[i];
-      cudaStream_t ls = fork ? cs->st[(i - a) % ConcStreams::kN] : s;
-      cudaError_t e = launch_table(sg.kind, sg.l, sg.w, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off,
-                                   sg.ntasks, sg.tiles, sg.smem, sg.points, ls, sg.variant, sg.pipe);
-      if (e != cudaSuccess) {
-        char where[160];
-        std::snprintf(where, sizeof where, "grouped kernel launch (kind %d, W %d, l %d, variant %d, %s, %d tasks)",
-                      sg.kind, sg.w, sg.l, sg.variant, sg.pipe ? "k_fpipe" : "k_fused/per-axis", sg.ntasks);
-        return cuda_fail(e, where);
+  auto launch_all = [&](cudaStream_t s) -> sgh_status {
+    // The segments of one (round, phase) stage touch disjoint grids: with
+    // kConcurrent (-DSGH_CONCURRENT=1), a stage's launches go to library
+    // streams forked from and joined back into `s`, so one kernel's tail
+    // overlaps the next ones.  Measured slower on C5 (169.2 vs 170-171, dehier
+    // 152.9 vs 155.0: the overlapping kernels compete), so off by default.
+    ConcStreams *cs = nullptr;
+    if (kConcurrent && (st = conc_streams(cs)) != SGH_OK) return st;
+    for (size_t a = 0; a < P.segs.size();) {
+      size_t b = a + 1;
+      while (b < P.segs.size() && P.segs[b].stage == P.segs[a].stage) ++b;
+      const bool fork = kConcurrent && b - a > 1;
+      if (fork) {
+        cudaEventRecord(cs->fork, s);
+        for (size_t i = 0; i < b - a && i < ConcStreams::kN; ++i) cudaStreamWaitEvent(cs->st[i], cs->fork, 0);
       }
-      count_launch();
-    }
-    if (fork) {
-      for (size_t i = 0; i < b - a && i < ConcStreams::kN; ++i) {
-        cudaEventRecord(cs->join[i], cs->st[i]);
-        cudaStreamWaitEvent(s, cs->join[i], 0);
+      for (size_t i = a; i < b; ++i) {
+        const Segment &sg = P.segs[i];
+        cudaStream_t ls = fork ? cs->st[(i - a) % ConcStreams::kN] : s;
+        cudaError_t e = launch_table(sg.kind, sg.l, sg.w, inv, d_tasks + sg.task_off, d_prefix + sg.prefix_off,
+                                     sg.ntasks, sg.tiles, sg.smem, sg.points, ls, sg.variant, sg.pipe);
+        if (e != cudaSuccess) {
+          char where[160];
+          std::snprintf(where, sizeof where, "grouped kernel launch (kind %d, W %d, l %d, variant %d, %s, %d tasks)",
+                        sg.kind, sg.w, sg.l, sg.variant, sg.pipe ? "k_fpipe" : "k_fused/per-axis", sg.ntasks);
+          return cuda_fail(e, where);
+        }
+        count_launch();
       }
+      if (fork) {
+        for (size_t i = 0; i < b - a && i < ConcStreams::kN; ++i) {
+          cudaEventRecord(cs->join[i], cs->st[i]);
+          cudaStreamWaitEvent(s, cs->join[i], 0);
+        }
+      }
+      a = b;
     }
-    a = b;
+    return SGH_OK;
+  };
+  // CUDA graph replay (kGraphs): a repeated call on a resident table (the
+  // combination technique's every iteration; bench.py's timed steps) replays
+  // the plan's ~36 launches as one graph instead of launching them from the
+  // host one by one.  The first resident call captures them (on a private
+  // stream: capture is not allowed on the legacy default stream) and launches
+  // the graph; later ones only launch it.  Not while per-launch profiling is
+  // on (those launches carry events).
+  if (kGraphs && !prof_active() && (flags & SGH_FLAG_TABLE_RESIDENT) && !uploaded) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(plan->graph_mu);
+    if (!(plan->gexec && plan->graph_ws == workspace && plan->graph_dev == dev)) {
+      cudaStream_t cap = nullptr;
+      if ((st = capture_stream(cap)) != SGH_OK) return st;
+      if ((e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+        return cuda_fail(e, "cudaStreamBeginCapture");
+      sgh_status lst = launch_all(cap);
+      cudaGraph_t g = nullptr;
+      e = cudaStreamEndCapture(cap, &g);
+      if (lst != SGH_OK) {
+        if (g) cudaGraphDestroy(g);
+        return lst;
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      cudaGraphExec_t x = nullptr;
+      e = cudaGraphInstantiate(&x, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+      if (plan->gexec) cudaGraphExecDestroy(plan->gexec);
+      plan->gexec = x;
+      plan->graph_ws = workspace;
+      plan->graph_dev = dev;
+    } else {
+      count_launch(P.segs.size());
+    }
+    if ((e = cudaGraphLaunch(plan->gexec, s)) != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+    return SGH_OK;
   }
-  return SGH_OK;
+  return launch_all(s);
 }
 
 // per-device scratch for single-grid digests (allocated once, not in a hot call)

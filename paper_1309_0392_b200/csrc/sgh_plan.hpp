@@ -30,6 +30,7 @@ ProfToken prof_begin(cudaStream_t s);
 // variant: 0 dense / per-axis, 1 BLOCKED fused tiles, 2 coarse-lattice views of a
 // blocked group, 3 a grouped launch mixing 1 and 2
 void prof_end(ProfToken tok, int kind, int l, bool inv, double bytes, cudaStream_t s, int variant = 0);
+bool prof_active();                   // per-launch profiling on (sgh_profile_enable(1))
 inline int task_variant(const Task &t) {
   if (t.kind != KIND_FUSED || t.bj < 0) return 0;
   return t.bt < t.gl[t.bj] ? 1 : 2;

@@ -42,6 +42,11 @@ static cudaEvent_t take_event() {
   return e;
 }
 
+bool prof_active() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  return g_prof_on;
+}
+
 ProfToken prof_begin(cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (!g_prof_on) return ProfToken{nullptr};
