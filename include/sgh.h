@@ -362,6 +362,18 @@ int64_t sgh_sparse_subspace_offset(int32_t d, int32_t n, int64_t index);
 sgh_status sgh_scatter(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids, int32_t n,
                        const double *sparse, void *workspace, size_t ws_bytes, void *stream);
 
+/* Host-only: the HBM bytes (16 B per point written by a kernel or copied on
+ * the device) one sharded call plans for rank `rank` of `nranks` -- the local
+ * axes 1..d-1 of its row shard (planned like a whole grid: fused / blocked
+ * groups over the stacked (d-1)-dimensional rows), then path 0 (all-to-all,
+ * sgh_hierarchize_sharded): pack + unpack copies and the slab pass along x_d;
+ * path 1 (halo, sgh_transform_sharded_halo): the super-block interior, the
+ * gathered coarse rows and the halo / coarse row copies.  Network bytes are
+ * not included.  flags: 0 or SGH_FLAG_DEHIERARCHIZE.  -1 on invalid
+ * arguments.  SURVEY 8(a) a7 / 8(f) 1. */
+double sgh_sharded_plan_bytes(const int32_t *levels, int32_t d, int32_t nranks, int32_t rank, uint32_t flags,
+                              int32_t path);
+
 /* Host-only description of the plan the library would run for one grid with
  * these flags (no CUDA call): one line per pass ("pass k:"), then one line per
  * phase with its kernel kind, tile width, special axis / block level and the

@@ -92,6 +92,8 @@ def _load():
         "sgh_launch_count": (ctypes.c_uint64, []),
         "sgh_plan_describe": (ctypes.c_int64, [i32p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_char_p, sz]),
         "sgh_plan_cost": (ctypes.c_double, [i32p, ctypes.c_int32, ctypes.c_uint32]),
+        "sgh_sharded_plan_bytes": (ctypes.c_double, [i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                                     ctypes.c_uint32, ctypes.c_int32]),
         "sgh_sparse_num_points": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
         "sgh_combi_workspace_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32]),
         "sgh_gather": (st, [vpp, i32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64,
@@ -125,7 +127,7 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_sharded_halo_workspace_bytes",
             "sgh_transform_sharded_halo", "sgh_transform_sharded_halo_loopback", "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
-            "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_plan_cost", "sgh_sparse_num_points",
+            "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_plan_cost", "sgh_sharded_plan_bytes", "sgh_sparse_num_points",
             "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter", "sgh_gather_ex",
             "sgh_sparse_num_subspaces", "sgh_sparse_subspace_offset", "sgh_ablation_bfs_permute_1d",
             "sgh_ablation_bfs_hierarchize_1d", "sgh_ablation_bfs_dehierarchize_1d",
@@ -211,6 +213,19 @@ def plan_cost(levels: Sequence[int], inverse: bool = False, fuse=True) -> float:
     if c < 0:
         raise ValueError(f"invalid levels {tuple(levels)}")
     return c
+
+
+def sharded_plan_bytes(levels: Sequence[int], nranks: int, rank: int, *, inverse: bool = False,
+                       path: str = "halo") -> float:
+    """HBM bytes one sharded call plans on rank `rank` (host-only; network
+    bytes excluded): path "a2a" (sgh_hierarchize_sharded) or "halo"
+    (sgh_transform_sharded_halo)."""
+    a, d = _levels_arr(levels)
+    b = float(lib.sgh_sharded_plan_bytes(a, d, nranks, rank, ctypes.c_uint32(1 if inverse else 0),
+                                         {"a2a": 0, "halo": 1}[path]))
+    if b < 0:
+        raise ValueError(f"invalid sharded configuration {tuple(levels)} nranks={nranks} rank={rank}")
+    return b
 
 
 def transform(grid: torch.Tensor, levels: Sequence[int], *, inverse: bool = False, axis_order=None,

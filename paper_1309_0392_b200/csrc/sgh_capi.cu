@@ -157,8 +157,17 @@ void plan_view(double *grid, int64_t O, int64_t OS, int64_t PS, int64_t S, int64
   if (tb < l) plan_view(grid, O, OS, PS << tb, S, base + ((int64_t(1) << tb) - 1) * PS, l - tb, phases);
 }
 
+// Outer multiplier of the planner (1 = a whole grid).  The sharded paths plan
+// a row shard of x_d as `rows` consecutive (d-1)-dimensional grids: every
+// planned view's outer count O (units beyond its axis group, dense at stride
+// OS with O * OS = the grid's extent) is multiplied by it, which extends the
+// view over the stacked copies.  Two-blocked plans (whose outer index is split,
+// O1 / OS2) are not used while it is set.  Thread-local: set it only through
+// plan_grid_rows.
+static thread_local int64_t g_outer_mult = 1;
+
 void plan_axis(double *grid, const int32_t *levels, int d, int k, std::vector<Task> &phases, int64_t rows_last) {
-  int64_t S = 1, O = 1;
+  int64_t S = 1, O = g_outer_mult;
   for (int j = 0; j < k; ++j) S *= (int64_t(1) << levels[j]) - 1;
   for (int j = k + 1; j < d; ++j) O *= (j == d - 1 && rows_last >= 0) ? rows_last : (int64_t(1) << levels[j]) - 1;
   const int64_t n = (int64_t(1) << levels[k]) - 1;
@@ -216,7 +225,7 @@ static void finish_fused(Task &t) {
 
 static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, int b, Task &t) {
   const int64_t kFusedT = fused_budget();
-  int64_t Sa = 1, P = 1, O = 1;
+  int64_t Sa = 1, P = 1, O = g_outer_mult;
   int busy = 0;
   for (int k = 0; k < a; ++k) Sa *= (int64_t(1) << levels[k]) - 1;
   for (int k = a; k < b; ++k) {
@@ -282,7 +291,7 @@ static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a
                                std::vector<Task> &phases) {
   const int64_t budget = W == 1 ? fused_budget_w1() + fused_budget_w1() / 16 : fused_budget() + fused_budget() / 16;
   if (b - a > 16 || b - a < 2 || levels[j] < 3) return false;
-  int64_t Sa = 1, O = 1, Prest = 1, A = 1;
+  int64_t Sa = 1, O = g_outer_mult, Prest = 1, A = 1;
   for (int k = 0; k < a; ++k) Sa *= (int64_t(1) << levels[k]) - 1;
   for (int k = b; k < d; ++k) O *= (int64_t(1) << levels[k]) - 1;
   int busy = 0;
@@ -552,6 +561,178 @@ static bool plan_two_blocked(double *grid, const int32_t *levels, int d, int a, 
   return ok;
 }
 
+static double kind_bw(const Task &t);
+
+// ------------------------------------------- PREFIX TWO-BLOCKED plans (hier)
+// Grids with >= 3 non-trivial axes (trivial axes squeezed out: same layout):
+// the last two axes a, b are cut into aligned blocks, the axes before them
+// (the prefix, P0 points) stay whole poles, and ONE pass of box tiles
+// (P0 x (2^ta + 1) x (2^tb + 1) points) writes every point that is fine along
+// both (the SURVEY 8(a) a4 block scheme with the prefix axes carried along).
+// The rest is partitioned by the set C of blocked axes a point is coarse along;
+// class C's tiles hold the coarse lattice (stride 2^t) along the axes in C and
+// the same blocks + ends along the others, run the prefix axes, then a, then b
+// (the oracle's order: bitwise), and write only the class's points.
+// Class C reads original values of the classes containing C only, so running
+// the classes by increasing C (main, {a}, {b}, {a,b}) is in-place safe
+// (SURVEY H2).  A class whose lattice does not fit a tile is itself a box
+// problem with the other axis restricted to its fine points (solve_box,
+// recursive).  Hierarchization only: the inverse would need the block ends
+// half-transformed (cf. split_inverse_lattice).
+struct BoxAxis {
+  int l;            // level of the view (n = 2^l - 1 points)
+  int64_t G, base;  // global stride of its points and offset of its first point
+  int f;            // only points with tz(i) < f are written (f == l: all)
+};
+struct BoxCtx {
+  double *grid;
+  int np;           // prefix axes (whole poles)
+  int8_t pl[16];    // their levels
+  int64_t P0;       // their points (odd)
+  int64_t budget;   // tile points
+  int64_t N;        // grid points
+};
+
+static Task box_task(const BoxCtx &c, const BoxAxis &a, int ta, const BoxAxis &b, int tb) {
+  Task t;
+  std::memset(&t, 0, sizeof t);
+  t.grid = c.grid;
+  t.kind = KIND_FUSED;
+  t.m = c.np + 2;
+  int64_t R = 1;
+  for (int j = 0; j < c.np; ++j) {
+    t.gl[j] = c.pl[j];
+    t.gR[j] = (int32_t)R;
+    t.fR[j] = make_fdiv((uint32_t)R);
+    R *= (int64_t(1) << c.pl[j]) - 1;
+  }
+  const bool ba = ta < a.l, bb = tb < b.l;
+  const int64_t ea = ba ? (int64_t(1) << ta) + 1 : (int64_t(1) << a.l) - 1;
+  const int64_t eb = bb ? (int64_t(1) << tb) + 1 : (int64_t(1) << b.l) - 1;
+  t.gl[c.np] = (int8_t)a.l;
+  t.gR[c.np] = (int32_t)R;
+  t.fR[c.np] = make_fdiv((uint32_t)R);
+  R *= ea;
+  t.gl[c.np + 1] = (int8_t)b.l;
+  t.gR[c.np + 1] = (int32_t)R;
+  t.fR[c.np + 1] = make_fdiv((uint32_t)R);
+  R *= eb;
+  t.P = (int32_t)R;
+  t.S = 1;
+  t.O = 1;
+  t.OS = c.N;
+  t.base = a.base + b.base;
+  t.l = t.gl[0];
+  t.W = 1;
+  t.R = 1;
+  t.bj = c.np;
+  t.bt = ba ? ta : a.l;                              // >= gl[bj]: whole (lattice) poles
+  t.nb_log = ba ? a.l - ta : 0;
+  t.A = (int32_t)c.P0;
+  t.ej = (int32_t)ea;
+  t.fA = make_fdiv((uint32_t)c.P0);
+  t.fE = make_fdiv((uint32_t)ea);
+  t.Gj = a.G;
+  t.Gnext = b.G;
+  t.bt2 = bb ? tb : -1;
+  t.nb2_log = bb ? b.l - tb : 0;
+  t.aligned = ((t.Gj & 1) == (t.A & 1)) && ((t.Gnext & 1) == ((int64_t(t.A) * t.ej) & 1));
+  t.ncb = 1;
+  t.tiles = int64_t(1) << (t.nb_log + t.nb2_log);
+  finish_fused(t);
+  return t;
+}
+
+// relative time of a phase list (1 = one pass over the grid at 1 TB/s)
+static double box_cost(const BoxCtx &c, const std::vector<Task> &ph, size_t from) {
+  double cost = 0;
+  for (size_t i = from; i < ph.size(); ++i) {
+    const double f = task_points(ph[i]) / double(c.N);
+    cost += f / (i == 0 ? kind_bw(ph[i]) : 0.7 * kind_bw(ph[i])) + 0.01;
+  }
+  return cost;
+}
+
+// Append the phases of box problem (a, b) to `out` (execution order).  False
+// if some class finds no tile that fits within `depth` levels of recursion.
+static bool solve_box(const BoxCtx &c, const BoxAxis &a, const BoxAxis &b, int depth, std::vector<Task> &out,
+                      bool both_blocked = false) {
+  auto options = [](const BoxAxis &x) {
+    std::vector<int> o;
+    if (x.f < x.l) {                                 // fine-only axis: the given blocks
+      o.push_back(x.f);
+      return o;
+    }
+    o.push_back(x.l);                                // whole poles, then blocks large -> small
+    for (int t = x.l - 1; t >= 2; --t) o.push_back(t);
+    return o;
+  };
+  auto extent = [](const BoxAxis &x, int t) {
+    return t < x.l ? (int64_t(1) << t) + 1 : (int64_t(1) << x.l) - 1;
+  };
+  double best = 1e30;
+  std::vector<Task> bestv;
+  for (int ta : options(a)) {
+    const int64_t ea = extent(a, ta);
+    if (c.P0 * ea > c.budget) continue;
+    if (both_blocked && ta == a.l) continue;
+    for (int tb : options(b)) {                      // the largest block of b that fits
+      if (both_blocked && tb == b.l) continue;
+      const int64_t eb = extent(b, tb);
+      if (c.P0 * ea * eb > c.budget) continue;
+      std::vector<Task> ph{box_task(c, a, ta, b, tb)};
+      const bool ca = ta < a.l && a.f == a.l, cb = tb < b.l && b.f == b.l;
+      bool ok = depth > 0 || !(ca || cb);
+      const BoxAxis al{a.l - ta, a.G << ta, a.base + ((int64_t(1) << ta) - 1) * a.G, a.l - ta};
+      const BoxAxis bl{b.l - tb, b.G << tb, b.base + ((int64_t(1) << tb) - 1) * b.G, b.l - tb};
+      const BoxAxis af{a.l, a.G, a.base, ta}, bf{b.l, b.G, b.base, tb};
+      if (ok && ca) ok = solve_box(c, al, bf, depth - 1, ph);
+      if (ok && cb) ok = solve_box(c, af, bl, depth - 1, ph);
+      if (ok && ca && cb) ok = solve_box(c, al, bl, depth - 1, ph);
+      if (ok) {
+        const double cost = box_cost(c, ph, 0);
+        if (cost < best) {
+          best = cost;
+          bestv.swap(ph);
+        }
+      }
+      break;
+    }
+  }
+  if (bestv.empty()) return false;
+  out.insert(out.end(), bestv.begin(), bestv.end());
+  return true;
+}
+
+// force: both blocked axes in blocks at the top level (SGH_FLAG_TWO_BLOCKED, tests)
+static bool plan_prefix_two_blocked(double *grid, const int32_t *levels, int d, std::vector<Task> &phases,
+                                    bool force = false) {
+  int sq[SGH_MAX_D], m = 0;
+  for (int k = 0; k < d; ++k)
+    if (levels[k] > 1) sq[m++] = levels[k];
+  if (m < 3 || sq[m - 2] < 3 || sq[m - 1] < 3) return false;
+  BoxCtx c;
+  c.grid = grid;
+  c.np = m - 2;
+  c.P0 = 1;
+  for (int j = 0; j < c.np; ++j) {
+    c.pl[j] = (int8_t)sq[j];
+    c.P0 *= (int64_t(1) << sq[j]) - 1;
+  }
+  c.budget = fused_budget_w1() + fused_budget_w1() / 16;
+  if (c.P0 * 25 > c.budget) return false;            // not even 5 x 5 blocks
+  const int64_t na = (int64_t(1) << sq[m - 2]) - 1;
+  c.N = c.P0 * na * ((int64_t(1) << sq[m - 1]) - 1);
+  const BoxAxis a{sq[m - 2], c.P0, 0, sq[m - 2]};
+  const BoxAxis b{sq[m - 1], c.P0 * na, 0, sq[m - 1]};
+  const size_t first = phases.size();
+  if (!solve_box(c, a, b, 3, phases, force)) {
+    phases.resize(first);
+    return false;
+  }
+  return true;
+}
+
 // Estimated time per point (1 / TB/s) of a pass, from the kernels' measured
 // B200 throughput (profiles/r01): wide contiguous tiles stream best, narrow
 // column tiles lose DRAM efficiency.
@@ -702,7 +883,7 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
     }
   }
   // two-blocked plan (grids with exactly two adjacent non-trivial axes)
-  if (blocked_ok) {
+  if (blocked_ok && g_outer_mult == 1) {
     std::vector<Task> bestp;
     // SGH_FLAG_TWO_BLOCKED: take a two-blocked plan whenever one exists (tests)
     double bc = (flags & SGH_FLAG_TWO_BLOCKED) ? 1e30 : cost[d];
@@ -721,6 +902,17 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
             bestp = ph;
           }
         }
+    // prefix two-blocked plan (hierarchization, >= 3 non-trivial axes)
+    if (!inv && g_outer_mult == 1) {
+      std::vector<Task> ph;
+      if (plan_prefix_two_blocked(grid, levels, d, ph, (flags & SGH_FLAG_TWO_BLOCKED) != 0)) {
+        const double c = pass_cost(ph);
+        if (c < bc - 1e-12) {
+          bc = c;
+          bestp = ph;
+        }
+      }
+    }
     if (!bestp.empty()) {
       passes.push_back(std::move(bestp));
       return;
@@ -736,6 +928,17 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
     else phases = best[j];
     if (!phases.empty()) passes.push_back(std::move(phases));
   }
+}
+
+// plan_grid over `outer` stacked copies of the grid (a row shard of a
+// (d+1)-dimensional grid: rows of its last axis, each one d-dimensional grid)
+void plan_grid_rows(double *grid, const int32_t *levels, int d, int64_t outer, uint32_t flags,
+                    std::vector<std::vector<Task>> &passes) {
+  struct Reset {
+    ~Reset() { g_outer_mult = 1; }
+  } reset;
+  g_outer_mult = outer < 1 ? 1 : outer;
+  plan_grid(grid, levels, d, flags, passes);
 }
 
 // ------------------------------------------------- pinned staging ring

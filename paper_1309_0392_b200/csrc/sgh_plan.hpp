@@ -127,6 +127,9 @@ size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t 
                            uint32_t flags);
 // flags: SGH_FLAG_DEHIERARCHIZE / SGH_FLAG_PER_AXIS / SGH_FLAG_WHOLE_POLES (sgh.h)
 void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::vector<std::vector<Task>> &passes);
+// plan_grid of `outer` stacked copies of the grid (a row shard of the next axis)
+void plan_grid_rows(double *grid, const int32_t *levels, int d, int64_t outer, uint32_t flags,
+                    std::vector<std::vector<Task>> &passes);
 constexpr uint32_t kKnownFlags =
     SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS | SGH_FLAG_WHOLE_POLES | SGH_FLAG_TWO_BLOCKED | SGH_FLAG_TABLE_RESIDENT;
 // flags that select the plan (the plan cache key)

@@ -483,6 +483,49 @@ sgh_status sgh_shard_layout(const int32_t *levels, int32_t d, int32_t nranks, in
 });
 }
 
+double sgh_sharded_plan_bytes(const int32_t *levels, int32_t d, int32_t nranks, int32_t rank, uint32_t flags,
+                              int32_t path) {
+  return guarded_value<double>(-1.0, [&]() -> double {
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return -1.0;
+  if (rank < 0 || rank >= nranks || (path != 0 && path != 1)) return -1.0;
+  const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
+  auto points = [](const std::vector<Task> &ph) {
+    double p = 0;
+    for (const Task &t : ph) p += task_points(t);
+    return p;
+  };
+  double pts = 0;
+  std::vector<std::vector<Task>> passes;
+  if (path == 0) {
+    ShardGeom G;
+    int64_t b, e;
+    if (validate_levels(levels, d, nullptr) != SGH_OK || shard_rows_impl(levels, d, nranks, 0, &b, &e) != SGH_OK ||
+        make_geom(levels, d, nranks, rank, G) != SGH_OK)
+      return -1.0;
+    plan_grid_rows(nullptr, G.levels, d - 1, G.rows[rank], inv ? uint32_t(SGH_FLAG_DEHIERARCHIZE) : 0u, passes);
+    for (const auto &ph : passes) pts += points(ph);
+    pts += 2.0 * double(G.rows[rank]) * double(G.C);          // pack + unpack copies
+    std::vector<Task> slab;
+    if (G.cols[rank] > 0) plan_view(nullptr, 1, G.nd * G.cols[rank], G.cols[rank], G.cols[rank], 0, G.levels[d - 1], slab);
+    pts += points(slab);
+  } else {
+    HaloGeom H;
+    if (make_halo_geom(levels, d, nranks, H) != SGH_OK) return -1.0;
+    plan_grid_rows(nullptr, H.levels, d - 1, H.rows[rank], inv ? uint32_t(SGH_FLAG_DEHIERARCHIZE) : 0u, passes);
+    for (const auto &ph : passes) pts += points(ph);
+    std::vector<Task> in;
+    if (!plan_view_range(nullptr, 1, 0, H.C, H.C, 0, H.levels[d - 1], H.T, rank, in)) return -1.0;
+    for (const Task &t : in)                                  // 2^rlog blocks of 2^t - 1 fine points each
+      pts += double(t.O) * double(t.S) * double(int64_t(1) << t.rlog) * double((int64_t(1) << t.t) - 1);
+    std::vector<Task> co;
+    plan_view(nullptr, 1, 0, H.C, H.C, H.C, H.p, co);
+    pts += points(co);
+    pts += double(H.C) * ((rank >= 1) + (rank + 1 < H.P));  // halo row in, own coarse row back
+  }
+  return 16.0 * pts;
+});
+}
+
 sgh_status sgh_comm_unique_id(void *out) {
   if (!out) return invalid("out is NULL");
   ncclUniqueId id;

@@ -192,6 +192,26 @@ def test_plan_two_blocked_available():
     assert N <= sum(x for _, _, x in q[0]) < 1.06 * N
 
 
+@pytest.mark.parametrize("levels", [(5, 7, 9), (2, 2, 9, 9), (1, 5, 7, 9), (5, 1, 7, 9), (4, 6, 8), (2, 10, 10),
+                                    (3, 4, 3), (2, 2, 2, 5, 5), (4, 4, 11)], ids=str)
+def test_plan_prefix_two_blocked_partition(levels):
+    """Prefix two-blocked hierarchization plans (>= 3 non-trivial axes): ONE
+    pass whose phases -- the box tiles (fine along both blocked axes), then
+    the classes coarse along {a}, {b}, {a, b} -- write every point exactly
+    once; the first phase is the largest (the tiles).  Dehierarchization never
+    takes it (the inverse would need half-transformed block ends)."""
+    N = si.num_points(levels)
+    p = _plan_passes(levels, fuse="two_blocked")
+    assert len(p) == 1 and int(p[0][0][1]["bt2"]) >= 2
+    pts = [x for _, _, x in p[0]]
+    assert sum(pts) == N and pts[0] == max(pts)
+    sq = [l for l in levels if l > 1]
+    assert all(a["levels"].count(",") == len(sq) - 1 for _, a, _ in p[0])
+    q = _plan_passes(levels, inverse=True, fuse="two_blocked")
+    assert all(len(ph) == 0 or ph[0][1].get("levels", "").count(",") < len(sq) - 1 or
+               int(ph[0][1].get("bt2", "-1")) < 0 for ph in q)
+
+
 def test_plan_two_blocked_forced():
     """SGH_FLAG_TWO_BLOCKED (fuse="two_blocked") selects the two-blocked plan
     wherever one exists (how the GPU parity tests exercise it)."""

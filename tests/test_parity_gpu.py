@@ -259,6 +259,23 @@ def test_two_blocked_dehier_bitwise(sgh, levels):
                    oracle.dehierarchize(h.copy(), levels))
 
 
+PREFIX_TWO_BLOCKED_SHAPES = [(5, 7, 9), (2, 2, 9, 9), (1, 5, 7, 9), (5, 1, 7, 9), (4, 6, 8), (3, 3, 8, 7),
+                             (2, 10, 10), (5, 5, 5), (3, 4, 3), (2, 2, 2, 5, 5), (3, 9, 4), (4, 4, 11)]
+
+
+@pytest.mark.parametrize("levels", PREFIX_TWO_BLOCKED_SHAPES, ids=str)
+def test_prefix_two_blocked_bitwise(sgh, levels):
+    """Prefix two-blocked hierarchization (grids with >= 3 non-trivial axes:
+    prefix axes whole, the last two in aligned blocks, then the classes of
+    points coarse along {a}, {b}, {a, b}, recursively) forced with
+    fuse="two_blocked": bitwise vs the oracle."""
+    N = si.num_points(levels)
+    u = si.fill_uniform(N, grid_id=N % 991)
+    assert "bt2=" in sgh.plan_describe(levels, fuse="two_blocked")
+    want = oracle.hierarchize(u.copy(), levels)
+    assert_bitwise(gpu_transform(sgh, u, levels, fuse="two_blocked"), want)
+
+
 def test_two_blocked_c4_golden(sgh):
     c = SD["configs"]["C4"]
     g = torch.empty(si.num_points(c["levels"]), dtype=torch.float64, device="cuda")
