@@ -223,6 +223,27 @@ static void finish_fused(Task &t) {
   }
 }
 
+// PADDED SMEM layout (Task::sy / sz) for W == 1 special-axis tasks whose tile
+// rows do not keep the global 8-byte phase in the dense layout (coarse-lattice
+// views: Gj even, A odd): rows of the special axis at an SMEM pitch sy of
+// Gj's parity, rows after it at a pitch sz of Gnext's parity, so every run
+// starts at its global phase and the task loads / stores with 16-byte and
+// bulk copies (`aligned`).  Runs of one element (A == 1) keep 8-byte copies.
+static void pad_layout(Task &t) {
+  t.sy = t.sz = 0;
+  if (t.kind != KIND_FUSED || t.W != 1 || t.bj < 0 || t.aligned || t.A <= 1) return;
+  static const bool no_pad = tuning_env("SGH_NO_PAD") != nullptr;   // experiment
+  if (no_pad) return;
+  const int64_t sy = t.A + ((t.A ^ t.Gj) & 1);
+  const int64_t ez = t.P / (int64_t(t.A) * t.ej);
+  int64_t sz = sy * t.ej;
+  if (ez > 1 && ((sz ^ t.Gnext) & 1)) ++sz;
+  if (ez * sz + 2 > int64_t(kFusedT1) + kFusedT1 / 8) return;   // the SMEM stage: keep 8-byte copies
+  t.sy = (int32_t)sy;
+  t.sz = (int32_t)sz;
+  t.aligned = 1;
+}
+
 static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, int b, Task &t) {
   const int64_t kFusedT = fused_budget();
   int64_t Sa = 1, P = 1, O = g_outer_mult;
@@ -360,6 +381,7 @@ static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a
     // to follow the SMEM one: rows x + A (y + ej z) at x S + y Gj + z Gnext with
     // S, A odd (products of odd extents) -> Gj odd and Gnext = ej (mod 2).
     t.aligned = ((Gj & 1) == (A & 1)) && (Gnext == 0 || (Gnext & 1) == ((A * ej) & 1));
+    pad_layout(t);
     t.ncb = (W > 1) ? (Sa + W - 1) / W : 1;
     t.tiles = (O << t.nb_log) * t.ncb;
     if (lj <= 1 && busy - (levels[j] > 1) == 0) break;   // nothing left to transform
@@ -637,6 +659,7 @@ static Task box_task(const BoxCtx &c, const BoxAxis &a, int ta, const BoxAxis &b
   t.bt2 = bb ? tb : -1;
   t.nb2_log = bb ? b.l - tb : 0;
   t.aligned = ((t.Gj & 1) == (t.A & 1)) && ((t.Gnext & 1) == ((int64_t(t.A) * t.ej) & 1));
+  pad_layout(t);
   t.ncb = 1;
   t.tiles = int64_t(1) << (t.nb_log + t.nb2_log);
   finish_fused(t);
@@ -765,19 +788,24 @@ static double kind_bw(const Task &t) {
       // lattice views: 8-byte copies; single-element runs (a lattice of the
       // contiguous axis) touch one 32-byte sector per point and write partial
       // sectors (measured ~0.3 TB/s algorithmic on C3's (5,4,4) lattice)
-      if (t.bj >= 0 && !t.aligned) bw = std::min(bw, run <= 1 ? 0.35 : 1.5);
+      static const bool pad_cost_old = tuning_env("SGH_PAD_COST_OLD") != nullptr;   // experiment
+      if (t.bj >= 0 && (!t.aligned || (pad_cost_old && t.sy > 0))) {
+        static const double ubw = tuning_env("SGH_UNALIGNED_BW") ? atof(tuning_env("SGH_UNALIGNED_BW")) : 1.5;
+        bw = std::min(bw, run <= 1 ? 0.35 : ubw);
+      }
 #ifndef SGH_COST_R1
       // round 2: tasks on the pipelined bulk-copy kernel k_fpipe run at its
       // measured rates (profiles/r02: C5's contiguous-run tiles 5.3 TB/s, C4's
       // 257 x 33 two-blocked tiles 5.8, C2's 255 x 33 blocked tiles 4.4);
       // W = 1 tiles with runs shorter than 128 doubles stay on k_fused (2.85)
-      if (pipe_task(t)) {
+      if (pipe_task(t, true)) {   // the cost model takes the batched (conservative) kernel
         if (t.bt2 >= 0 && t.bt < t.gl[t.bj]) bw = t.ej >= 257 ? 5.6 : 4.5;
         else bw = 5.3;
       } else if (t.W == 1 && t.aligned && run < 128) {
         bw = std::min(bw, 2.9);
       }
 #endif
+      if (pad_cost_old && t.sy > 0) bw = std::min(bw, 1.5);
       return bw;
     }
     default: return 4.0;
@@ -903,7 +931,8 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
           }
         }
     // prefix two-blocked plan (hierarchization, >= 3 non-trivial axes)
-    if (!inv && g_outer_mult == 1) {
+    static const bool no_ptb = tuning_env("SGH_NO_PTB") != nullptr;   // experiment
+    if (!inv && g_outer_mult == 1 && !no_ptb) {
       std::vector<Task> ph;
       if (plan_prefix_two_blocked(grid, levels, d, ph, (flags & SGH_FLAG_TWO_BLOCKED) != 0)) {
         const double c = pass_cost(ph);
@@ -1118,7 +1147,7 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
         if (j < per[g].size()) {
           const Task &t = per[g][j];
           groups[{t.kind, t.kind == KIND_REG ? t.l : 0, (t.kind == KIND_STRIDED || t.kind == KIND_FUSED) ? t.W : 0,
-                  (split ? task_variant(t) : 0) * 2 + (pipe_task(t) ? 1 : 0)}]
+                  (split ? task_variant(t) : 0) * 2 + (pipe_task(t, num_grids > 1) ? 1 : 0)}]
               .push_back(&t);
         }
       for (auto &kv : groups) {
@@ -1592,10 +1621,10 @@ int64_t sgh_plan_describe(const int32_t *levels, int32_t d, uint32_t flags, char
         std::string lv;
         for (int j = 0; j < t.m; ++j) lv += (j ? "," : "") + std::to_string(int(t.gl[j]));
         std::snprintf(line, sizeof line,
-                      "  FUSED W=%d levels=(%s) special=%d bt=%d bt2=%d aligned=%d skip=%u P=%d R=%d A=%d ej=%d "
-                      "runlen=%lld tiles=%lld points=%.0f\n",
+                      "  FUSED W=%d levels=(%s) special=%d bt=%d bt2=%d aligned=%d pad=%d skip=%u P=%d R=%d A=%d "
+                      "ej=%d runlen=%lld tiles=%lld points=%.0f\n",
                       t.W, lv.c_str(), t.bj, t.bj >= 0 ? t.bt : -1, t.bj >= 0 ? t.bt2 : -1,
-                      t.bj >= 0 ? t.aligned : 1, t.skipmask, t.P, t.R, t.bj >= 0 ? t.A : 0, t.bj >= 0 ? t.ej : 0,
+                      t.bj >= 0 ? t.aligned : 1, t.sy > 0, t.skipmask, t.P, t.R, t.bj >= 0 ? t.A : 0, t.bj >= 0 ? t.ej : 0,
                       (long long)(t.W > 1 ? t.W : t.bj < 0 ? int64_t(t.R) * t.P : (t.Gj == t.A ? int64_t(t.A) * t.ej : t.A)),
                       (long long)t.tiles, task_points(t));
       } else {

@@ -124,6 +124,13 @@ struct Task {
   // number of poles gOk[j] gR[j] W
   int32_t gOk[16];
   FDiv fNP[16];
+  // PADDED W == 1 tile layout (sy > 0): SMEM pitches of the special axis' rows
+  // and of the rows after it.  A dense tile row r = x + A (y + ej z) sits in
+  // SMEM at x + y sy + z sz instead of at r, with sy = parity(Gj) and
+  // sz = parity(Gnext) (mod 2): every run of A elements then starts at the
+  // 8-byte phase of its global address, so lattice views (Gj even) load and
+  // store with 16-byte / bulk copies like dense tiles.  sy == 0: dense.
+  int32_t sy, sz;
 };
 
 static_assert(sizeof(Task) % 8 == 0, "Task must stay 8-byte aligned");

@@ -582,9 +582,27 @@ struct GroupSync {
 // levels; hierarchization runs fine -> coarse, dehierarchization the reverse.
 // UNIT: the axis is the tile's first (R == 1): the point stride RS is a
 // compile-time constant (immediate SMEM offsets) and a pole index needs no division.
-template <bool INV, int W, bool UNIT = false, int NT = FT<W>::v, class SY = CtaSync>
+// Dense tile row -> SMEM offset: the identity (dense tiles), or the PADDED
+// layout of a W == 1 tile (Task::sy > 0): row r = x + A (y + ej z) at
+// x + y sy + z sz.  Poles keep their dense row enumeration; only addresses
+// are remapped, and the point stride along the axis (STR) is the padded one.
+struct NoRemap {
+  __device__ __forceinline__ int operator()(int r) const { return r; }
+};
+struct PadRemap {
+  FDiv fA, fE;
+  int A, ej, sy, sz;
+  __device__ __forceinline__ int operator()(int r) const {
+    const int w = (int)fdiv((uint32_t)r, fA);
+    const int z = (int)fdiv((uint32_t)w, fE);
+    return r - w * A + (w - z * ej) * sy + z * sz;
+  }
+};
+
+template <bool INV, int W, bool UNIT = false, int NT = FT<W>::v, class SY = CtaSync, class RM = NoRemap>
 __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, const FDiv fR, int Ok,
-                                           const HaloSkip hs, const FDiv *fnp = nullptr, const SY sy = SY()) {
+                                           const HaloSkip hs, const FDiv *fnp = nullptr, const SY sy = SY(),
+                                           const RM rm = RM(), int str = 0) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   if (UNIT) {
     RS = (W == 1) ? 1 : W + 1;
@@ -592,7 +610,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
   }
   const int n = (1 << l) - 1;
   const int npoles = Ok * R * W;
-  const int STR = R * RS;
+  const int STR = str > 0 ? str : R * RS;
   auto pole_row = [&](int p) -> int {
     const int rest = p >> LOGW;
     if (UNIT) return rest * n;
@@ -600,7 +618,7 @@ __device__ __forceinline__ void fused_axis(double *sm, int RS, int l, int R, con
     const int rk = rest - oo * R;
     return oo * n * R + rk;
   };
-  auto pole_base = [&](int p) -> double * { return sm + pole_row(p) * RS + (p & (W - 1)); };
+  auto pole_base = [&](int p) -> double * { return sm + rm(pole_row(p)) * RS + (p & (W - 1)); };
   // register poles of level L over all poles: the level dispatch is hoisted
   // out of the pole loop
   auto reg_poles = [&](auto LC, int off, int str) {
@@ -717,20 +735,21 @@ __device__ __forceinline__ bool warp_rows_dispatch(double *sm, int nrows, int l)
 // skip_oe (dehierarchization of a two-blocked tile, axis a): poles in the
 // first / last outer row (oo = 0, Ok - 1: the second blocked axis' end rows,
 // final values) are left untouched.
-template <bool INV, int W, int NT = FT<W>::v, class SY = CtaSync>
+template <bool INV, int W, int NT = FT<W>::v, class SY = CtaSync, class RM = NoRemap>
 __device__ __forceinline__ void fused_axis_block(double *sm, int RS, int t, int R, const FDiv fR, int Ok,
                                                  bool lo_ok, bool hi_ok, const FDiv *fnp = nullptr,
-                                                 bool skip_oe = false, const SY sy = SY()) {
+                                                 bool skip_oe = false, const SY sy = SY(), const RM rm = RM(),
+                                                 int str = 0) {
   constexpr int LOGW = (W == 1) ? 0 : (W == 8) ? 3 : (W == 16) ? 4 : (W == 32) ? 5 : (W == 64) ? 6 : 7;
   const int ej = (1 << t) + 1;
   const int npoles = Ok * R * W;
-  const int STR = R * RS;
+  const int STR = str > 0 ? str : R * RS;
   auto pole_base = [&](int p) -> double * {
     const int c = p & (W - 1);
     const int rest = p >> LOGW;
     const int oo = (int)fdiv((uint32_t)rest, fR);
     const int rk = rest - oo * R;
-    return sm + (oo * ej * R + rk) * RS + c;     // local point y = 0
+    return sm + rm(oo * ej * R + rk) * RS + c;   // local point y = 0
   };
   const int K = t / kTB;
   const int tr = t - kTB * K;
@@ -1044,11 +1063,14 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
   const int64_t Gj = T.Gj, Gn = T.Gnext;         // registers: the cp.async "memory" clobbers
   const bool aligned = T.aligned != 0;              // would otherwise reload Task fields per run
   double *const g0 = f.g;
-  const bool dense_y = (Gj == (int64_t)A);
+  const int psy = T.sy, psz = T.sz;                 // padded layout (sy > 0)
+  const bool dense_y = (Gj == (int64_t)A) && psy == 0;
   const int len = dense_y ? ny * A : A;
   const int nseg = dense_y ? nz : nz * ny;
   const int nyw = dense_y ? 1 : ny;                // segment s = z * nyw + (y - y0)
-  auto seg_lo = [=](int z, int yy) { return ((z0 + z) * ej + y0 + yy) * A; };
+  auto seg_lo = [=](int z, int yy) {
+    return psy > 0 ? (z0 + z) * psz + (y0 + yy) * psy : ((z0 + z) * ej + y0 + yy) * A;
+  };
   auto seg_g = [=](int z, int yy) { return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)(z0 + z) * Gn; };
   if (STORE && SGH_BULK_STORE && aligned && nseg <= 64 && len >= 64) {   // bulk stores by one thread
     bulk_fence_barrier();
@@ -1235,9 +1257,31 @@ __device__ __forceinline__ unsigned long long gtime() {
 #endif
 
 // all axes of the group on a staged tile (Alg. 1's axis loop, in SMEM)
+template <bool INV, int W, int NT, class SY, class RM>
+__device__ __forceinline__ void fused_compute_rm(const Task &T, const FusedTile &f, double *sm, const SY sy,
+                                                 int trace_k, const RM rm);
+
 template <bool INV, int W, int NT = FT<W>::v, class SY = CtaSync>
 __device__ __forceinline__ void fused_compute(const Task &T, const FusedTile &f, double *sm, const SY sy = SY(),
                                               int trace_k = -1) {
+  if (W == 1 && T.sy > 0) {                         // padded layout (lattice views)
+    PadRemap rm;
+    rm.fA = T.fA;
+    rm.fE = T.fE;
+    rm.A = T.A;
+    rm.ej = T.ej;
+    rm.sy = T.sy;
+    rm.sz = T.sz;
+    fused_compute_rm<INV, W, NT, SY, PadRemap>(T, f, sm, sy, trace_k, rm);
+  } else {
+    fused_compute_rm<INV, W, NT, SY, NoRemap>(T, f, sm, sy, trace_k, NoRemap());
+  }
+}
+
+template <bool INV, int W, int NT, class SY, class RM>
+__device__ __forceinline__ void fused_compute_rm(const Task &T, const FusedTile &f, double *sm, const SY sy,
+                                                 int trace_k, const RM rm) {
+  constexpr bool PAD = !std::is_same<RM, NoRemap>::value;
   constexpr int RS = (W == 1) ? 1 : W + 1;
   const int rows_total = f.units * T.P;
   const bool blocked = T.bj >= 0 && T.bt < T.gl[T.bj];
@@ -1259,17 +1303,21 @@ __device__ __forceinline__ void fused_compute(const Task &T, const FusedTile &f,
     const FDiv fR = T.fR[j];
     const bool full = (f.units == T.R);               // precomputed per-axis constants apply
     const FDiv fnp = T.fNP[j];
+    // padded layout: the point stride of axis j (x axes: unchanged; the
+    // special axis: sy; the axes after it: their z stride times sz)
+    int str = 0;
+    if (PAD) str = (j < T.bj) ? R : (j == T.bj) ? T.sy : (R / (T.A * T.ej)) * T.sz;
     if (blocked && j == T.bj) {
       // dehierarchization of a two-blocked tile: the second axis' end rows are final
-      fused_axis_block<INV, W, NT, SY>(sm, RS, T.bt, R, fR, full ? T.gOk[j] : rows_total / (T.ej * R), f.lo_ok,
-                                       f.hi_ok, full ? &fnp : nullptr, INV && T.bt2 >= 0, sy);
+      fused_axis_block<INV, W, NT, SY, RM>(sm, RS, T.bt, R, fR, full ? T.gOk[j] : rows_total / (T.ej * R), f.lo_ok,
+                                           f.hi_ok, full ? &fnp : nullptr, INV && T.bt2 >= 0, sy, rm, str);
       if (sy.tid() == 0 && j < 8) PTRACE_IF(trace_k >= 0, trace_k, 8 + j);
       continue;
     }
     if (T.bt2 >= 0 && j == T.bj + 1) {              // second blocked axis
-      fused_axis_block<INV, W, NT, SY>(sm, RS, T.bt2, R, fR,
-                                       full ? T.gOk[j] : rows_total / (((1 << T.bt2) + 1) * R), f.lo2_ok, f.hi2_ok,
-                                       full ? &fnp : nullptr, false, sy);
+      fused_axis_block<INV, W, NT, SY, RM>(sm, RS, T.bt2, R, fR,
+                                           full ? T.gOk[j] : rows_total / (((1 << T.bt2) + 1) * R), f.lo2_ok,
+                                           f.hi2_ok, full ? &fnp : nullptr, false, sy, rm, str);
       if (sy.tid() == 0 && j < 8) PTRACE_IF(trace_k >= 0, trace_k, 8 + j);
       continue;
     }
@@ -1282,8 +1330,8 @@ __device__ __forceinline__ void fused_compute(const Task &T, const FusedTile &f,
     }
 #endif
     const int Ok = full ? T.gOk[j] : rows_total / (n * R);
-    if (R == 1) fused_axis<INV, W, true, NT, SY>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr, sy);
-    else fused_axis<INV, W, false, NT, SY>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr, sy);
+    if (R == 1 && !PAD) fused_axis<INV, W, true, NT, SY>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr, sy);
+    else fused_axis<INV, W, false, NT, SY, RM>(sm, RS, l, R, fR, Ok, hs, full ? &fnp : nullptr, sy, rm, str);
     if (sy.tid() == 0 && j < 8) PTRACE_IF(trace_k >= 0, trace_k, 8 + j);
   }
 }
@@ -1577,8 +1625,9 @@ __device__ __forceinline__ void bulk_load(double *sdst, const double *gsrc, uint
 struct PipeRuns {
   double *g0;
   int64_t Gj, Gn;
-  int A, ej, y0, z0, nyw, len, count;
+  int A, ej, y0, z0, nyw, len, count, sy, sz;
   __device__ __forceinline__ PipeRuns(const Task &T, const FusedTile &f, bool store) {
+    sy = sz = 0;
     if (T.bj < 0) {                                 // dense: one range of R units
       g0 = f.g;
       Gj = Gn = 0;
@@ -1604,14 +1653,16 @@ struct PipeRuns {
     Gj = T.Gj;
     Gn = T.Gnext;
     g0 = f.g;
-    const bool dense_y = (Gj == (int64_t)A);
+    sy = T.sy;
+    sz = T.sz;
+    const bool dense_y = (Gj == (int64_t)A) && sy == 0;
     len = dense_y ? ny * A : A;
     nyw = dense_y ? 1 : ny;
     count = (ny > 0 && nz > 0) ? nz * nyw : 0;
   }
   __device__ __forceinline__ int lo(int i) const {
     const int z = i / nyw, yy = i - z * nyw;
-    return ((z0 + z) * ej + y0 + yy) * A;
+    return sy > 0 ? (z0 + z) * sz + (y0 + yy) * sy : ((z0 + z) * ej + y0 + yy) * A;
   }
   __device__ __forceinline__ double *g(int i) const {
     const int z = i / nyw, yy = i - z * nyw;
@@ -1907,8 +1958,14 @@ __global__ void __launch_bounds__(CFG::threads, 1) k_fpipe(const __grid_constant
 // likewise: C5 146 vs 167.  Loading short runs with 16-byte cp.async from the
 // producer warp instead was slower still (C3 0.11, C5 101-145): one warp
 // cannot issue a tile's worth of small copies in time.  Both stay on k_fused.)
-bool pipe_task(const Task &t) {
+bool pipe_task(const Task &t, bool batched) {
   if (t.kind != KIND_FUSED || (t.bj >= 0 && !t.aligned)) return false;
+  // padded lattice views: on k_fpipe in single-grid calls (C2: 130 vs 125
+  // Gpoints/s -- and the blocked tiles launched before them ran at 0.70 vs
+  // 0.62 of the peak when the next kernel was k_fpipe rather than k_fused),
+  // on k_fused in grouped launches over several grids (C5: 175.0 vs 165.8)
+  static const bool pad_pipe = tuning_env("SGH_PAD_PIPE") != nullptr;   // experiment
+  if (t.sy > 0 && batched && !pad_pipe) return false;
   if (t.W > 1) return t.W >= kPipeMinW;
   if (t.bj < 0) return true;                      // dense: one range per tile
   const int64_t run = (t.Gj == t.A) ? int64_t(t.A) * t.ej : t.A;
@@ -2065,6 +2122,7 @@ size_t task_smem(const Task &t) {
     }
     case KIND_STRIDED: return size_t((int64_t(1) << t.t) + 1) * size_t(t.W + 2) * 8;
     case KIND_FUSED:
+      if (t.W == 1 && t.sy > 0) return (size_t(t.P / (t.A * t.ej)) * size_t(t.sz) + 2) * 8;   // padded
       return t.W == 1 ? (size_t(t.R) * size_t(t.P) + 2) * 8 : (size_t(t.P) * size_t(t.W + 1) + 2) * 8;
     default: return 0;
   }
@@ -2118,7 +2176,7 @@ static int pipe_stages(KernelFn fn, size_t stage_bytes) {
 
 // Launch one task (single grid).  Returns the CUDA error of the launch.
 cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
-  const bool pipe = pipe_task(task);
+  const bool pipe = pipe_task(task, false);
   KernelFn fn = pipe ? fpipe_for<PipeSingle>(task.W, inv) : kernel_for(task.kind, task.l, task.W, inv);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};

@@ -19,7 +19,9 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
                          int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream,
                          int variant = 0, bool pipe = false);
 // W == 1 FUSED tasks that run on the pipelined bulk-copy kernel k_fpipe (grouped separately)
-bool pipe_task(const Task &t);
+// batched: grouped launches of the batched driver over several grids (padded
+// lattice views stay on k_fused there); false: one grid's tasks
+bool pipe_task(const Task &t, bool batched = false);
 size_t task_smem(const Task &t);
 
 // per-launch profiling (sgh_profile.cu); a no-op unless sgh_profile_enable(1)
