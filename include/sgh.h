@@ -215,7 +215,15 @@ sgh_status sgh_transform_sharded_loopback(double *const *shards, const int32_t *
  *             spare row of C doubles (the halo slot; unspecified on return),
  *             C = prod_{k<d} n_k.
  *  workspace: >= sgh_sharded_halo_workspace_bytes() bytes (nranks * C doubles).
- *  flags:     SGH_FLAG_DEHIERARCHIZE for the inverse (coarse lattice first).
+ *  flags:     SGH_FLAG_DEHIERARCHIZE for the inverse (coarse lattice first);
+ *             SGH_FLAG_PER_AXIS: the unfused hierarchization below.
+ * Hierarchization is FUSED by default: the ORIGINAL first rows are gathered
+ * before any transform, and one box plan over the shard (axes 1..d-1 whole /
+ * in aligned blocks together with blocks of x_d inside the super-block and the
+ * super-block's own coarse lattice as later classes; the a4 block scheme)
+ * writes the interior in ~1 HBM round trip; the gathered coarse rows are then
+ * hierarchized as a grid of levels (l_1..l_{d-1}, p).  Unfused (and the
+ * inverse): axes 1..d-1 on the shard, then the gather, then the x_d interior.
  * Errors: INVALID_ARGUMENT if nranks is not a power of two >= 2 or
  * nranks > 2^{l_d - 1}.  Collective: every rank calls it. */
 size_t sgh_sharded_halo_workspace_bytes(const int32_t *levels, int32_t d, int32_t nranks);
@@ -369,7 +377,8 @@ sgh_status sgh_scatter(double *const *grids, const int32_t *levels, int32_t d, i
  * sgh_hierarchize_sharded): pack + unpack copies and the slab pass along x_d;
  * path 1 (halo, sgh_transform_sharded_halo): the super-block interior, the
  * gathered coarse rows and the halo / coarse row copies.  Network bytes are
- * not included.  flags: 0 or SGH_FLAG_DEHIERARCHIZE.  -1 on invalid
+ * not included.  flags: 0, SGH_FLAG_DEHIERARCHIZE, SGH_FLAG_PER_AXIS (the
+ * unfused halo hierarchization).  -1 on invalid
  * arguments.  SURVEY 8(a) a7 / 8(f) 1. */
 double sgh_sharded_plan_bytes(const int32_t *levels, int32_t d, int32_t nranks, int32_t rank, uint32_t flags,
                               int32_t path);

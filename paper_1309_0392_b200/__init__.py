@@ -216,13 +216,13 @@ def plan_cost(levels: Sequence[int], inverse: bool = False, fuse=True) -> float:
 
 
 def sharded_plan_bytes(levels: Sequence[int], nranks: int, rank: int, *, inverse: bool = False,
-                       path: str = "halo") -> float:
+                       path: str = "halo", fused: bool = True) -> float:
     """HBM bytes one sharded call plans on rank `rank` (host-only; network
     bytes excluded): path "a2a" (sgh_hierarchize_sharded) or "halo"
-    (sgh_transform_sharded_halo)."""
+    (sgh_transform_sharded_halo; fused=False: its unfused hierarchization)."""
     a, d = _levels_arr(levels)
-    b = float(lib.sgh_sharded_plan_bytes(a, d, nranks, rank, ctypes.c_uint32(1 if inverse else 0),
-                                         {"a2a": 0, "halo": 1}[path]))
+    fl = (FLAG_DEHIERARCHIZE if inverse else 0) | (0 if fused else FLAG_PER_AXIS)
+    b = float(lib.sgh_sharded_plan_bytes(a, d, nranks, rank, ctypes.c_uint32(fl), {"a2a": 0, "halo": 1}[path]))
     if b < 0:
         raise ValueError(f"invalid sharded configuration {tuple(levels)} nranks={nranks} rank={rank}")
     return b
@@ -507,13 +507,16 @@ class ShardComm:
                      workspace.numel() * workspace.element_size(), _stream(stream)))
         return shard
 
-    def transform_halo(self, shard: torch.Tensor, levels, workspace: torch.Tensor, inverse=False, stream=None):
+    def transform_halo(self, shard: torch.Tensor, levels, workspace: torch.Tensor, inverse=False, stream=None,
+                       fused=True):
         """Halo + coarse-lattice sharded pass: ``shard`` = this rank's rows plus
-        one spare row (sgh_transform_sharded_halo)."""
+        one spare row (sgh_transform_sharded_halo; fused=False: the unfused
+        hierarchization)."""
         a, d = _levels_arr(levels)
+        fl = (FLAG_DEHIERARCHIZE if inverse else 0) | (0 if fused else FLAG_PER_AXIS)
         with torch.cuda.device(shard.device):
             _check(lib.sgh_transform_sharded_halo(_grid_ptr(shard, None), a, d, self.handle,
-                                                  ctypes.c_uint32(FLAG_DEHIERARCHIZE if inverse else 0),
+                                                  ctypes.c_uint32(fl),
                                                   ctypes.c_void_p(workspace.data_ptr()),
                                                   workspace.numel() * workspace.element_size(), _stream(stream)))
         return shard
@@ -546,14 +549,17 @@ def sharded_halo_workspace_bytes(levels, nranks: int) -> int:
     return int(lib.sgh_sharded_halo_workspace_bytes(a, d, int(nranks)))
 
 
-def transform_sharded_halo_loopback(shards, levels, workspace: torch.Tensor, inverse=False, stream=None):
+def transform_sharded_halo_loopback(shards, levels, workspace: torch.Tensor, inverse=False, stream=None,
+                                    fused=True):
     """Halo path for len(shards) virtual ranks on one device (test utility);
-    shards[r] = rank r's rows + one spare row."""
+    shards[r] = rank r's rows + one spare row; fused=False: the unfused
+    hierarchization."""
     P = len(shards)
     a, d = _levels_arr(levels)
     ptrs = (ctypes.c_void_p * P)(*[s.data_ptr() for s in shards])
+    fl = (FLAG_DEHIERARCHIZE if inverse else 0) | (0 if fused else FLAG_PER_AXIS)
     with torch.cuda.device(workspace.device):
-        _check(lib.sgh_transform_sharded_halo_loopback(ptrs, a, d, P, FLAG_DEHIERARCHIZE if inverse else 0,
+        _check(lib.sgh_transform_sharded_halo_loopback(ptrs, a, d, P, fl,
                                                        ctypes.c_void_p(workspace.data_ptr()),
                                                        workspace.numel() * workspace.element_size(),
                                                        _stream(stream)))

@@ -605,6 +605,8 @@ struct BoxAxis {
   int l;            // level of the view (n = 2^l - 1 points)
   int64_t G, base;  // global stride of its points and offset of its first point
   int f;            // only points with tz(i) < f are written (f == l: all)
+  int T = -1;       // restricted to the aligned super-block r of level T (T == l or < 0: the whole pole;
+  int64_t r = 0;    //   halo-sharded plans: the points of one rank's row shard)
 };
 struct BoxCtx {
   double *grid;
@@ -657,7 +659,12 @@ static Task box_task(const BoxCtx &c, const BoxAxis &a, int ta, const BoxAxis &b
   t.Gj = a.G;
   t.Gnext = b.G;
   t.bt2 = bb ? tb : -1;
-  t.nb2_log = bb ? b.l - tb : 0;
+  const int Tb = (b.T < 0 || b.T > b.l) ? b.l : b.T;
+  t.nb2_log = bb ? Tb - tb : 0;                    // blocks of the (super-block of the) pole
+  if (bb && Tb < b.l) {
+    t.nb2_tot = b.l - tb;
+    t.blk2_0 = b.r << (Tb - tb);
+  }
   t.aligned = ((t.Gj & 1) == (t.A & 1)) && ((t.Gnext & 1) == ((int64_t(t.A) * t.ej) & 1));
   pad_layout(t);
   t.ncb = 1;
@@ -684,6 +691,8 @@ static bool solve_box(const BoxCtx &c, const BoxAxis &a, const BoxAxis &b, int d
     std::vector<int> o;
     if (x.f < x.l) {                                 // fine-only axis: the given blocks
       o.push_back(x.f);
+      if (x.T >= 0 && x.T < x.l)                     // a super-block: smaller blocks + its own lattice
+        for (int t = x.f - 1; t >= 2; --t) o.push_back(t);
       return o;
     }
     o.push_back(x.l);                                // whole poles, then blocks large -> small
@@ -704,11 +713,22 @@ static bool solve_box(const BoxCtx &c, const BoxAxis &a, const BoxAxis &b, int d
       const int64_t eb = extent(b, tb);
       if (c.P0 * ea * eb > c.budget) continue;
       std::vector<Task> ph{box_task(c, a, ta, b, tb)};
-      const bool ca = ta < a.l && a.f == a.l, cb = tb < b.l && b.f == b.l;
+      // a class along an axis: the points coarse w.r.t. the tile's blocks but
+      // still to be written (tz < f)
+      const bool ca = ta < a.f, cb = tb < b.f;
       bool ok = depth > 0 || !(ca || cb);
-      const BoxAxis al{a.l - ta, a.G << ta, a.base + ((int64_t(1) << ta) - 1) * a.G, a.l - ta};
-      const BoxAxis bl{b.l - tb, b.G << tb, b.base + ((int64_t(1) << tb) - 1) * b.G, b.l - tb};
-      const BoxAxis af{a.l, a.G, a.base, ta}, bf{b.l, b.G, b.base, tb};
+      auto lat = [](const BoxAxis &x, int t) {       // the coarse lattice {i : 2^t | i}
+        BoxAxis y{x.l - t, x.G << t, x.base + ((int64_t(1) << t) - 1) * x.G, x.f - t};
+        y.T = x.T < 0 ? -1 : x.T - t;
+        y.r = x.r;
+        return y;
+      };
+      auto fine = [](const BoxAxis &x, int t) {      // only the points fine w.r.t. blocks of level t
+        BoxAxis y = x;
+        y.f = t;
+        return y;
+      };
+      const BoxAxis al = lat(a, ta), bl = lat(b, tb), af = fine(a, ta), bf = fine(b, tb);
       if (ok && ca) ok = solve_box(c, al, bf, depth - 1, ph);
       if (ok && cb) ok = solve_box(c, af, bl, depth - 1, ph);
       if (ok && ca && cb) ok = solve_box(c, al, bl, depth - 1, ph);
@@ -751,6 +771,48 @@ static bool plan_prefix_two_blocked(double *grid, const int32_t *levels, int d, 
   const size_t first = phases.size();
   if (!solve_box(c, a, b, 3, phases, force)) {
     phases.resize(first);
+    return false;
+  }
+  return true;
+}
+
+// Halo-sharded hierarchization of one rank's row shard as ONE box plan
+// (SURVEY 8(f) 1 with the a4 block scheme): the shard holds the aligned
+// super-block r (level T) of every x_d pole, its first row and one spare halo
+// row after its rows; the prefix axes and the last non-trivial axis a < d - 1
+// stay whole / blocked as in plan_prefix_two_blocked, and x_d is cut into
+// blocks inside the super-block (+ the super-block's own coarse lattice as
+// classes).  The tiles read the shard's first row and the halo row as block
+// ends: both must hold ORIGINAL values.  Writes every point of the shard whose
+// x_d index is fine w.r.t. T (all rows but row 0 for r >= 1).  Hierarchization
+// only.  False if no plan fits.
+bool plan_shard_box(double *shard, const int32_t *levels, int d, int T, int64_t r, std::vector<Task> &phases) {
+  if (d < 2 || T < 2) return false;
+  int sq[SGH_MAX_D], m = 0;
+  for (int k = 0; k < d - 1; ++k)
+    if (levels[k] > 1) sq[m++] = levels[k];
+  if (m < 1) return false;
+  BoxCtx c;
+  c.grid = shard;
+  c.np = m - 1;
+  c.P0 = 1;
+  for (int j = 0; j < c.np; ++j) {
+    c.pl[j] = (int8_t)sq[j];
+    c.P0 *= (int64_t(1) << sq[j]) - 1;
+  }
+  c.budget = fused_budget_w1() + fused_budget_w1() / 16;
+  if (c.P0 * 25 > c.budget) return false;
+  const int64_t na = (int64_t(1) << sq[m - 1]) - 1;
+  const int64_t C = c.P0 * na;
+  c.N = C << T;
+  const BoxAxis a{sq[m - 1], c.P0, 0, sq[m - 1]};
+  const int64_t first = (r == 0) ? 1 : (r << T);    // global 1-based x_d index of shard row 0
+  BoxAxis b{levels[d - 1], C, -(first - 1) * C, T};
+  b.T = T;
+  b.r = r;
+  const size_t first_phase = phases.size();
+  if (!solve_box(c, a, b, 5, phases)) {
+    phases.resize(first_phase);
     return false;
   }
   return true;

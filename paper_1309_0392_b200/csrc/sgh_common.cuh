@@ -131,6 +131,11 @@ struct Task {
   // 8-byte phase of its global address, so lattice views (Gj even) load and
   // store with 16-byte / bulk copies like dense tiles.  sy == 0: dense.
   int32_t sy, sz;
+  // BLOCK RANGE of the second blocked axis (halo-sharded box plans): the
+  // tiles cover 2^nb2_log consecutive blocks starting at block blk2_0 of the
+  // pole's 2^nb2_tot blocks (nb2_tot == 0: all blocks, blk2_0 = 0)
+  int32_t nb2_tot, pad0_;
+  int64_t blk2_0;
 };
 
 static_assert(sizeof(Task) % 8 == 0, "Task must stay 8-byte aligned");

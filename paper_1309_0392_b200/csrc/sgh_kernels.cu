@@ -1017,11 +1017,11 @@ __device__ __forceinline__ FusedTile fused_tile(const Task &T, int64_t q) {
   f.lo2_ok = f.hi2_ok = true;
   int64_t z0 = 0;
   if (T.bt2 >= 0) {                                // second blocked axis (bj + 1)
-    const int b2 = (int)(rest & ((int64_t(1) << T.nb2_log) - 1));
+    const int64_t b2 = (rest & ((int64_t(1) << T.nb2_log) - 1)) + T.blk2_0;   // block range (sharded)
     rest >>= T.nb2_log;
-    z0 = (int64_t(b2) << T.bt2) - 1;
+    z0 = (b2 << T.bt2) - 1;
     f.lo2_ok = b2 > 0;
-    f.hi2_ok = b2 < (1 << T.nb2_log) - 1;
+    f.hi2_ok = b2 < (int64_t(1) << (T.nb2_tot > 0 ? T.nb2_tot : T.nb2_log)) - 1;
     f.zlo = f.lo2_ok ? 0 : 1;
     f.zhi = f.hi2_ok ? (1 << T.bt2) : (1 << T.bt2) - 1;
   }
@@ -2064,7 +2064,8 @@ int fused_stages() {
   return st;
 }
 
-static KernelFn kernel_for(int kind, int l, int w, bool inv) {
+static KernelFn kernel_for(int kind, int l, int w, bool inv, int stages = -1) {
+  if (stages < 0) stages = fused_stages();
   switch (kind) {
     case KIND_FLAT_SLABS: return inv ? k_flat_slabs<true> : k_flat_slabs<false>;
     case KIND_FLAT_BLOCKS: return inv ? k_flat_blocks<true> : k_flat_blocks<false>;
@@ -2077,7 +2078,7 @@ static KernelFn kernel_for(int kind, int l, int w, bool inv) {
         default: return nullptr;
       }
     case KIND_FUSED:
-      if (fused_stages() == 2) {
+      if (stages == 2) {
         switch (w) {
           case 1: return inv ? k_fused<true, 1, 2> : k_fused<false, 1, 2>;
           case 8: return inv ? k_fused<true, 8, 2> : k_fused<false, 8, 2>;
@@ -2208,7 +2209,10 @@ cudaError_t launch_single(const Task &task, bool inv, cudaStream_t stream) {
 cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, const int64_t *d_prefix,
                          int32_t ntasks, int64_t total_tiles, size_t smem, double points, cudaStream_t stream,
                          int variant, bool pipe) {
-  KernelFn fn = pipe ? fpipe_for<PipeBatched>(w, inv) : kernel_for(kind, l, w, inv);
+  // experiment: groups of small W == 1 tiles on the double-buffered k_fused
+  static const size_t small2 = tuning_env("SGH_SMALL_STAGES2") ? (size_t)atol(tuning_env("SGH_SMALL_STAGES2")) : 0;
+  const int stages = (kind == KIND_FUSED && !pipe && w == 1 && smem <= small2) ? 2 : fused_stages();
+  KernelFn fn = pipe ? fpipe_for<PipeBatched>(w, inv) : kernel_for(kind, l, w, inv, stages);
   if (!fn) return cudaErrorInvalidValue;
   Src src{};
   src.tasks = d_tasks;
@@ -2218,7 +2222,7 @@ cudaError_t launch_table(int kind, int l, int w, bool inv, const Task *d_tasks, 
   if (kind == KIND_FUSED) {
     src.stage_doubles = (int32_t)((smem + 15) / 16 * 2);
     if (pipe) src.nstages = pipe_stages(fn, size_t(src.stage_doubles) * 8);
-    smem = size_t(pipe ? src.nstages : fused_stages()) * src.stage_doubles * 8;
+    smem = size_t(pipe ? src.nstages : stages) * src.stage_doubles * 8;
   }
   const int nt = pipe ? PipeBatched::threads : kind == KIND_FUSED ? (w == 1 ? FT<1>::v : FT<8>::v) : kThreads;
   const int64_t cap = resident_ctas(fn, smem, nt);

@@ -45,15 +45,13 @@ inline double task_points(const Task &t) {
       const int lj = t.gl[t.bj];
       const double fine = double((int64_t(1) << lj) - 1) - double((int64_t(1) << (lj - t.bt)) - 1);
       if (t.bt2 >= 0) {                             // two blocked axes: fine along both
-        const int l2 = t.gl[t.bj + 1];
-        const double fine2 = double((int64_t(1) << l2) - 1) - double((int64_t(1) << (l2 - t.bt2)) - 1);
+        const double fine2 = double(int64_t(1) << t.nb2_log) * double((int64_t(1) << t.bt2) - 1);
         return double(t.O) * double(t.S) * double(t.P / t.ej / ((1 << t.bt2) + 1)) * fine * fine2;
       }
       return double(t.O) * double(t.S) * double(t.P / t.ej) * fine;
     }
     if (t.bj >= 0 && t.bt2 >= 0) {                 // lattice axis x blocked axis: fine rows of the latter
-      const int l2 = t.gl[t.bj + 1];
-      const double fine2 = double((int64_t(1) << l2) - 1) - double((int64_t(1) << (l2 - t.bt2)) - 1);
+      const double fine2 = double(int64_t(1) << t.nb2_log) * double((int64_t(1) << t.bt2) - 1);
       return double(t.O) * double(t.S) * double(t.P / ((1 << t.bt2) + 1)) * fine2;
     }
     return double(t.O) * double(t.P) * double(t.S);   // every point, once
@@ -129,6 +127,9 @@ size_t batched_table_bytes(double *const *grids, const int32_t *levels, int32_t 
                            uint32_t flags);
 // flags: SGH_FLAG_DEHIERARCHIZE / SGH_FLAG_PER_AXIS / SGH_FLAG_WHOLE_POLES (sgh.h)
 void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::vector<std::vector<Task>> &passes);
+// halo-sharded hierarchization of rank r's row shard as one box plan (the
+// interior of super-block r of level T of x_d fused with the other axes)
+bool plan_shard_box(double *shard, const int32_t *levels, int d, int T, int64_t r, std::vector<Task> &phases);
 // plan_grid of `outer` stacked copies of the grid (a row shard of the next axis)
 void plan_grid_rows(double *grid, const int32_t *levels, int d, int64_t outer, uint32_t flags,
                     std::vector<std::vector<Task>> &passes);

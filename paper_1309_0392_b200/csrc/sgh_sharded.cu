@@ -402,8 +402,32 @@ static sgh_status halo_rank_steps(double *shard, double *G, const HaloGeom &H, i
   return SGH_OK;
 }
 
+// FUSED hierarchization of rank r's shard (one box plan, plan_shard_box): G
+// holds every rank's ORIGINAL first row (gathered before any transform); the
+// halo is G[r + 1]; the box plan writes the super-block's interior; the coarse
+// rows G[1..P-1] form a grid of levels (l_1..l_{d-1}, p), hierarchized whole
+// (every rank, redundantly); rank r >= 1 takes its first row back.  Every
+// point sees the oracle's axis order with the oracle's operations:
+// bitwise.  Per rank ~1 HBM round trip instead of the two of halo_rank_steps.
+static sgh_status halo_fused_hier(double *shard, double *G, const HaloGeom &H, int r, std::vector<Task> &box,
+                                  cudaStream_t s) {
+  sgh_status st;
+  const int64_t C = H.C, R = H.rows[r];
+  if (r + 1 < H.P && (st = d2d(shard + R * C, G + (r + 1) * C, C, s, "halo row")) != SGH_OK) return st;
+  if ((st = launch_phases(box, false, s)) != SGH_OK) return st;
+  int32_t lv[SGH_MAX_D];
+  for (int k = 0; k + 1 < H.d; ++k) lv[k] = H.levels[k];
+  lv[H.d - 1] = H.p;                                  // the coarse lattice: P - 1 rows
+  std::vector<std::vector<Task>> passes;
+  plan_grid(G + C, lv, H.d, 0u, passes);
+  for (auto &ph : passes)
+    if ((st = launch_phases(ph, false, s)) != SGH_OK) return st;
+  if (r >= 1 && (st = d2d(shard, G + r * C, C, s, "coarse row back")) != SGH_OK) return st;
+  return SGH_OK;
+}
+
 static sgh_status sharded_halo_nccl(double *shard, const int32_t *levels, int32_t d, void *comm, void *workspace,
-                                    size_t ws_bytes, void *stream, bool inv) {
+                                    size_t ws_bytes, void *stream, bool inv, bool fused) {
   if (!comm) return invalid("comm is NULL");
   Comm *c = static_cast<Comm *>(comm);
   HaloGeom H;
@@ -420,12 +444,17 @@ static sgh_status sharded_halo_nccl(double *shard, const int32_t *levels, int32_
     ncclResult_t nr = ncclAllGather(shard, G, size_t(H.C), ncclDouble, c->nccl, s);
     return nr == ncclSuccess ? SGH_OK : nccl_fail(nr, "ncclAllGather (coarse rows)");
   };
+  std::vector<Task> box;
+  if (!inv && fused && plan_shard_box(shard, H.levels, H.d, H.T, c->rank, box)) {
+    if ((st = gather()) != SGH_OK) return st;         // the ORIGINAL first rows
+    return halo_fused_hier(shard, G, H, c->rank, box, s);
+  }
   return halo_rank_steps(shard, G, H, c->rank, inv, s, gather, true, true);
 }
 
 // P virtual ranks on one device (test): the gather is P device copies.
 static sgh_status sharded_halo_loopback(double *const *shards, const int32_t *levels, int32_t d, int32_t P,
-                                        void *workspace, size_t ws_bytes, void *stream, bool inv) {
+                                        void *workspace, size_t ws_bytes, void *stream, bool inv, bool fused) {
   HaloGeom H;
   sgh_status st = make_halo_geom(levels, d, P, H);
   if (st != SGH_OK) return st;
@@ -439,6 +468,19 @@ static sgh_status sharded_halo_loopback(double *const *shards, const int32_t *le
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double *ws = static_cast<double *>(workspace);
   const int64_t GC = H.P * H.C;
+  if (!inv && fused) {
+    std::vector<std::vector<Task>> boxes(P);
+    bool all = true;
+    for (int r = 0; r < P && all; ++r) all = plan_shard_box(shards[r], H.levels, H.d, H.T, r, boxes[r]);
+    if (all) {
+      for (int r = 0; r < P; ++r)                      // every rank's G = all ORIGINAL first rows
+        for (int q = 0; q < P; ++q)
+          if ((st = d2d(ws + r * GC + q * H.C, shards[q], H.C, s, "loopback gather")) != SGH_OK) return st;
+      for (int r = 0; r < P; ++r)
+        if ((st = halo_fused_hier(shards[r], ws + r * GC, H, r, boxes[r], s)) != SGH_OK) return st;
+      return SGH_OK;
+    }
+  }
   for (int r = 0; r < P; ++r)
     if ((st = halo_local_axes(shards[r], H, r, inv, s)) != SGH_OK) return st;
   for (int r = 0; r < P; ++r)                          // every rank's G = all first rows
@@ -486,7 +528,7 @@ sgh_status sgh_shard_layout(const int32_t *levels, int32_t d, int32_t nranks, in
 double sgh_sharded_plan_bytes(const int32_t *levels, int32_t d, int32_t nranks, int32_t rank, uint32_t flags,
                               int32_t path) {
   return guarded_value<double>(-1.0, [&]() -> double {
-  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return -1.0;
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS)) return -1.0;
   if (rank < 0 || rank >= nranks || (path != 0 && path != 1)) return -1.0;
   const bool inv = (flags & SGH_FLAG_DEHIERARCHIZE) != 0;
   auto points = [](const std::vector<Task> &ph) {
@@ -511,6 +553,17 @@ double sgh_sharded_plan_bytes(const int32_t *levels, int32_t d, int32_t nranks, 
   } else {
     HaloGeom H;
     if (make_halo_geom(levels, d, nranks, H) != SGH_OK) return -1.0;
+    std::vector<Task> box;
+    if (!inv && !(flags & SGH_FLAG_PER_AXIS) && plan_shard_box(nullptr, H.levels, d, H.T, rank, box)) {
+      pts += points(box);                                     // fused: one box plan over the shard
+      int32_t lv[SGH_MAX_D];
+      for (int k = 0; k + 1 < d; ++k) lv[k] = H.levels[k];
+      lv[d - 1] = H.p;
+      plan_grid(nullptr, lv, d, 0u, passes);                  // the coarse rows (redundantly)
+      for (const auto &ph : passes) pts += points(ph);
+      pts += double(H.C) * ((rank >= 1) + (rank + 1 < H.P));  // halo row in, own coarse row back
+      return 16.0 * pts;
+    }
     plan_grid_rows(nullptr, H.levels, d - 1, H.rows[rank], inv ? uint32_t(SGH_FLAG_DEHIERARCHIZE) : 0u, passes);
     for (const auto &ph : passes) pts += points(ph);
     std::vector<Task> in;
@@ -598,8 +651,9 @@ size_t sgh_sharded_halo_workspace_bytes(const int32_t *levels, int32_t d, int32_
 sgh_status sgh_transform_sharded_halo(double *shard, const int32_t *levels, int32_t d, void *comm, uint32_t flags,
                                       void *workspace, size_t ws_bytes, void *stream) {
   return guarded([&]() -> sgh_status {
-  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
-  return sharded_halo_nccl(shard, levels, d, comm, workspace, ws_bytes, stream, (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS)) return invalid("unknown flags");
+  return sharded_halo_nccl(shard, levels, d, comm, workspace, ws_bytes, stream, (flags & SGH_FLAG_DEHIERARCHIZE) != 0,
+                           (flags & SGH_FLAG_PER_AXIS) == 0);
 });
 }
 
@@ -607,9 +661,9 @@ sgh_status sgh_transform_sharded_halo_loopback(double *const *shards, const int3
                                                int32_t nranks, uint32_t flags, void *workspace, size_t ws_bytes,
                                                void *stream) {
   return guarded([&]() -> sgh_status {
-  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
+  if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE | SGH_FLAG_PER_AXIS)) return invalid("unknown flags");
   return sharded_halo_loopback(shards, levels, d, nranks, workspace, ws_bytes, stream,
-                               (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
+                               (flags & SGH_FLAG_DEHIERARCHIZE) != 0, (flags & SGH_FLAG_PER_AXIS) == 0);
 });
 }
 

@@ -212,6 +212,24 @@ def test_plan_prefix_two_blocked_partition(levels):
                int(ph[0][1].get("bt2", "-1")) < 0 for ph in q)
 
 
+@pytest.mark.parametrize("levels,P", [((14, 13), 2), ((14, 13), 4), ((14, 13), 8), ((8, 8, 8), 2), ((8, 8, 8), 4)],
+                         ids=str)
+def test_sharded_plan_bytes_fused(levels, P):
+    """Sharded paths: the fused halo hierarchization
+    plans <= 1.3 x 16 B per point of a rank's shard (one box plan + the coarse
+    rows), the unfused one ~2 passes; the all-to-all path's local axes are
+    planned like a whole grid (plan_grid_rows), so C2's local part is ~1 pass
+    (+ pack / unpack copies and the slab pass)."""
+    N = si.num_points(levels)
+    per = 16.0 * N / P
+    fused = max(sgh.sharded_plan_bytes(levels, P, r, path="halo") for r in range(P))
+    unfused = max(sgh.sharded_plan_bytes(levels, P, r, path="halo", fused=False) for r in range(P))
+    assert fused <= 1.3 * per < unfused
+    assert max(sgh.sharded_plan_bytes(levels, P, r, path="halo", inverse=True) for r in range(P)) == unfused
+    a2a = max(sgh.sharded_plan_bytes(levels, P, r, path="a2a") for r in range(P))
+    assert a2a <= 1.01 * (3 + (len(levels) - 1 if len(levels) < 3 else 1.1)) * per
+
+
 def test_plan_two_blocked_forced():
     """SGH_FLAG_TWO_BLOCKED (fuse="two_blocked") selects the two-blocked plan
     wherever one exists (how the GPU parity tests exercise it)."""

@@ -447,13 +447,17 @@ def test_sharded_loopback_bitwise(sgh, levels, P, inverse):
 
 
 @pytest.mark.parametrize("levels,P", [((6, 5), 2), ((6, 5), 4), ((5, 4, 6), 8), ((3, 7), 8), ((8, 2, 3, 4), 4),
-                                      ((4, 2), 2), ((2, 3, 9), 16), ((14, 13), 8), ((14, 13), 2), ((27,), 8)], ids=str)
-@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
-def test_sharded_halo_loopback_bitwise(sgh, levels, P, inverse):
+                                      ((4, 2), 2), ((2, 3, 9), 16), ((14, 13), 8), ((14, 13), 2), ((27,), 8),
+                                      ((7, 7, 8), 4), ((5, 9), 2), ((9, 6), 16)], ids=str)
+@pytest.mark.parametrize("inverse,fused", [(False, True), (False, False), (True, True)],
+                         ids=["hier", "hier_unfused", "dehier"])
+def test_sharded_halo_loopback_bitwise(sgh, levels, P, inverse, fused):
     """Halo + coarse-lattice sharded pass on P virtual ranks:
     shard interiors from shard + one halo row, coarse lattice from the gathered
-    first rows; equals the single-grid oracle bitwise.  Spare rows are NaN-filled
-    (never read as data)."""
+    first rows; equals the single-grid oracle bitwise.  Hierarchization is fused
+    by default (one box plan per shard over ORIGINAL end rows, then the coarse
+    rows as a grid) and also run unfused.  Spare rows are NaN-filled (never read
+    as data)."""
     N = si.num_points(levels)
     u = si.fill_uniform(N, grid_id=78)
     want = u.copy()
@@ -466,7 +470,7 @@ def test_sharded_halo_loopback_bitwise(sgh, levels, P, inverse):
         buf[:(e - b) * C].copy_(torch.from_numpy(u[b * C:e * C]))
         shards.append(buf)
     ws = torch.empty(P * sgh.sharded_halo_workspace_bytes(levels, P) // 8, dtype=torch.float64, device="cuda")
-    sgh.transform_sharded_halo_loopback(shards, levels, ws, inverse=inverse)
+    sgh.transform_sharded_halo_loopback(shards, levels, ws, inverse=inverse, fused=fused)
     got = torch.cat([s[:-C] for s in shards]).cpu().numpy()
     assert_bitwise(got, want)
 
