@@ -309,7 +309,7 @@ static bool plan_fused_group(double *grid, const int32_t *levels, int d, int a, 
 // after j in the group is transformed (the block ends must be final values
 // when a block tile reads them).  Returns false if no block of >= 4 points fits.
 static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a, int b, int j, int W,
-                               std::vector<Task> &phases) {
+                               std::vector<Task> &phases, bool inv = false) {
   const int64_t budget = W == 1 ? fused_budget_w1() + fused_budget_w1() / 16 : fused_budget() + fused_budget() / 16;
   if (b - a > 16 || b - a < 2 || levels[j] < 3) return false;
   int64_t Sa = 1, O = g_outer_mult, Prest = 1, A = 1;
@@ -385,6 +385,17 @@ static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a
     t.ncb = (W > 1) ? (Sa + W - 1) / W : 1;
     t.tiles = (O << t.nb_log) * t.ncb;
     if (lj <= 1 && busy - (levels[j] > 1) == 0) break;   // nothing left to transform
+    if (lj == 1 && b - a == 2 && j == a && Sa == 1 && !inv) {
+      // a single lattice point along j and ONE other group axis k: the phase
+      // is a plain pole view along k (REG / STRIDED kernels: one thread per
+      // column) instead of one FUSED tile per unit (C3's (1, 4) lattice of
+      // isolated elements: 3,375 tiles of 15 points)
+      const int k = (j == a) ? a + 1 : a;
+      int64_t Gk = Sa;
+      for (int q = a; q < k; ++q) Gk *= (int64_t(1) << levels[q]) - 1;
+      if (levels[k] > 1) plan_view(grid, O, t.OS, Gk, Sa, base, levels[k], phases);
+      break;
+    }
     finish_fused(t);
     phases.push_back(t);
     if (!blocked) break;
@@ -959,7 +970,7 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
         // unit-stride axis, columns of isolated elements (C3: 77.9 vs 80.8 Gpoints/s)
         for (int W = (Sa == 1 ? 1 : fused_wmax()); W >= (Sa == 1 ? 1 : 8); W >>= 1) {
           std::vector<Task> bp;
-          if (!plan_blocked_group(grid, levels, d, i, j, s, W, bp)) continue;
+          if (!plan_blocked_group(grid, levels, d, i, j, s, W, bp, inv)) continue;
           if (inv && later && Sa == 1 && s == i && bp.size() >= 2 && bp[1].gl[bp[1].bj] < 2) continue;
           if (inv && later) split_inverse_lattice(bp, s - i);
           const double cj = cost[i] + pass_cost(bp);
