@@ -1965,7 +1965,9 @@ bool pipe_task(const Task &t, bool batched) {
   // 0.62 of the peak when the next kernel was k_fpipe rather than k_fused),
   // on k_fused in grouped launches over several grids (C5: 175.0 vs 165.8)
   static const bool pad_pipe = tuning_env("SGH_PAD_PIPE") != nullptr;   // experiment
-  if (t.sy > 0 && batched && !pad_pipe) return false;
+  static const int pad_pipe_min_p =
+      tuning_env("SGH_PAD_PIPE_MIN_P") ? atoi(tuning_env("SGH_PAD_PIPE_MIN_P")) : (1 << 30);   // experiment
+  if (t.sy > 0 && batched && !pad_pipe && t.P < pad_pipe_min_p) return false;
   if (t.W > 1) return t.W >= kPipeMinW;
   if (t.bj < 0) return true;                      // dense: one range per tile
   const int64_t run = (t.Gj == t.A) ? int64_t(t.A) * t.ej : t.A;
