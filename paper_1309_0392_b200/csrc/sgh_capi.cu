@@ -879,6 +879,14 @@ static double kind_bw(const Task &t) {
       }
 #endif
       if (pad_cost_old && t.sy > 0) bw = std::min(bw, 1.5);
+      // padded lattice / blocked views run on k_fused in the batched launches
+      // at ~1.5 TB/s (small tiles, load -> transform -> store per CTA): half
+      // the run-length rate.  C5, one call: scale 1.0 175.5 Gpoints/s at 1.63
+      // planned passes (dominant launch 0.77 of the peak), 0.7 175.6 (1.67,
+      // 0.79), 0.5 175.6 (1.72, 0.81), 0.35 173.2 (1.76, 0.83)
+      static const double pad_scale =
+          tuning_env("SGH_PAD_BW_SCALE") ? atof(tuning_env("SGH_PAD_BW_SCALE")) : 0.5;   // tuning override
+      if (t.sy > 0) bw *= pad_scale;
       return bw;
     }
     default: return 4.0;
