@@ -444,8 +444,13 @@ static sgh_status sharded_halo_nccl(double *shard, const int32_t *levels, int32_
     ncclResult_t nr = ncclAllGather(shard, G, size_t(H.C), ncclDouble, c->nccl, s);
     return nr == ncclSuccess ? SGH_OK : nccl_fail(nr, "ncclAllGather (coarse rows)");
   };
-  std::vector<Task> box;
-  if (!inv && fused && plan_shard_box(shard, H.levels, H.d, H.T, c->rank, box)) {
+  // fused or not must be the same decision on every rank (the gather happens
+  // at a different point): decided from rank 0's plan, whose tile shapes are
+  // every rank's
+  std::vector<Task> probe, box;
+  if (!inv && fused && plan_shard_box(nullptr, H.levels, H.d, H.T, 0, probe)) {
+    if (!plan_shard_box(shard, H.levels, H.d, H.T, c->rank, box))
+      return invalid("internal: the fused halo plan of this rank differs from rank 0's");
     if ((st = gather()) != SGH_OK) return st;         // the ORIGINAL first rows
     return halo_fused_hier(shard, G, H, c->rank, box, s);
   }
