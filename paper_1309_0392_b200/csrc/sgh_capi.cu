@@ -210,7 +210,7 @@ static int fused_wmax() {
 
 // per-axis constants of a full FUSED tile (Task::gOk, Task::fNP)
 static void finish_fused(Task &t) {
-  const int64_t rows = int64_t(t.P) * ((t.W == 1 && t.bj < 0) ? t.R : 1);
+  const int64_t rows = int64_t(t.P) * (t.W == 1 ? t.R : 1);   // R units per W == 1 tile (dense, lattice views)
   const int Wc = t.W == 1 ? 1 : t.W;
   for (int j = 0; j < t.m; ++j) {
     int64_t e = (int64_t(1) << t.gl[j]) - 1;
@@ -238,6 +238,9 @@ static void pad_layout(Task &t) {
   const int64_t ez = t.P / (int64_t(t.A) * t.ej);
   int64_t sz = sy * t.ej;
   if (ez > 1 && ((sz ^ t.Gnext) & 1)) ++sz;
+  // one row after the special axis: its pitch is free -- give it the parity of
+  // the outer stride OS, so R > 1 units per tile stack at their global phase
+  if (ez == 1 && ((sz ^ t.OS) & 1)) ++sz;
   if (ez * sz + 2 > int64_t(kFusedT1) + kFusedT1 / 8) return;   // the SMEM stage: keep 8-byte copies
   t.sy = (int32_t)sy;
   t.sz = (int32_t)sz;
@@ -395,6 +398,16 @@ static bool plan_blocked_group(double *grid, const int32_t *levels, int d, int a
       for (int q = a; q < k; ++q) Gk *= (int64_t(1) << levels[q]) - 1;
       if (levels[k] > 1) plan_view(grid, O, t.OS, Gk, Sa, base, levels[k], phases);
       break;
+    }
+    const int64_t foot = t.sy > 0 ? int64_t(t.P / (t.A * t.ej)) * t.sz : t.P;   // SMEM pitch of a unit
+    // (units stack in SMEM at `foot`, in global memory at OS: with 16-byte
+    // copies both must have the same 8-byte parity)
+    if (!blocked && W == 1 && O > 1 && (!t.aligned || ((foot ^ t.OS) & 1) == 0)) {
+      // a coarse-lattice view: R consecutive outer units per tile, as many as
+      // the tile budget holds (small lattice tiles are latency-bound)
+      const int64_t R = std::min<int64_t>(O, std::max<int64_t>(1, budget / std::max<int64_t>(1, foot)));
+      t.R = (int32_t)R;
+      t.tiles = (O + R - 1) / R;
     }
     finish_fused(t);
     phases.push_back(t);
@@ -1051,6 +1064,22 @@ void plan_grid_rows(double *grid, const int32_t *levels, int d, int64_t outer, u
   plan_grid(grid, levels, d, flags, passes);
 }
 
+// A single grid's coarse-lattice views keep >= 2 tiles per SM of a B200: the
+// R units per tile that fill the tiles of a batched launch (many grids) would
+// leave SMs idle in a launch of one grid's lattice (C2: 64 tiles of 4 units).
+static void single_grid_units(std::vector<std::vector<Task>> &passes) {
+  constexpr int64_t kMinTiles = 2 * 148;
+  for (auto &ph : passes)
+    for (Task &t : ph) {
+      if (t.kind != KIND_FUSED || t.W != 1 || t.bj < 0 || t.R <= 1) continue;
+      const int64_t R = std::max<int64_t>(1, std::min<int64_t>(t.R, t.O / kMinTiles));
+      if (R == t.R) continue;
+      t.R = (int32_t)R;
+      t.tiles = (t.O + R - 1) / R;
+      finish_fused(t);
+    }
+}
+
 // ------------------------------------------------- pinned staging ring
 // Task tables are staged in pinned host memory and copied asynchronously into
 // the caller's workspace.  A slot is reused only after its copy has completed.
@@ -1141,6 +1170,7 @@ static sgh_status transform_single(double *grid, const int32_t *levels, int32_t 
   if (!axis_order && all_axes) {
     std::vector<std::vector<Task>> passes;
     plan_grid(grid, levels, d, flags, passes);
+    single_grid_units(passes);
     for (auto &phases : passes) {
       if (inv) std::reverse(phases.begin(), phases.end());   // coarse lattice first (H2)
       for (const Task &t : phases) {
@@ -1207,6 +1237,7 @@ static void build_batched_plan(double *const *grids, const int32_t *levels, int3
   size_t rounds = 0;
   for (int64_t g = 0; g < num_grids; ++g) {
     plan_grid(grids ? grids[g] : nullptr, levels + g * d, d, flags, all[g]);
+    if (num_grids == 1) single_grid_units(all[g]);
     rounds = std::max(rounds, all[g].size());
   }
   std::vector<std::vector<Task>> per(num_grids);

@@ -1025,6 +1025,12 @@ __device__ __forceinline__ FusedTile fused_tile(const Task &T, int64_t q) {
     f.zlo = f.lo2_ok ? 0 : 1;
     f.zhi = f.hi2_ok ? (1 << T.bt2) : (1 << T.bt2) - 1;
   }
+  int units = 1;
+  if (W == 1 && T.R > 1) {                         // a coarse-lattice view: R consecutive outer units per tile
+    const int64_t o0 = rest * T.R;
+    units = (int)min((int64_t)T.R, T.O - o0);
+    rest = o0;
+  }
   int64_t ooff = rest * T.OS;
   if (T.O1 > 0) {                                  // two-level outer index
     const int64_t o2 = rest / T.O1;
@@ -1032,7 +1038,7 @@ __device__ __forceinline__ FusedTile fused_tile(const Task &T, int64_t q) {
   }
   const int64_t y0 = blocked ? (int64_t(b) << T.bt) - 1 : 0;   // 0-based pole index of local y = 0
   f.g = T.grid + T.base + ooff + c0 + y0 * T.Gj + z0 * T.Gnext;
-  f.units = 1;
+  f.units = units;
   f.wc = (W > 1) ? (int)min((int64_t)W, T.S - c0) : 1;
   f.lo_ok = !blocked || b > 0;
   f.hi_ok = !blocked || b < (1 << T.nb_log) - 1;
@@ -1055,12 +1061,15 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
   const int ny = y1 - y0 + 1;
   // rows z of the axes after the special one: all of them, or the existing /
   // fine rows of a second blocked axis
-  int z0 = 0, nz = T.P / (A * ej);
+  const int ez = T.P / (A * ej);                   // rows after the special axis per unit
+  int z0 = 0, nz = ez * f.units;                    // units (lattice views, R > 1) stack along z
   if (T.bt2 >= 0) {
     z0 = STORE ? 1 : f.zlo;
     nz = (STORE ? nz - 2 : f.zhi) - z0 + 1;
   }
   const int64_t Gj = T.Gj, Gn = T.Gnext;         // registers: the cp.async "memory" clobbers
+  const int64_t OSu = T.OS;
+  const bool multi = f.units > 1;
   const bool aligned = T.aligned != 0;              // would otherwise reload Task fields per run
   double *const g0 = f.g;
   const int psy = T.sy, psz = T.sz;                 // padded layout (sy > 0)
@@ -1071,7 +1080,12 @@ __device__ __forceinline__ void fused_segments(const Task &T, const FusedTile &f
   auto seg_lo = [=](int z, int yy) {
     return psy > 0 ? (z0 + z) * psz + (y0 + yy) * psy : ((z0 + z) * ej + y0 + yy) * A;
   };
-  auto seg_g = [=](int z, int yy) { return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)(z0 + z) * Gn; };
+  auto seg_g = [=](int z, int yy) {
+    const int zz = z0 + z;
+    if (!multi) return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)zz * Gn;
+    const int u = zz / ez;                          // unit u of the tile at u OS
+    return g0 + (int64_t)u * OSu + (int64_t)(y0 + yy) * Gj + (int64_t)(zz - u * ez) * Gn;
+  };
   if (STORE && SGH_BULK_STORE && aligned && nseg <= 64 && len >= 64) {   // bulk stores by one thread
     bulk_fence_barrier();
     if (threadIdx.x == 0) {
@@ -1625,9 +1639,12 @@ __device__ __forceinline__ void bulk_load(double *sdst, const double *gsrc, uint
 struct PipeRuns {
   double *g0;
   int64_t Gj, Gn;
-  int A, ej, y0, z0, nyw, len, count, sy, sz;
+  int A, ej, y0, z0, nyw, len, count, sy, sz, ez;
+  int64_t OSu;
   __device__ __forceinline__ PipeRuns(const Task &T, const FusedTile &f, bool store) {
     sy = sz = 0;
+    ez = 1;
+    OSu = 0;
     if (T.bj < 0) {                                 // dense: one range of R units
       g0 = f.g;
       Gj = Gn = 0;
@@ -1645,7 +1662,9 @@ struct PipeRuns {
     const int y1 = (store && blocked) ? ej - 2 : f.yhi;
     const int ny = y1 - y0 + 1;
     z0 = 0;
-    int nz = T.P / (A * ej);
+    ez = T.P / (A * ej);
+    OSu = f.units > 1 ? T.OS : 0;                   // units (lattice views, R > 1) stack along z
+    int nz = ez * f.units;
     if (T.bt2 >= 0) {
       z0 = store ? 1 : f.zlo;
       nz = (store ? nz - 2 : f.zhi) - z0 + 1;
@@ -1666,7 +1685,10 @@ struct PipeRuns {
   }
   __device__ __forceinline__ double *g(int i) const {
     const int z = i / nyw, yy = i - z * nyw;
-    return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)(z0 + z) * Gn;
+    const int zz = z0 + z;
+    if (OSu == 0) return g0 + (int64_t)(y0 + yy) * Gj + (int64_t)zz * Gn;
+    const int u = zz / ez;
+    return g0 + (int64_t)u * OSu + (int64_t)(y0 + yy) * Gj + (int64_t)(zz - u * ez) * Gn;
   }
 };
 
@@ -2125,7 +2147,7 @@ size_t task_smem(const Task &t) {
     }
     case KIND_STRIDED: return size_t((int64_t(1) << t.t) + 1) * size_t(t.W + 2) * 8;
     case KIND_FUSED:
-      if (t.W == 1 && t.sy > 0) return (size_t(t.P / (t.A * t.ej)) * size_t(t.sz) + 2) * 8;   // padded
+      if (t.W == 1 && t.sy > 0) return (size_t(t.R) * size_t(t.P / (t.A * t.ej)) * size_t(t.sz) + 2) * 8;   // padded
       return t.W == 1 ? (size_t(t.R) * size_t(t.P) + 2) * 8 : (size_t(t.P) * size_t(t.W + 1) + 2) * 8;
     default: return 0;
   }
