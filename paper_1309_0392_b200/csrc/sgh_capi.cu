@@ -845,7 +845,33 @@ bool plan_shard_box(double *shard, const int32_t *levels, int d, int T, int64_t 
 // Estimated time per point (1 / TB/s) of a pass, from the kernels' measured
 // B200 throughput (profiles/r01): wide contiguous tiles stream best, narrow
 // column tiles lose DRAM efficiency.
+// experiments (-DSGH_TUNING): SGH_BW_SCALE=kind:factor[,kind:factor] scales a
+// kind's modelled rate (kinds 0..4; 5 = W > 1 FUSED, 6 = k_fpipe tasks)
+static double bw_scale(int k) {
+  static double f[8] = {-1};
+  if (f[0] < 0) {
+    for (double &x : f) x = 1.0;
+    if (const char *e = tuning_env("SGH_BW_SCALE")) {
+      int kk;
+      double v;
+      int used = 0;
+      while (std::sscanf(e, "%d:%lf%n", &kk, &v, &used) == 2) {
+        if (kk >= 0 && kk < 8) f[kk] = v;
+        e += used;
+        if (*e == ',') ++e;
+      }
+    }
+  }
+  return f[k];
+}
+static double kind_bw_raw(const Task &t);
 static double kind_bw(const Task &t) {
+  double bw = kind_bw_raw(t);
+  if (t.kind == KIND_FUSED && pipe_task(t, true)) return bw * bw_scale(6);
+  if (t.kind == KIND_FUSED && t.W > 1) return bw * bw_scale(5);
+  return bw * bw_scale(t.kind);
+}
+static double kind_bw_raw(const Task &t) {
   switch (t.kind) {
     case KIND_FLAT_SLABS:
     case KIND_FLAT_BLOCKS: return 5.6;
