@@ -475,6 +475,36 @@ def test_sharded_halo_loopback_bitwise(sgh, levels, P, inverse, fused):
     assert_bitwise(got, want)
 
 
+@pytest.mark.parametrize("levels", [(8, 8, 8), (14, 13), (5, 4, 6)], ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_sharded_nccl_one_rank_bitwise(sgh, levels, inverse):
+    """The NCCL transport itself on the one GPU the pool provides: a one-rank
+    communicator (library-owned, from a unique id broadcast over a one-rank
+    gloo group) through sgh_hierarchize_sharded -- the grouped
+    ncclSend / ncclRecv all-to-all runs (to itself), the pack / slab / unpack
+    copies with it; bitwise vs the oracle."""
+    import socket
+
+    import torch.distributed as dist
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        comm = sgh.ShardComm()
+        N = si.num_points(levels)
+        u = si.fill_uniform(N, grid_id=91)
+        want = (oracle.dehierarchize if inverse else oracle.hierarchize)(u.copy(), levels)
+        g = torch.from_numpy(u.copy()).cuda()
+        ws = torch.empty(sgh.sharded_workspace_bytes(levels, 1) // 8 + 1, dtype=torch.float64, device="cuda")
+        comm.transform(g, levels, ws, inverse=inverse)
+        torch.cuda.synchronize()
+        assert_bitwise(g.cpu().numpy(), want)
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
 def test_launch_count_increases(sgh):
     before = sgh.launch_count()
     g = torch.zeros(961, dtype=torch.float64, device="cuda")
