@@ -230,6 +230,26 @@ def test_sharded_plan_bytes_fused(levels, P):
     assert a2a <= 1.01 * (3 + (len(levels) - 1 if len(levels) < 3 else 1.1)) * per
 
 
+def test_plan_c5_single_pass_plans_partition():
+    """Every C5 member whose hierarchization plan is ONE pass with a second
+    blocked axis (two-blocked / prefix two-blocked) writes each point exactly
+    once over its phases; every other FUSED pass without a split inverse does
+    too (the planner's in-place invariant over the whole 4,255-grid set)."""
+    n_box = 0
+    for lv in si.combination_set(4, 22):
+        N = si.num_points(lv)
+        for ph in _plan_passes(lv):
+            if ph[0][0] != "FUSED":
+                continue
+            if any(int(a.get("bt2", "-1")) >= 0 for _, a, _ in ph):
+                if len([l for l in lv if l > 1]) >= 3:      # prefix two-blocked: a partition
+                    n_box += 1
+                    assert sum(p for _, _, p in ph) == N, lv
+                continue
+            assert sum(p for _, _, p in ph) == N, lv
+    assert n_box >= 100
+
+
 def test_plan_two_blocked_forced():
     """SGH_FLAG_TWO_BLOCKED (fuse="two_blocked") selects the two-blocked plan
     wherever one exists (how the GPU parity tests exercise it)."""
