@@ -210,6 +210,9 @@ def main():
                          "paper's 1-D l=27 and 10-D (9,2,..,2) sweep tops; C5cycle is the whole combination "
                          "cycle on the C5 set: hierarchize, gather, scatter, dehierarchize (SURVEY 8(f))")
     ap.add_argument("--impl", default="sgh", choices=["sgh", "reference"])
+    ap.add_argument("--gather-bfs", action="store_true",
+                    help="C5cycle ablation: permute the grids' x_1 rows to BFS order into a scratch copy and gather "
+                         "from it (SGH_FLAG_X1_BFS)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -331,6 +334,7 @@ def sgh_arm(args, rank, world, local_rank):
     members, ids, desc = workload(args.workload)
     sizes = [si.num_points(l) for l in members]
     sharded = args.workload == "C4" and world > 1
+    gather_desc = None
     if args.workload == "C5" and world > 1:
         part = c5_partition(sgh, members, world, args.inverse)[rank]
         my_members, my_ids = [members[i] for i in part], [ids[i] for i in part]
@@ -373,11 +377,26 @@ def sgh_arm(args, rank, world, local_rank):
             cfg = si.CONFIGS["C5"]
             coeffs = [float(si.combination_coefficient(cfg.d, cfg.n, lv)) for lv in my_members]
             sparse = torch.empty(sgh.sparse_num_points(cfg.d, cfg.n), dtype=torch.float64, device=dev)
+            # --gather-bfs (ablation, one GPU): gather from a scratch copy whose
+            # x_1 rows are in BFS order (sgh_permute_x1_bfs + SGH_FLAG_X1_BFS:
+            # same sums; measured slower overall, DESIGN section 1 f3)
+            bfs_views = None
+            if args.gather_bfs and world == 1 and torch.cuda.mem_get_info(dev)[0] > 8 * batch.total_points + (8 << 30):
+                scratch = torch.empty(batch.total_points, dtype=torch.float64, device=dev)
+                bfs_views, off = [], 0
+                for v in batch.views:
+                    bfs_views.append(scratch[off:off + v.numel()])
+                    off += v.numel()
+            gather_desc = ("x_1 rows permuted to BFS order into a scratch copy, then gathered (contiguous reads)"
+                           if bfs_views is not None else "row-major pull")
 
             def step():
                 batch.hierarchize(fuse=fuse)
                 if world > 1:   # ranks continue each other's sums in grid order, then broadcast
                     sgh.gather_chain(batch.views, my_members, coeffs, cfg.n, sparse)
+                elif bfs_views is not None:
+                    sgh.permute_x1_bfs(batch.views, bfs_views, my_members)
+                    sgh.gather(bfs_views, my_members, coeffs, cfg.n, sparse, x1_bfs=True)
                 else:
                     sgh.gather(batch.views, my_members, coeffs, cfg.n, sparse)
                 sgh.scatter(sparse, batch.views, my_members, cfg.n)
@@ -513,7 +532,7 @@ def sgh_arm(args, rank, world, local_rank):
                                           if args.workload == "C5cycle"
                                           else ((f"sharded along x_d, {'halo + coarse-lattice all-gather' if args.sharded == 'halo' else 'NCCL all-to-all'}")
                                                 if sharded else "replicas")),
-                          "seed": si.SEED},
+                          "seed": si.SEED, **({"gather": gather_desc} if gather_desc else {})},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                "gpu_launches": launches, "kernels": kern_tab, "model": model}
         print(json.dumps(out), flush=True)

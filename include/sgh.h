@@ -355,6 +355,11 @@ sgh_status sgh_gather(const double *const *grids, const int32_t *levels, const d
  *  or n - d > 30 (a subspace larger than any grid can hold); otherwise as
  *  sgh_gather.  An empty range does nothing. */
 #define SGH_FLAG_ACCUMULATE 16u
+/* SGH_FLAG_X1_BFS (sgh_gather_ex): every grid's x_1 rows are stored in BFS
+ * order (sgh_permute_x1_bfs) -- the gather then reads contiguous runs of each
+ * level's points instead of one double per 2^{l_1 - lam_1 + 1}; same values,
+ * same additions in the same order: bitwise equal to the row-major gather. */
+#define SGH_FLAG_X1_BFS 128u
 sgh_status sgh_gather_ex(const double *const *grids, const int32_t *levels, const double *coeffs, int32_t d,
                          int64_t num_grids, int32_t n, double *sparse, int64_t sub_begin, int64_t sub_end,
                          uint32_t flags, void *workspace, size_t ws_bytes, void *stream);
@@ -363,6 +368,18 @@ sgh_status sgh_gather_ex(const double *const *grids, const int32_t *levels, cons
  * invalid arguments. */
 int64_t sgh_sparse_num_subspaces(int32_t d, int32_t n);
 int64_t sgh_sparse_subspace_offset(int32_t d, int32_t n, int64_t index);
+
+/* Out-of-place permutation of every x_1 row (n_1 = 2^{l_1} - 1 contiguous
+ * doubles) of each grid into BFS order (Fig. fig:hierDehier: the
+ * level-1 point, then level 2, .., each level by j_1): natural 1-based index i,
+ * level lam = l_1 - tz(i), j = i >> (tz(i) + 1), goes to position
+ * 2^{lam-1} - 1 + j.  The layout SGH_FLAG_X1_BFS gathers from.
+ *  src, dst: host arrays of num_grids DEVICE pointers (N doubles each; dst[g]
+ *            must not alias src[g]); levels: host int32[num_grids][d].
+ *  Stream-ordered; one launch per 96 grids.  Errors: INVALID_ARGUMENT (NULL /
+ *  aliased pointers, invalid levels), CUDA. */
+sgh_status sgh_permute_x1_bfs(const double *const *src, double *const *dst, const int32_t *levels, int32_t d,
+                              int64_t num_grids, void *stream);
 
 /* SCATTER: every point of every grid receives its sparse-grid value
  * (restriction of the combined surpluses; dehierarchize the grids afterwards

@@ -40,6 +40,7 @@ FLAG_TWO_BLOCKED = 32
 FLAG_TABLE_RESIDENT = 64
 FLAG_SCATTER = 8
 FLAG_ACCUMULATE = 16
+FLAG_X1_BFS = 128
 STATUS = {0: "SGH_OK", 1: "SGH_ERR_INVALID_ARGUMENT", 2: "SGH_ERR_CAPACITY", 3: "SGH_ERR_CUDA",
           4: "SGH_ERR_NCCL", 5: "SGH_ERR_WORKSPACE"}
 
@@ -99,6 +100,7 @@ def _load():
         "sgh_gather": (st, [vpp, i32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64,
                             ctypes.c_int32, vp, vp, sz, vp]),
         "sgh_scatter": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, vp, vp, sz, vp]),
+        "sgh_permute_x1_bfs": (st, [vpp, vpp, i32p, ctypes.c_int32, ctypes.c_int64, vp]),
         "sgh_gather_ex": (st, [vpp, i32p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.c_int64,
                                ctypes.c_int32, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
         "sgh_sparse_num_subspaces": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
@@ -128,7 +130,7 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_transform_sharded_halo", "sgh_transform_sharded_halo_loopback", "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
             "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_plan_cost", "sgh_sharded_plan_bytes", "sgh_sparse_num_points",
-            "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter", "sgh_gather_ex",
+            "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter", "sgh_gather_ex", "sgh_permute_x1_bfs",
             "sgh_sparse_num_subspaces", "sgh_sparse_subspace_offset", "sgh_ablation_bfs_permute_1d",
             "sgh_ablation_bfs_hierarchize_1d", "sgh_ablation_bfs_dehierarchize_1d",
             "sgh_status_string", "sgh_last_error", "sgh_version")
@@ -580,12 +582,29 @@ def _combi_common(grids, levels_list):
     return d, flat, ptrs
 
 
-def gather(grids, levels_list, coeffs, n: int, sparse: torch.Tensor = None, stream=None) -> torch.Tensor:
-    """sparse = sum_g coeffs[g] * grids[g] (hierarchical surpluses) in the SG layout."""
+def permute_x1_bfs(src, dst, levels_list, stream=None):
+    """dst[g] = src[g] with every x_1 row in BFS order (sgh_permute_x1_bfs):
+    the layout ``gather(..., x1_bfs=True)`` reads."""
+    d, flat, ptrs = _combi_common(src, levels_list)
+    for g, lv in zip(dst, levels_list):
+        _grid_ptr(g, lv)
+    dptrs = (ctypes.c_void_p * len(dst))(*[g.data_ptr() for g in dst])
+    with torch.cuda.device(src[0].device):
+        _check(lib.sgh_permute_x1_bfs(ptrs, dptrs, flat, d, len(src), _stream(stream)))
+    return dst
+
+
+def gather(grids, levels_list, coeffs, n: int, sparse: torch.Tensor = None, stream=None,
+           x1_bfs: bool = False) -> torch.Tensor:
+    """sparse = sum_g coeffs[g] * grids[g] (hierarchical surpluses) in the SG layout.
+    x1_bfs: the grids' x_1 rows are in BFS order (permute_x1_bfs)."""
     d, flat, ptrs = _combi_common(grids, levels_list)
     dev = grids[0].device
     if sparse is None:
         sparse = torch.empty(sparse_num_points(d, n), dtype=torch.float64, device=dev)
+    if x1_bfs:
+        return gather_ex(grids, levels_list, coeffs, n, sparse, 0, sparse_num_subspaces(d, n), stream=stream,
+                         x1_bfs=True)
     wsb = int(lib.sgh_combi_workspace_bytes(flat, d, len(grids), int(n), 0))
     ws = torch.empty(max(wsb, 16) // 8 + 2, dtype=torch.float64, device=dev)
     c = (ctypes.c_double * len(grids))(*[float(x) for x in coeffs])
@@ -610,7 +629,7 @@ def sparse_subspace_offset(d: int, n: int, index: int) -> int:
 
 
 def gather_ex(grids, levels_list, coeffs, n: int, sparse: torch.Tensor, sub_begin: int, sub_end: int,
-              accumulate: bool = False, stream=None) -> torch.Tensor:
+              accumulate: bool = False, stream=None, x1_bfs: bool = False) -> torch.Tensor:
     """Gather restricted to subspaces [sub_begin, sub_end) (SG order); with
     ``accumulate`` every sum continues from the value already in ``sparse``
     (sgh.h sgh_gather_ex, SGH_FLAG_ACCUMULATE)."""
@@ -621,7 +640,8 @@ def gather_ex(grids, levels_list, coeffs, n: int, sparse: torch.Tensor, sub_begi
     c = (ctypes.c_double * len(grids))(*[float(x) for x in coeffs])
     with torch.cuda.device(dev):
         _check(lib.sgh_gather_ex(ptrs, flat, c, d, len(grids), int(n), ctypes.c_void_p(sparse.data_ptr()),
-                                 int(sub_begin), int(sub_end), FLAG_ACCUMULATE if accumulate else 0,
+                                 int(sub_begin), int(sub_end),
+                                 (FLAG_ACCUMULATE if accumulate else 0) | (FLAG_X1_BFS if x1_bfs else 0),
                                  ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8, _stream(stream)))
     _keep_on(stream, ws)
     return sparse

@@ -72,6 +72,7 @@ struct CombiArgs {
   double *sparse;
   int32_t d, n;
   int32_t accumulate;              // gather: sums start from the values in sparse (SGH_FLAG_ACCUMULATE)
+  int32_t x1_bfs;                  // gather: the grids' x_1 rows are in BFS order (SGH_FLAG_X1_BFS)
 };
 
 // binom / sbase: the tables staged in SMEM (lanes index them with different
@@ -199,6 +200,8 @@ __global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ Com
     }
     const int nc = s_sub.nc;
     const int64_t c0 = s_sub.c0;
+    const bool bfs = A.x1_bfs != 0;
+    const int x1base = (1 << (s_sub.lam[0] - 1)) - 1;     // BFS x_1 rows: level lam_1 starts here
     const int p0 = (int)(q - __ldg(&A.prefix[idx])) * kCombiPts;
     const int np = min(kCombiPts, s_sub.npts - p0);
     int jj[K][D];                                  // 2 j_k + 1 per point
@@ -241,7 +244,10 @@ __global__ void __launch_bounds__(kThreads) k_gather(const __grid_constant__ Com
         for (int u = 0; u < K; ++u) {
           int gi = 0;
 #pragma unroll
-          for (int k = 0; k < D; ++k) gi += ((jj[u][k] << C.sh[k]) - 1) * C.str[k];
+          for (int k = 0; k < D; ++k) {
+            if (k == 0 && bfs) gi += x1base + (jj[u][0] >> 1);   // BFS row: level block, then j_1
+            else gi += ((jj[u][k] << C.sh[k]) - 1) * C.str[k];
+          }
           v[u] = (threadIdx.x + u * kThreads < np) ? __ldg(C.grid + gi) : 0.0;
         }
 #pragma unroll
@@ -468,7 +474,7 @@ static sgh_status run_combi(double *const *grids, const int32_t *levels, const d
   if (!levels || (num_grids > 0 && !grids) || !sparse || (gather && num_grids > 0 && !coeffs))
     return invalid("NULL argument");
   if (num_grids == 0 && !gather) return SGH_OK;
-  if (flags & ~uint32_t(SGH_FLAG_ACCUMULATE)) return invalid("unknown gather flags");
+  if (flags & ~uint32_t(SGH_FLAG_ACCUMULATE | SGH_FLAG_X1_BFS)) return invalid("unknown gather flags");
   CombiPlan P;
   sgh_status st = build_combi_plan(grids, levels, coeffs, d, num_grids, n, gather, P, sub_begin, sub_end);
   if (st != SGH_OK) return st;
@@ -499,6 +505,7 @@ static sgh_status run_combi(double *const *grids, const int32_t *levels, const d
   A.d = d;
   A.n = n;
   A.accumulate = (flags & SGH_FLAG_ACCUMULATE) ? 1 : 0;
+  A.x1_bfs = (flags & SGH_FLAG_X1_BFS) ? 1 : 0;
   if (A.items == 0 || A.tiles == 0) return SGH_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -532,6 +539,126 @@ static sgh_status run_combi(double *const *grids, const int32_t *levels, const d
   prof_end(tok, gather ? 5 : 6, 0, false, 8.0 * pts + 8.0 * double(P.M), s);
   if (e != cudaSuccess) return cuda_fail(e, gather ? "gather launch" : "scatter launch");
   count_launch();
+  return SGH_OK;
+}
+
+// ------------------------------------------------ x_1 rows in BFS order
+// The gather reads grid g's point (j_1, ..) of W_lam at x_1 index
+// (2 j_1 + 1) 2^{l_1 - lam_1}: consecutive sparse points are 2^{l_1-lam_1+1}
+// doubles apart, one useful double per 32-byte sector for every lam_1 < l_1
+// (DRAM reads ~6x the surpluses).  Permuting every x_1 row into BFS order --
+// level 1 first, then level 2, .., each level's points by j_1 (P:232-233,
+// Fig. fig:hierDehier: the paper's BFS layout) -- makes those reads
+// contiguous runs; the sums are unchanged (the same values, added in the
+// same order).  Natural 1-based index i (level lam = l_1 - tz(i),
+// j = i >> (tz(i) + 1)) goes to BFS position 2^{lam-1} - 1 + j.
+constexpr int kPermBatch = 96;     // grids per launch (kernel parameter table)
+constexpr int kPermSeg = 4096;     // points per tile: R whole rows (l_1 <= 12) or a 2^12 row segment
+struct PermGrid {
+  const double *src;
+  double *dst;
+  int64_t rows;                    // N / n_1
+  int32_t l1, R;                   // R rows per tile (l_1 <= 12)
+  FDiv fn1;                        // division by n_1
+};
+struct PermArgs {
+  PermGrid g[kPermBatch];
+  int64_t prefix[kPermBatch + 1];  // tiles
+  int32_t ng;
+};
+
+__global__ void __launch_bounds__(kThreads) k_x1_bfs(const __grid_constant__ PermArgs A) {
+  __shared__ double s[kPermSeg];
+  int gi = 0;
+  const int64_t total = A.prefix[A.ng];
+  for (int64_t q = blockIdx.x; q < total; q += gridDim.x) {
+    while (A.prefix[gi + 1] <= q) ++gi;            // tiles of a CTA only increase
+    const PermGrid &G = A.g[gi];
+    const int64_t lq = q - A.prefix[gi];
+    const int l1 = G.l1;
+    const int n1 = (1 << l1) - 1;
+    __syncthreads();                               // the previous tile's reads of s are done
+    if (l1 <= 12) {                                // R whole rows: one contiguous range
+      const int64_t r0 = lq * G.R;
+      const int nr = (int)min((int64_t)G.R, G.rows - r0);
+      const double *src = G.src + r0 * n1;
+      double *dst = G.dst + r0 * n1;
+      const int cnt = nr * n1;
+      for (int e = threadIdx.x; e < cnt; e += kThreads) s[e] = __ldcs(src + e);
+      __syncthreads();
+      for (int o = threadIdx.x; o < cnt; o += kThreads) {
+        const int row = (int)fdiv((uint32_t)o, G.fn1);
+        const int p = o - row * n1;                // BFS position
+        const int lam = 32 - __clz(p + 1);         // level: positions 2^{lam-1}-1 .. 2^lam-2
+        const int j = p + 1 - (1 << (lam - 1));
+        const int i = (2 * j + 1) << (l1 - lam);   // natural 1-based index
+        dst[o] = s[row * n1 + i - 1];
+      }
+    } else {                                       // one aligned 2^12-index segment of one row
+      const int sh = l1 - 12;
+      const int64_t row = lq >> sh;
+      const int S0 = (int)(lq & ((1 << sh) - 1)) << 12;
+      const double *src = G.src + row * n1;
+      double *dst = G.dst + row * n1;
+      for (int k = threadIdx.x; k < kPermSeg; k += kThreads) {
+        const int i = S0 + k;
+        if (i >= 1 && i <= n1) s[k] = __ldcs(src + i - 1);
+      }
+      __syncthreads();
+      // levels with tz(i) = t < 12: 2^{11-t} points S0 + 2^t (2m + 1), at the
+      // contiguous BFS positions 2^{l1-t-1} - 1 + (S0 >> (t+1)) + m
+      for (int o = threadIdx.x; o < kPermSeg - 1; o += kThreads) {
+        const int t = 11 - (31 - __clz(kPermSeg - 1 - o));   // run t covers o in [4096 - 2^{12-t}, 4096 - 2^{11-t})
+        const int m = o - (kPermSeg - (kPermSeg >> t));
+        const int i = S0 + (1 << t) * (2 * m + 1);
+        dst[((1 << (l1 - t - 1)) - 1) + (S0 >> (t + 1)) + m] = s[i - S0];
+      }
+      if (threadIdx.x == 0 && S0 > 0) {            // the segment's first index: a coarser level
+        const int t = __ffs(S0) - 1;
+        dst[((1 << (l1 - t - 1)) - 1) + (S0 >> (t + 1))] = s[0];
+      }
+    }
+  }
+}
+
+static sgh_status permute_x1_bfs(const double *const *src, double *const *dst, const int32_t *levels, int32_t d,
+                                 int64_t num_grids, cudaStream_t s) {
+  if (num_grids < 0) return invalid("num_grids < 0");
+  if (num_grids > 0 && (!src || !dst || !levels)) return invalid("NULL argument");
+  for (int64_t b = 0; b < num_grids; b += kPermBatch) {
+    PermArgs A;
+    std::memset(&A, 0, sizeof A);
+    A.ng = (int32_t)std::min<int64_t>(kPermBatch, num_grids - b);
+    int64_t acc = 0;
+    for (int k = 0; k < A.ng; ++k) {
+      const int64_t g = b + k;
+      int64_t N = 0;
+      sgh_status st = validate_levels(levels + g * d, d, &N);
+      if (st != SGH_OK) return st;
+      if (!src[g] || !dst[g]) return invalid("grid pointer is NULL");
+      if (src[g] == dst[g]) return invalid("the permutation is out of place (src == dst)");
+      PermGrid &P = A.g[k];
+      P.src = src[g];
+      P.dst = dst[g];
+      P.l1 = levels[g * d];
+      const int64_t n1 = (int64_t(1) << P.l1) - 1;
+      P.rows = N / n1;
+      P.R = P.l1 <= 12 ? (kPermSeg >> P.l1) : 1;
+      P.fn1 = make_fdiv((uint32_t)n1);
+      A.prefix[k] = acc;
+      acc += P.l1 <= 12 ? (P.rows + P.R - 1) / P.R : (P.rows << (P.l1 - 12));
+    }
+    A.prefix[A.ng] = acc;
+    if (acc == 0) continue;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::min<int64_t>(acc, int64_t(sms) * 6);
+    k_x1_bfs<<<(unsigned)grid, kThreads, 0, s>>>(A);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "x1 BFS permutation");
+    count_launch();
+  }
   return SGH_OK;
 }
 
@@ -588,6 +715,13 @@ sgh_status sgh_gather_ex(const double *const *grids, const int32_t *levels, cons
   if (sub_begin == sub_end) return SGH_OK;
   return run_combi(const_cast<double *const *>(grids), levels, coeffs, d, num_grids, n, sparse, workspace, ws_bytes,
                    static_cast<cudaStream_t>(stream), true, sub_begin, sub_end, flags);
+});
+}
+
+sgh_status sgh_permute_x1_bfs(const double *const *src, double *const *dst, const int32_t *levels, int32_t d,
+                              int64_t num_grids, void *stream) {
+  return guarded([&]() -> sgh_status {
+  return permute_x1_bfs(src, dst, levels, d, num_grids, static_cast<cudaStream_t>(stream));
 });
 }
 

@@ -534,6 +534,39 @@ def test_gather_scatter_bitwise(sgh, d, n):
         assert_bitwise(o.cpu().numpy(), w)
 
 
+def _bfs_rows_reference(u, levels):
+    """x_1 rows in BFS order (layout only, numpy): natural 1-based i -> position
+    2^{lam-1} - 1 + j, lam = l_1 - tz(i), j = i >> (tz(i) + 1)."""
+    l1 = levels[0]
+    n1 = (1 << l1) - 1
+    i = np.arange(1, n1 + 1)
+    tz = np.array([(int(x) & -int(x)).bit_length() - 1 for x in i])
+    pos = (1 << (l1 - tz - 1)) - 1 + (i >> (tz + 1))
+    rows = u.reshape(-1, n1)
+    out = np.empty_like(rows)
+    out[:, pos] = rows
+    return out.reshape(-1)
+
+
+@pytest.mark.parametrize("d,n", [(1, 9), (2, 10), (3, 9), (4, 12), (5, 9), (2, 16), (1, 15), (4, 16)], ids=str)
+def test_gather_x1_bfs_bitwise(sgh, d, n):
+    """The BFS-row gather (the grids' x_1 rows permuted into BFS order first,
+    sgh_permute_x1_bfs, then SGH_FLAG_X1_BFS): the permutation matches the
+    layout definition element by element (rows of l_1 <= 12 and of 2^12-index
+    segments), and the gather is bitwise the oracle's."""
+    cs = si.combination_set(d, n)
+    co = [float(si.combination_coefficient(d, n, lv)) for lv in cs]
+    hosts = [oracle.hierarchize(si.fill_uniform(si.num_points(lv), grid_id=g), lv) for g, lv in enumerate(cs)]
+    grids = [torch.from_numpy(h).cuda() for h in hosts]
+    perm = [torch.full_like(g, float("nan")) for g in grids]
+    sgh.permute_x1_bfs(grids, perm, cs)
+    torch.cuda.synchronize()
+    for p_, h, lv in zip(perm, hosts, cs):
+        assert_bitwise(p_.cpu().numpy(), _bfs_rows_reference(h, lv))
+    sp = sgh.gather(perm, cs, co, n, x1_bfs=True)
+    assert_bitwise(sp.cpu().numpy(), oracle.gather(hosts, cs, co, n))
+
+
 @pytest.mark.parametrize("d,n,split,chunks", [(2, 8, 3, 4), (3, 8, 10, 5), (4, 9, 17, 16), (5, 8, 40, 7)])
 def test_gather_ex_chain_bitwise(sgh, d, n, split, chunks):
     """sgh_gather_ex: the grid list split into two CONTIGUOUS blocks, the
