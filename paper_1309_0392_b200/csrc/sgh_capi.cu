@@ -800,6 +800,79 @@ static bool plan_prefix_two_blocked(double *grid, const int32_t *levels, int d, 
   return true;
 }
 
+// PREFIX TWO-BLOCKED DEHIERARCHIZATION (one level, no recursion): the
+// inverse needs, per axis, predecessors that are nodal along that axis and
+// the earlier ones but not yet along the later ones.  With C the set of
+// blocked axes a point is coarse along, the execution order
+//   T^A({a,b})  D_prefix, D_a on the points coarse along both
+//   {b}         the class coarse along b, all axes (its a-ends: T^A's output)
+//   T^B({a,b})  D_b on the points coarse along both (now final)
+//   {a}^A       D_prefix, D_a on the class coarse along a
+//   main        the box tiles, all axes: prefix axes skip the a-end rows
+//               ({a}^A's output) and the b-end rows (final); D_a skips the
+//               b-end rows; D_b reads final b-ends
+//   {a}^B       D_b on the class coarse along a (its b-ends are final)
+// gives every point D_prefix, D_a, D_b in the oracle's order with the right
+// predecessor states (bitwise).  Emitted reversed (the runner reverses
+// dehierarchization phase lists).  Every class must fit one tile.
+static bool plan_prefix_two_blocked_inv(double *grid, const int32_t *levels, int d, std::vector<Task> &phases) {
+  int sq[SGH_MAX_D], m = 0;
+  for (int k = 0; k < d; ++k)
+    if (levels[k] > 1) sq[m++] = levels[k];
+  if (m < 3 || sq[m - 2] < 3 || sq[m - 1] < 3) return false;
+  BoxCtx c;
+  c.grid = grid;
+  c.np = m - 2;
+  c.P0 = 1;
+  for (int j = 0; j < c.np; ++j) {
+    c.pl[j] = (int8_t)sq[j];
+    c.P0 *= (int64_t(1) << sq[j]) - 1;
+  }
+  c.budget = fused_budget_w1() + fused_budget_w1() / 16;
+  const int la = sq[m - 2], lb = sq[m - 1];
+  const int64_t na = (int64_t(1) << la) - 1;
+  c.N = c.P0 * na * ((int64_t(1) << lb) - 1);
+  const BoxAxis a{la, c.P0, 0, la}, b{lb, c.P0 * na, 0, lb};
+  auto lat = [](const BoxAxis &x, int t) {
+    return BoxAxis{x.l - t, x.G << t, x.base + ((int64_t(1) << t) - 1) * x.G, x.l - t};
+  };
+  const uint32_t pre_a = (1u << (c.np + 1)) - 1, only_b = 1u << (c.np + 1);
+  double best = 1e30;
+  std::vector<Task> bestv;
+  for (int ta = 2; ta < la; ++ta)
+    for (int tb = 2; tb < lb; ++tb) {
+      const int64_t ea = (int64_t(1) << ta) + 1, eb = (int64_t(1) << tb) + 1;
+      const int64_t nla = (int64_t(1) << (la - ta)) - 1, nlb = (int64_t(1) << (lb - tb)) - 1;
+      if (c.P0 * ea * eb > c.budget || c.P0 * ea * nlb > c.budget || c.P0 * nla * eb > c.budget ||
+          c.P0 * nla * nlb > c.budget)
+        continue;
+      const BoxAxis al = lat(a, ta), bl = lat(b, tb);
+      Task tAB_A = box_task(c, al, al.l, bl, bl.l);
+      tAB_A.skipmask = only_b;
+      Task tAB_B = box_task(c, al, al.l, bl, bl.l);
+      tAB_B.skipmask = pre_a;
+      BoxAxis af = a;
+      af.f = ta;
+      BoxAxis bf = b;
+      bf.f = tb;
+      Task tB = box_task(c, af, ta, bl, bl.l);
+      Task tA_A = box_task(c, al, al.l, bf, tb);
+      tA_A.skipmask = only_b;
+      Task tA_B = box_task(c, al, al.l, bf, tb);
+      tA_B.skipmask = pre_a;
+      Task tM = box_task(c, a, ta, b, tb);
+      std::vector<Task> ph{tA_B, tM, tA_A, tAB_B, tB, tAB_A};   // reversed execution order
+      const double cost = box_cost(c, std::vector<Task>{tM, tA_A, tA_B, tB, tAB_A, tAB_B}, 0);
+      if (cost < best) {
+        best = cost;
+        bestv.swap(ph);
+      }
+    }
+  if (bestv.empty()) return false;
+  phases.insert(phases.end(), bestv.begin(), bestv.end());
+  return true;
+}
+
 // Halo-sharded hierarchization of one rank's row shard as ONE box plan
 // (SURVEY 8(f) 1 with the a4 block scheme): the shard holds the aligned
 // super-block r (level T) of every x_d pole, its first row and one spare halo
@@ -1052,9 +1125,10 @@ void plan_grid(double *grid, const int32_t *levels, int d, uint32_t flags, std::
         }
     // prefix two-blocked plan (hierarchization, >= 3 non-trivial axes)
     static const bool no_ptb = tuning_env("SGH_NO_PTB") != nullptr;   // experiment
-    if (!inv && g_outer_mult == 1 && !no_ptb) {
+    if (g_outer_mult == 1 && !no_ptb) {
       std::vector<Task> ph;
-      if (plan_prefix_two_blocked(grid, levels, d, ph, (flags & SGH_FLAG_TWO_BLOCKED) != 0)) {
+      if (inv ? plan_prefix_two_blocked_inv(grid, levels, d, ph)
+              : plan_prefix_two_blocked(grid, levels, d, ph, (flags & SGH_FLAG_TWO_BLOCKED) != 0)) {
         const double c = pass_cost(ph);
         if (c < bc - 1e-12) {
           bc = c;

@@ -550,13 +550,16 @@ struct ItemWalk {
 // ran first) and must not be transformed again.
 struct HaloSkip {
   bool on;
+  bool zs;      // also the second blocked axis' end rows (z = 0, ez2 - 1): the
+                // inverse prefix two-blocked tile, whose b-end rows are final
   FDiv fA, fE;  // division by A (tile rows before the blocked axis), by ej
-  int ej;
+  int ej, ez2;
   __device__ __forceinline__ bool skip(int row) const {  // row: the pole's first local row
     if (!on) return false;
     const uint32_t q = fdiv((uint32_t)row, fA);
-    const int y = (int)(q - fdiv(q, fE) * (uint32_t)ej);
-    return y == 0 || y == ej - 1;
+    const uint32_t z = fdiv(q, fE);
+    const int y = (int)(q - z * (uint32_t)ej);
+    return y == 0 || y == ej - 1 || (zs && (z == 0 || (int)z == ez2 - 1));
   }
 };
 
@@ -1301,10 +1304,13 @@ __device__ __forceinline__ void fused_compute_rm(const Task &T, const FusedTile 
   const bool blocked = T.bj >= 0 && T.bt < T.gl[T.bj];
   HaloSkip hs;
   hs.on = false;
+  hs.zs = false;
   if (blocked) {
     hs.fA = T.fA;
     hs.fE = T.fE;
     hs.ej = T.ej;
+    hs.zs = INV && T.bt2 >= 0;
+    hs.ez2 = (1 << (T.bt2 >= 0 ? T.bt2 : 0)) + 1;
   }
 #ifdef SGH_DEBUG_NOCOMPUTE
   for (int j = 0; j < 0; ++j) {                     // timing experiment: load + store only

@@ -198,8 +198,11 @@ def test_plan_prefix_two_blocked_partition(levels):
     """Prefix two-blocked hierarchization plans (>= 3 non-trivial axes): ONE
     pass whose phases -- the box tiles (fine along both blocked axes), then
     the classes coarse along {a}, {b}, {a, b} -- write every point exactly
-    once; the first phase is the largest (the tiles).  Dehierarchization never
-    takes it (the inverse would need half-transformed block ends)."""
+    once; the first phase is the largest (the tiles).  The dehierarchization
+    plan, where one exists, is six phases emitted in reverse execution order
+    ({a}^B, tiles, {a}^A, T^B, {b}, T^A): the classes coarse along a and along
+    both run in two halves (by axes), so tiles + {a} + {b} + {a, b} cover
+    every point once."""
     N = si.num_points(levels)
     p = _plan_passes(levels, fuse="two_blocked")
     assert len(p) == 1 and int(p[0][0][1]["bt2"]) >= 2
@@ -208,8 +211,15 @@ def test_plan_prefix_two_blocked_partition(levels):
     sq = [l for l in levels if l > 1]
     assert all(a["levels"].count(",") == len(sq) - 1 for _, a, _ in p[0])
     q = _plan_passes(levels, inverse=True, fuse="two_blocked")
-    assert all(len(ph) == 0 or ph[0][1].get("levels", "").count(",") < len(sq) - 1 or
-               int(ph[0][1].get("bt2", "-1")) < 0 for ph in q)
+    inv_box = [ph for ph in q if len(ph) == 6 and any(int(a.get("bt2", "-1")) >= 0 for _, a, _ in ph)
+               and all(a.get("levels", "").count(",") == len(sq) - 1 for _, a, _ in ph)]
+    for ph in inv_box:
+        pq = [x for _, _, x in ph]
+        assert pq[0] == pq[2] and pq[3] == pq[5]
+        assert pq[1] + pq[2] + pq[4] + pq[5] == N and pq[1] == max(pq)
+        sk = [int(a.get("skip", "0")) for _, a, _ in ph]
+        b_bit = 1 << (len(sq) - 1)
+        assert sk[1] == 0 and sk[4] == 0 and sk[2] == sk[5] == b_bit and sk[0] == sk[3] == b_bit - 1
 
 
 @pytest.mark.parametrize("levels,P", [((14, 13), 2), ((14, 13), 4), ((14, 13), 8), ((8, 8, 8), 2), ((8, 8, 8), 4)],

@@ -276,6 +276,28 @@ def test_prefix_two_blocked_bitwise(sgh, levels):
     assert_bitwise(gpu_transform(sgh, u, levels, fuse="two_blocked"), want)
 
 
+PREFIX_TWO_BLOCKED_INV_SHAPES = [(2, 2, 9, 9), (4, 6, 8), (2, 10, 10), (5, 5, 5), (3, 4, 3), (2, 2, 2, 5, 5),
+                                 (3, 9, 4), (4, 4, 11), (3, 7, 9), (2, 8, 8), (1, 3, 1, 7, 9)]
+
+
+@pytest.mark.parametrize("levels", PREFIX_TWO_BLOCKED_INV_SHAPES, ids=str)
+def test_prefix_two_blocked_dehier_bitwise(sgh, levels):
+    """Prefix two-blocked DEhierarchization (one level: the points coarse along
+    both blocked axes through a and then b, the class coarse along b, the box
+    tiles with their end rows untouched, the class coarse along a in two
+    halves) forced with fuse="two_blocked": bitwise vs the oracle, also on the
+    oracle's own hierarchization output."""
+    N = si.num_points(levels)
+    a = si.fill_uniform(N, grid_id=N % 997)
+    d = sgh.plan_describe(levels, inverse=True, fuse="two_blocked")
+    assert any(int(x.split("bt2=")[1].split()[0]) >= 2 for x in d.splitlines() if "bt2=" in x)
+    assert_bitwise(gpu_transform(sgh, a, levels, inverse=True, fuse="two_blocked"),
+                   oracle.dehierarchize(a.copy(), levels))
+    h = oracle.hierarchize(a.copy(), levels)
+    assert_bitwise(gpu_transform(sgh, h, levels, inverse=True, fuse="two_blocked"),
+                   oracle.dehierarchize(h.copy(), levels))
+
+
 def test_two_blocked_c4_golden(sgh):
     c = SD["configs"]["C4"]
     g = torch.empty(si.num_points(c["levels"]), dtype=torch.float64, device="cuda")
