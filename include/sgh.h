@@ -111,6 +111,12 @@ sgh_status sgh_transform_ex(double *grid, const int32_t *levels, int32_t d,
                             const int32_t *axis_order, uint32_t axis_mask,
                             uint32_t flags, void *stream);
 
+/* The SURVEY 8(b) spelling of the general entry: sgh_transform_ex with all
+ * axes (axis_mask 0).  workspace / ws_bytes are accepted and unused (may be
+ * NULL / 0): every single-grid plan runs in place. */
+sgh_status sgh_hierarchize_ex(double *grid, const int32_t *levels, int32_t d, const int32_t *axis_order,
+                              uint32_t flags, void *workspace, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------ batched combination set */
 
 /* Bytes of device workspace the batched calls need for num_grids grids of
@@ -129,6 +135,13 @@ size_t sgh_batched_workspace_bytes(const int32_t *levels, int32_t d, int64_t num
 sgh_status sgh_hierarchize_batched(double *const *grids, const int32_t *levels, int32_t d,
                                    int64_t num_grids, uint32_t flags,
                                    void *workspace, size_t ws_bytes, void *stream);
+
+/* SURVEY 8(b) spellings: sgh_hierarchize_batched with SGH_FLAG_DEHIERARCHIZE
+ * set, and sgh_batched_workspace_bytes. */
+sgh_status sgh_dehierarchize_batched(double *const *grids, const int32_t *levels, int32_t d,
+                                     int64_t num_grids, uint32_t flags,
+                                     void *workspace, size_t ws_bytes, void *stream);
+size_t sgh_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags);
 
 /* Device bytes sgh_transform_batched_host() needs: every grid (256-byte
  * aligned) plus one task table per transfer chunk. */

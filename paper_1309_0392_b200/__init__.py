@@ -71,6 +71,9 @@ def _load():
         "sgh_transform_ex": (st, [vp, i32p, ctypes.c_int32, i32p, ctypes.c_uint32, ctypes.c_uint32, vp]),
         "sgh_batched_workspace_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32]),
         "sgh_hierarchize_batched": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
+        "sgh_dehierarchize_batched": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
+        "sgh_workspace_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32]),
+        "sgh_hierarchize_ex": (st, [vp, i32p, ctypes.c_int32, i32p, ctypes.c_uint32, vp, sz, vp]),
         "sgh_batched_host_buffer_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32]),
         "sgh_transform_batched_host": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, vp, sz, vp]),
         "sgh_shard_rows": (st, [i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, i64p, i64p]),
@@ -122,7 +125,8 @@ def _load():
 
 
 lib = _load()
-EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_transform_ex",
+EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_transform_ex", "sgh_hierarchize_ex",
+            "sgh_dehierarchize_batched", "sgh_workspace_bytes",
             "sgh_batched_workspace_bytes", "sgh_hierarchize_batched", "sgh_batched_host_buffer_bytes",
             "sgh_transform_batched_host", "sgh_shard_rows", "sgh_shard_layout", "sgh_comm_create", "sgh_comm_destroy",
             "sgh_comm_unique_id", "sgh_sharded_workspace_bytes", "sgh_hierarchize_sharded",

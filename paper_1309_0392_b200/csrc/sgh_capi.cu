@@ -1667,6 +1667,25 @@ sgh_status sgh_transform_ex(double *grid, const int32_t *levels, int32_t d, cons
 });
 }
 
+sgh_status sgh_hierarchize_ex(double *grid, const int32_t *levels, int32_t d, const int32_t *axis_order,
+                              uint32_t flags, void *workspace, size_t ws_bytes, void *stream) {
+  (void)workspace;                                 // every single-grid pass runs in place (sgh.h)
+  (void)ws_bytes;
+  return guarded([&]() -> sgh_status {
+  return transform_single(grid, levels, d, axis_order, 0u, flags, stream);
+});
+}
+
+size_t sgh_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
+  return sgh_batched_workspace_bytes(levels, d, num_grids, flags);
+}
+
+sgh_status sgh_dehierarchize_batched(double *const *grids, const int32_t *levels, int32_t d, int64_t num_grids,
+                                     uint32_t flags, void *workspace, size_t ws_bytes, void *stream) {
+  return sgh_hierarchize_batched(grids, levels, d, num_grids, flags | SGH_FLAG_DEHIERARCHIZE, workspace, ws_bytes,
+                                 stream);
+}
+
 size_t sgh_batched_workspace_bytes(const int32_t *levels, int32_t d, int64_t num_grids, uint32_t flags) {
   return guarded_value<size_t>(0, [&]() -> size_t {
   if (validate_batch(nullptr, levels, d, num_grids, false) != SGH_OK || num_grids == 0) return 0;

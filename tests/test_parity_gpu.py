@@ -527,6 +527,35 @@ def test_sharded_nccl_one_rank_bitwise(sgh, levels, inverse):
         dist.destroy_process_group()
 
 
+def test_survey_abi_spellings_bitwise(sgh):
+    """The SURVEY 8(b) spellings: sgh_hierarchize_ex (workspace accepted,
+    unused) and sgh_dehierarchize_batched / sgh_workspace_bytes, called through
+    the C ABI directly: bitwise vs the oracle."""
+    import ctypes
+    lv = (5, 4, 6)
+    N = si.num_points(lv)
+    u = si.fill_uniform(N, grid_id=5)
+    g = torch.from_numpy(u.copy()).cuda()
+    a = (ctypes.c_int32 * 3)(*lv)
+    assert sgh.lib.sgh_hierarchize_ex(ctypes.c_void_p(g.data_ptr()), a, 3, None, 0, None, 0, None) == 0
+    torch.cuda.synchronize()
+    h = oracle.hierarchize(u.copy(), lv)
+    assert_bitwise(g.cpu().numpy(), h)
+    members = [(5, 4, 6), (3, 3, 3), (7, 2, 1)]
+    flat = (ctypes.c_int32 * 9)(*[x for m in members for x in m])
+    hosts = [oracle.hierarchize(si.fill_uniform(si.num_points(m), grid_id=i), m) for i, m in enumerate(members)]
+    gs = [torch.from_numpy(x.copy()).cuda() for x in hosts]
+    ptrs = (ctypes.c_void_p * 3)(*[x.data_ptr() for x in gs])
+    wsb = sgh.lib.sgh_workspace_bytes(flat, 3, 3, 1)
+    assert wsb == sgh.lib.sgh_batched_workspace_bytes(flat, 3, 3, 1) > 0
+    ws = torch.empty(wsb // 8 + 2, dtype=torch.float64, device="cuda")
+    assert sgh.lib.sgh_dehierarchize_batched(ptrs, flat, 3, 3, 0, ctypes.c_void_p(ws.data_ptr()), ws.numel() * 8,
+                                             None) == 0
+    torch.cuda.synchronize()
+    for x, hst, m in zip(gs, hosts, members):
+        assert_bitwise(x.cpu().numpy(), oracle.dehierarchize(hst.copy(), m))
+
+
 def test_launch_count_increases(sgh):
     before = sgh.launch_count()
     g = torch.zeros(961, dtype=torch.float64, device="cuda")
