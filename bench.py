@@ -151,14 +151,30 @@ class ClockSampler:
 # ------------------------------------------------------------ cpu baseline
 def oracle_rate(members, ids, target_cpu_s=12.0, max_points=400_000_000, threads=None, steps=1, warmup=0,
                 seed=13090392):
-    """Time the CPU oracle (plain Alg. 1, one grid per thread) on a bounded,
-    deterministic sample of the workload.  Returns (Gpoints/s, sample desc, cores, per-step times)."""
+    """Time the CPU oracle (plain Alg. 1, one grid per thread; a single-grid
+    workload: its poles split over the threads) on a bounded, deterministic
+    sample of the workload.  Returns (Gpoints/s, sample desc, cores, per-step times)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import oracle
     import sgh_inputs as si
     threads = threads or os.cpu_count() or 1
     sizes = [si.num_points(l) for l in members]
+    if len(members) == 1:
+        # single-grid workloads (C2-C4, S1, S10): the whole grid, each axis
+        # pass's poles split over the host threads (SURVEY 8(c) "--threads T
+        # splits poles"; same arithmetic, bitwise equal)
+        g = oracle.fill_uniform(sizes[0], seed, ids[0])
+        times = []
+        for s in range(warmup + steps):
+            t0 = time.perf_counter()
+            oracle.transform_threads(g, members[0], threads)
+            dt = time.perf_counter() - t0
+            if s >= warmup:
+                times.append(dt)
+        desc = (f"the whole grid {tuple(members[0])} ({sizes[0]:,} points), plain Alg. 1 oracle, poles of "
+                f"each axis pass split over {threads} threads")
+        return sizes[0] / (sum(times) / len(times)) / 1e9, desc, threads, times, sizes[0]
     # calibrate single-thread rate on a mid-sized member
     order = sorted(range(len(members)), key=lambda i: sizes[i])
     probe = order[len(order) // 2]
@@ -306,7 +322,8 @@ def reference_arm(args, rank, world):
            # the sgh arm's config keys (the same workload), plus the bounded sample timed per step
            "config": {"workload": desc, "points": total, "bytes": 8 * total,
                       "l2": "host memory (oracle on host cores)",
-                      "parallelism": f"oracle, one grid per host thread ({cores} threads), rank 0 only",
+                      "parallelism": (f"oracle, one grid per host thread ({cores} threads), rank 0 only" if len(members) > 1
+                                      else f"oracle, poles split over {cores} host threads, rank 0 only"),
                       "seed": si.SEED, "sample_points_per_step": npts},
            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
     ):
         cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
-               _SRC, "-o", _LIB, "-lm"]
+               _SRC, "-o", _LIB, "-lm", "-lpthread"]
         subprocess.check_call(cmd, cwd=_HERE)
     return _LIB
 
@@ -54,6 +54,8 @@ def lib():
             f = getattr(L, name)
             f.argtypes = [_f64p, _i32p, ctypes.c_int32, _i32p]
             f.restype = ctypes.c_int
+        L.sgo_transform_threads.argtypes = [_f64p, _i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+        L.sgo_transform_threads.restype = ctypes.c_int
         L.sgo_counted_hierarchize.argtypes = [_f64p, _i32p, ctypes.c_int32, _i64p, _i64p]
         L.sgo_counted_hierarchize.restype = ctypes.c_int
         L.sgo_flop_count.argtypes = [_i32p, ctypes.c_int32]
@@ -106,6 +108,19 @@ def hierarchize(grid: np.ndarray, levels, axis_order=None) -> np.ndarray:
     rc = lib().sgo_hierarchize(_grid(grid), p, d, op)
     if rc:
         raise ValueError(f"sgo_hierarchize failed ({rc})")
+    return grid
+
+
+def transform_threads(grid: np.ndarray, levels, threads: int, inverse: bool = False) -> np.ndarray:
+    """In place, Alg. 1 (or its inverse) with each axis pass's poles split over
+    ``threads`` pthreads -- timing only (bench.py cpu_baseline), bitwise equal to
+    ``hierarchize`` / ``dehierarchize``; returns ``grid``."""
+    _a, p, d = _levels(levels)
+    if grid.size != num_points(levels):
+        raise ValueError("grid size does not match levels")
+    rc = lib().sgo_transform_threads(_grid(grid), p, d, int(bool(inverse)), int(threads))
+    if rc:
+        raise ValueError(f"sgo_transform_threads failed ({rc})")
     return grid
 
 

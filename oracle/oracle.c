@@ -7,11 +7,12 @@
  * into a scratch vector, transformed, and scattered back (a plain copy; it does
  * not change any arithmetic).
  *
- * Build: gcc -O2 -std=c11 -ffp-contract=off -fPIC -shared oracle.c -o liboracle.so
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fPIC -shared oracle.c -o liboracle.so -lm -lpthread
  */
 #include "oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -140,6 +141,63 @@ int sgo_dehierarchize(double *grid, const int32_t *levels, int32_t d, const int3
         if (rc) return rc;
     }
     return 0;
+}
+
+/* Timing only (bench.py cpu_baseline, SURVEY 8(c) "--threads T splits poles"):
+ * the same Alg. 1 with the poles of each axis pass split into T contiguous
+ * ranges, one pthread per range, each with its own pole scratch.  Poles are
+ * independent, so the result is bitwise that of sgo_hierarchize. */
+struct pole_range {
+    double *grid;
+    const int32_t *levels;
+    int32_t d, axis, inverse;
+    int64_t p0, p1;      /* pole indices p = o*S + r in [p0, p1) */
+    int rc;
+};
+
+static void *pole_range_run(void *arg) {
+    struct pole_range *R = (struct pole_range *)arg;
+    int64_t S, n, O;
+    pole_extents(R->levels, R->d, R->axis, &S, &n, &O);
+    double *pole = (double *)malloc((size_t)n * sizeof(double));
+    if (!pole) { R->rc = -1; return NULL; }
+    for (int64_t p = R->p0; p < R->p1; ++p) {
+        const int64_t o = p / S, r = p % S;
+        double *base = R->grid + o * n * S + r;
+        for (int64_t i = 0; i < n; ++i) pole[i] = base[i * S];
+        if (R->inverse) dehierarchize_pole(pole, R->levels[R->axis]);
+        else hierarchize_pole(pole, R->levels[R->axis], NULL, NULL);
+        for (int64_t i = 0; i < n; ++i) base[i * S] = pole[i];
+    }
+    free(pole);
+    R->rc = 0;
+    return NULL;
+}
+
+int sgo_transform_threads(double *grid, const int32_t *levels, int32_t d, int32_t inverse, int32_t threads) {
+    if (!grid || !valid_levels(levels, d) || threads < 1 || threads > 1024) return -1;
+    struct pole_range *R = (struct pole_range *)calloc((size_t)threads, sizeof(*R));
+    pthread_t *tid = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    if (!R || !tid) { free(R); free(tid); return -1; }
+    int rc = 0;
+    for (int32_t k = 0; k < d && !rc; ++k) {           /* P:125, dimensions in order */
+        if (levels[k] == 1) continue;
+        int64_t S, n, O;
+        pole_extents(levels, d, k, &S, &n, &O);
+        const int64_t poles = O * S;
+        for (int32_t t = 0; t < threads; ++t) {
+            R[t] = (struct pole_range){grid, levels, d, k, inverse,
+                                       poles * t / threads, poles * (t + 1) / threads, 0};
+            if (pthread_create(&tid[t], NULL, pole_range_run, &R[t])) { rc = -1; threads = t; break; }
+        }
+        for (int32_t t = 0; t < threads; ++t) {
+            pthread_join(tid[t], NULL);
+            if (R[t].rc) rc = -1;
+        }
+    }
+    free(R);
+    free(tid);
+    return rc;
 }
 
 int sgo_counted_hierarchize(double *grid, const int32_t *levels, int32_t d,

@@ -49,6 +49,12 @@ int sgo_hierarchize(double *grid, const int32_t *levels, int32_t d, const int32_
 int sgo_dehierarchize_axis(double *grid, const int32_t *levels, int32_t d, int32_t axis);
 int sgo_dehierarchize(double *grid, const int32_t *levels, int32_t d, const int32_t *axis_order);
 
+/* Timing only (bench.py cpu_baseline): sgo_hierarchize (inverse = 0) or
+ * sgo_dehierarchize (inverse = 1) with axis order 1..d and the poles of every
+ * axis pass split over `threads` pthreads (poles are independent);
+ * bitwise the same result.  Returns 0, or -1 on bad args. */
+int sgo_transform_threads(double *grid, const int32_t *levels, int32_t d, int32_t inverse, int32_t threads);
+
 /* Alg. 1 instrumented ("verified by instructing the code"): performs the
  * same updates and counts every floating point add/sub and multiply. */
 int sgo_counted_hierarchize(double *grid, const int32_t *levels, int32_t d,

@@ -208,6 +208,20 @@ def test_round_trip(levels):
     assert normwise(v, u) <= 1e-13
 
 
+@pytest.mark.parametrize("levels", [(5, 5), (7, 3, 4), (1, 6, 2), (3, 3, 3, 3), (11,)], ids=str)
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_threaded_timing_oracle_is_alg1(levels, threads):
+    """The pole-threaded timing variant (bench cpu_baseline) is bitwise the
+    single-thread Alg. 1 in both directions: poles are independent."""
+    u = si.fill_uniform(si.num_points(levels), grid_id=5)
+    a = oracle.hierarchize(u.copy(), levels)
+    b = oracle.transform_threads(u.copy(), levels, threads)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    c = oracle.dehierarchize(a.copy(), levels)
+    e = oracle.transform_threads(a.copy(), levels, threads, inverse=True)
+    assert np.array_equal(c.view(np.uint64), e.view(np.uint64))
+
+
 def test_axis_order_and_linearity():
     """Tensor-product structure: axis permutations agree, and the
     transform is linear, normwise <= 1e-14."""
