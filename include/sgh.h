@@ -249,6 +249,39 @@ sgh_status sgh_transform_sharded_halo_loopback(double *const *shards, const int3
                                                int32_t nranks, uint32_t flags, void *workspace, size_t ws_bytes,
                                                void *stream);
 
+/* ---- device-API (LSA) exchange for the all-to-all path (SURVEY 8(f) 4 iii) ----
+ * The re-shard of sgh_hierarchize_sharded done inside kernels over NVLink peer
+ * memory (NCCL 2.28 device API) instead of pack -> ncclSend/Recv -> unpack:
+ * rank r's kernel stores its rows(r) x C_q blocks straight into rank q's slab
+ * (a symmetric window, layout n_d x |C_q| row-major) and, after the x_d pass
+ * (Alg. 1's outer loop reaching d), loads its blocks back from
+ * every rank's slab into its shard.  Same arithmetic and order as the NCCL
+ * path: bitwise identical to the single-grid transform.
+ *
+ * sgh_comm_lsa_enable: COLLECTIVE over the communicator's ranks, once (not in
+ *   the hot call): allocates (ncclMemAlloc) and registers a symmetric window of
+ *   window_bytes (>= sgh_sharded_lsa_window_bytes of the largest grid to be
+ *   transformed; library-owned, freed by sgh_comm_destroy) and a device
+ *   communicator with one LSA barrier per exchange CTA.  SGH_ERR_NCCL when the
+ *   load/store-accessible team does not span every rank (e.g. ranks on several
+ *   nodes) or the device API is unavailable; SGH_ERR_INVALID_ARGUMENT when
+ *   already enabled or nranks > 64.
+ * sgh_transform_sharded_lsa: COLLECTIVE; shard = this rank's rows (no spare
+ *   row), in place; flags: SGH_FLAG_DEHIERARCHIZE for the inverse.  Needs no
+ *   workspace (the window is the slab).  SGH_ERR_WORKSPACE if the window is
+ *   too small.  Stream-ordered; the exchange kernels synchronize with the
+ *   peers' exchange kernels through the LSA barriers only.
+ * sgh_transform_sharded_lsa_loopback (test): the same kernels for nranks
+ *   VIRTUAL ranks on the current device (window pointers from a table, no
+ *   barriers); workspace: nranks * sgh_sharded_lsa_window_bytes() bytes. */
+sgh_status sgh_comm_lsa_enable(void *comm, size_t window_bytes);
+size_t sgh_sharded_lsa_window_bytes(const int32_t *levels, int32_t d, int32_t nranks);
+sgh_status sgh_transform_sharded_lsa(double *shard, const int32_t *levels, int32_t d, void *comm, uint32_t flags,
+                                     void *stream);
+sgh_status sgh_transform_sharded_lsa_loopback(double *const *shards, const int32_t *levels, int32_t d,
+                                              int32_t nranks, uint32_t flags, void *workspace, size_t ws_bytes,
+                                              void *stream);
+
 /* ----------------------------------------- harness utilities (not the method) */
 
 /* Seeded counter-based fill: value of global flat

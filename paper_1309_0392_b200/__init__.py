@@ -89,6 +89,11 @@ def _load():
         "sgh_transform_sharded_halo": (st, [vp, i32p, ctypes.c_int32, vp, ctypes.c_uint32, vp, sz, vp]),
         "sgh_transform_sharded_halo_loopback": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
                                                      vp, sz, vp]),
+        "sgh_comm_lsa_enable": (st, [vp, sz]),
+        "sgh_sharded_lsa_window_bytes": (sz, [i32p, ctypes.c_int32, ctypes.c_int32]),
+        "sgh_transform_sharded_lsa": (st, [vp, i32p, ctypes.c_int32, vp, ctypes.c_uint32, vp]),
+        "sgh_transform_sharded_lsa_loopback": (st, [vpp, i32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+                                                    vp, sz, vp]),
         "sgh_fill_uniform": (st, [vp, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, vp]),
         "sgh_fill_uniform_batched": (st, [vpp, i64p, u64p, ctypes.c_int64, ctypes.c_uint64, vp, sz, vp]),
         "sgh_digest": (st, [vp, ctypes.c_int64, ctypes.c_int64, u64p, vp]),
@@ -131,7 +136,9 @@ EXPORTED = ("sgh_num_points", "sgh_hierarchize", "sgh_dehierarchize", "sgh_trans
             "sgh_transform_batched_host", "sgh_shard_rows", "sgh_shard_layout", "sgh_comm_create", "sgh_comm_destroy",
             "sgh_comm_unique_id", "sgh_sharded_workspace_bytes", "sgh_hierarchize_sharded",
             "sgh_dehierarchize_sharded", "sgh_transform_sharded_loopback", "sgh_sharded_halo_workspace_bytes",
-            "sgh_transform_sharded_halo", "sgh_transform_sharded_halo_loopback", "sgh_fill_uniform",
+            "sgh_transform_sharded_halo", "sgh_transform_sharded_halo_loopback", "sgh_comm_lsa_enable",
+            "sgh_sharded_lsa_window_bytes", "sgh_transform_sharded_lsa", "sgh_transform_sharded_lsa_loopback",
+            "sgh_fill_uniform",
             "sgh_fill_uniform_batched", "sgh_digest", "sgh_digest_batched", "sgh_launch_count",
             "sgh_profile_enable", "sgh_profile_read", "sgh_plan_describe", "sgh_plan_cost", "sgh_sharded_plan_bytes", "sgh_sparse_num_points",
             "sgh_combi_workspace_bytes", "sgh_gather", "sgh_scatter", "sgh_gather_ex", "sgh_permute_x1_bfs",
@@ -527,6 +534,22 @@ class ShardComm:
                                                   workspace.numel() * workspace.element_size(), _stream(stream)))
         return shard
 
+    def enable_lsa(self, window_bytes: int):
+        """Collective: the device-API (NVLink load/store) exchange for
+        ``transform_lsa`` with a library-owned symmetric window of
+        ``window_bytes`` (>= sharded_lsa_window_bytes of the grid)."""
+        _check(lib.sgh_comm_lsa_enable(self.handle, int(window_bytes)))
+
+    def transform_lsa(self, shard: torch.Tensor, levels, inverse=False, stream=None):
+        """All-to-all sharded pass with the re-shard inside kernels over peer
+        memory (sgh_transform_sharded_lsa); ``shard`` = this rank's rows."""
+        a, d = _levels_arr(levels)
+        with torch.cuda.device(shard.device):
+            _check(lib.sgh_transform_sharded_lsa(_grid_ptr(shard, None), a, d, self.handle,
+                                                 ctypes.c_uint32(FLAG_DEHIERARCHIZE if inverse else 0),
+                                                 _stream(stream)))
+        return shard
+
     def close(self):
         if self.handle:
             lib.sgh_comm_destroy(self.handle)
@@ -548,6 +571,25 @@ def transform_sharded_loopback(shards, levels, workspace: torch.Tensor, inverse=
         _check(lib.sgh_transform_sharded_loopback(ptrs, a, d, P, FLAG_DEHIERARCHIZE if inverse else 0,
                                                   ctypes.c_void_p(workspace.data_ptr()),
                                                   workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def sharded_lsa_window_bytes(levels, nranks: int) -> int:
+    a, d = _levels_arr(levels)
+    return int(lib.sgh_sharded_lsa_window_bytes(a, d, int(nranks)))
+
+
+def transform_sharded_lsa_loopback(shards, levels, workspace: torch.Tensor, inverse=False, stream=None):
+    """The device-API exchange kernels for len(shards) virtual ranks on one
+    device (test utility): window pointers from a table, no barriers."""
+    P = len(shards)
+    a, d = _levels_arr(levels)
+    ptrs = (ctypes.c_void_p * P)(*[s.data_ptr() for s in shards])
+    with torch.cuda.device(workspace.device):
+        _check(lib.sgh_transform_sharded_lsa_loopback(ptrs, a, d, P, FLAG_DEHIERARCHIZE if inverse else 0,
+                                                      ctypes.c_void_p(workspace.data_ptr()),
+                                                      workspace.numel() * workspace.element_size(),
+                                                      _stream(stream)))
+    return shards
 
 
 def sharded_halo_workspace_bytes(levels, nranks: int) -> int:

@@ -16,10 +16,12 @@
 // [r 2^{l_d-p}, (r+1) 2^{l_d-p}) intersected with [1, n_d].
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <algorithm>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -148,6 +150,13 @@ static sgh_status slab_axis(double *slab, const ShardGeom &G, int rank, bool inv
 struct Comm {
   ncclComm_t nccl = nullptr;
   int nranks = 1, rank = 0;
+  // device-API (LSA) exchange, after sgh_comm_lsa_enable: a symmetric window
+  // (every rank's slab) and a device communicator with one LSA barrier per CTA
+  bool lsa = false;
+  void *win_buf = nullptr;
+  size_t win_bytes = 0;
+  ncclWindow_t win = nullptr;
+  ncclDevComm dev{};
 };
 
 static sgh_status nccl_fail(ncclResult_t r, const char *where) {
@@ -496,6 +505,224 @@ static sgh_status sharded_halo_loopback(double *const *shards, const int32_t *le
   return SGH_OK;
 }
 
+// ====================================== device-API (LSA) all-to-all re-shard
+// the re-shard of the all-to-all path done inside kernels
+// over NVLink peer memory (NCCL 2.28 device API, load/store-accessible team)
+// instead of pack -> ncclSend/Recv -> unpack.  Every rank's slab n_d x |C_q|
+// (the layout the receiver's x_d pass needs, unchanged) lives in a symmetric
+// window.  Forward: each rank PUSHES its rows(r) x C_q blocks straight from
+// its shard into rank q's window at row offset row_begin(r) -- the pack and
+// the exchange are one kernel.  Backward: each rank PULLS rows(r) x C_q from
+// every rank q's window into its shard's column block -- the exchange and the
+// unpack are one kernel.  Ordering: CTA b of every rank meets CTA b of every
+// other rank at an LSA barrier (one per CTA index): push = barrier (no rank
+// still reads the windows from a previous call) -> stores -> barrier
+// (release: the owner's x_d pass sees them); pull = barrier (acquire: every
+// rank's x_d pass is done) -> loads.  The arithmetic (local axes, x_d pass) is
+// the same launches as the NCCL path: bitwise.  The loopback variant runs the
+// same kernels for P virtual ranks on one device with a table of window
+// pointers and no barriers (stream order).
+constexpr int kLsaThreads = 512;
+constexpr int kLsaMaxCtas = 296;       // LSA barriers requested per communicator
+constexpr int kLsaMaxP = 64;
+
+struct ReshardArgs {
+  double *shard;                 // [R][C]: read by the push, written by the pull
+  int64_t R, C, row_begin;       // this rank's rows of x_d and their global offset
+  int P;
+  double *peer[kLsaMaxP];        // loopback: every rank's window (LSA: unused)
+};
+
+template <bool LSA, bool PULL>
+__global__ void __launch_bounds__(kLsaThreads) k_reshard(const __grid_constant__ ReshardArgs a,
+                                                         const __grid_constant__ ncclDevComm dc, ncclWindow_t win) {
+  __shared__ double *base[kLsaMaxP];
+  for (int q = threadIdx.x; q < a.P; q += blockDim.x)
+    base[q] = LSA ? static_cast<double *>(ncclGetLsaPointer(win, 0, ncclTeamRankToLsa(dc, ncclTeamWorld(dc), q)))
+                  : a.peer[q];
+  if constexpr (LSA) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamLsa(dc), dc.lsaBarrier, blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    __syncthreads();
+    // segment (i, q): row i of the shard, column block C_q -- contiguous on
+    // both sides (shard row i, window row row_begin + i of width |C_q|)
+    const int64_t nseg = a.R * a.P;
+    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+      const int64_t i = g / a.P;
+      const int q = int(g - i * a.P);
+      const int64_t c0 = a.C * q / a.P, w = a.C * (q + 1) / a.P - c0;
+      double *wr = base[q] + (a.row_begin + i) * w;
+      double *sh = a.shard + i * a.C + c0;
+      for (int64_t j = threadIdx.x; j < w; j += blockDim.x) {
+        if (PULL) sh[j] = wr[j];
+        else wr[j] = sh[j];
+      }
+    }
+    if (!PULL) bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+  } else {
+    __syncthreads();
+    const int64_t nseg = a.R * a.P;
+    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
+      const int64_t i = g / a.P;
+      const int q = int(g - i * a.P);
+      const int64_t c0 = a.C * q / a.P, w = a.C * (q + 1) / a.P - c0;
+      double *wr = base[q] + (a.row_begin + i) * w;
+      double *sh = a.shard + i * a.C + c0;
+      for (int64_t j = threadIdx.x; j < w; j += blockDim.x) {
+        if (PULL) sh[j] = wr[j];
+        else wr[j] = sh[j];
+      }
+    }
+  }
+}
+
+// the same number of CTAs on every rank (one LSA barrier each), all co-resident
+static int lsa_ctas() {
+  static int ctas = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!ctas) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reshard<true, false>, kLsaThreads, 0);
+    ctas = std::max(1, std::min(kLsaMaxCtas, sms * std::max(occ, 1)));
+  }
+  return ctas;
+}
+
+static int64_t lsa_window_elems(const ShardGeom &G) { return G.nd * max_cols(G); }
+
+static sgh_status reshard_launch(bool lsa, bool pull, const ReshardArgs &a, Comm *c, cudaStream_t s) {
+  const int grid = lsa ? lsa_ctas() : int(std::min<int64_t>(std::max<int64_t>(a.R * a.P, 1), 2 * 148));
+  ncclDevComm dc{};
+  if (lsa) dc = c->dev;
+  ncclWindow_t w = lsa ? c->win : nullptr;
+  if (lsa && pull) k_reshard<true, true><<<grid, kLsaThreads, 0, s>>>(a, dc, w);
+  else if (lsa) k_reshard<true, false><<<grid, kLsaThreads, 0, s>>>(a, dc, w);
+  else if (pull) k_reshard<false, true><<<grid, kLsaThreads, 0, s>>>(a, dc, w);
+  else k_reshard<false, false><<<grid, kLsaThreads, 0, s>>>(a, dc, w);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch (k_reshard)");
+  count_launch();
+  return SGH_OK;
+}
+
+static sgh_status lsa_enable(Comm *c, size_t bytes) {
+  if (c->lsa) return invalid("the device-API exchange is already enabled on this communicator");
+  if (c->nranks > kLsaMaxP) return invalid("the device-API exchange supports at most 64 ranks");
+  bytes = std::max<size_t>((bytes + 4095) / 4096 * 4096, 4096);
+  ncclResult_t r = ncclMemAlloc(&c->win_buf, bytes);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclMemAlloc (LSA window)");
+  r = ncclCommWindowRegister(c->nccl, c->win_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess) {
+    ncclMemFree(c->win_buf);
+    c->win_buf = nullptr;
+    return nccl_fail(r, "ncclCommWindowRegister");
+  }
+  ncclDevCommRequirements req;
+  std::memset(&req, 0, sizeof req);
+  req.lsaBarrierCount = kLsaMaxCtas;
+  r = ncclDevCommCreate(c->nccl, &req, &c->dev);
+  if (r != ncclSuccess) {
+    ncclCommWindowDeregister(c->nccl, c->win);
+    ncclMemFree(c->win_buf);
+    c->win_buf = nullptr;
+    c->win = nullptr;
+    return nccl_fail(r, "ncclDevCommCreate");
+  }
+  if (c->dev.lsaSize != c->nranks) {
+    ncclDevCommDestroy(c->nccl, &c->dev);
+    ncclCommWindowDeregister(c->nccl, c->win);
+    ncclMemFree(c->win_buf);
+    c->win_buf = nullptr;
+    c->win = nullptr;
+    set_error("the load/store-accessible (NVLink) team does not span every rank of the communicator");
+    return SGH_ERR_NCCL;
+  }
+  c->win_bytes = bytes;
+  c->lsa = true;
+  return SGH_OK;
+}
+
+static void lsa_release(Comm *c) {
+  if (!c->lsa) return;
+  ncclDevCommDestroy(c->nccl, &c->dev);
+  ncclCommWindowDeregister(c->nccl, c->win);
+  ncclMemFree(c->win_buf);
+  c->lsa = false;
+  c->win_buf = nullptr;
+  c->win = nullptr;
+}
+
+static sgh_status sharded_lsa(double *shard, const int32_t *levels, int32_t d, void *comm, void *stream, bool inv) {
+  if (!comm) return invalid("comm is NULL");
+  Comm *c = static_cast<Comm *>(comm);
+  if (!c->lsa) return invalid("sgh_comm_lsa_enable() was not called on this communicator");
+  ShardGeom G;
+  sgh_status st = validate_levels(levels, d, nullptr);
+  if (st != SGH_OK) return st;
+  if ((st = make_geom(levels, d, c->nranks, c->rank, G)) != SGH_OK) return st;
+  if (!shard && G.rows[c->rank] > 0) return invalid("shard is NULL");
+  if (size_t(lsa_window_elems(G)) * 8 > c->win_bytes) {
+    set_error("LSA window smaller than sgh_sharded_lsa_window_bytes()");
+    return SGH_ERR_WORKSPACE;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int r = c->rank;
+  ReshardArgs a{};
+  a.shard = shard;
+  a.R = G.rows[r];
+  a.C = G.C;
+  a.row_begin = G.row_begin[r];
+  a.P = G.P;
+  if ((st = local_axes(shard, G, r, inv, s)) != SGH_OK) return st;
+  if ((st = reshard_launch(true, false, a, c, s)) != SGH_OK) return st;
+  if ((st = slab_axis(static_cast<double *>(c->win_buf), G, r, inv, s)) != SGH_OK) return st;
+  return reshard_launch(true, true, a, c, s);
+}
+
+static sgh_status sharded_lsa_loopback(double *const *shards, const int32_t *levels, int32_t d, int32_t P,
+                                       void *workspace, size_t ws_bytes, void *stream, bool inv) {
+  ShardGeom G;
+  sgh_status st = validate_levels(levels, d, nullptr);
+  if (st != SGH_OK) return st;
+  int64_t b, e;
+  if ((st = shard_rows_impl(levels, d, P, 0, &b, &e)) != SGH_OK) return st;
+  if (P > kLsaMaxP) return invalid("the device-API exchange supports at most 64 ranks");
+  if ((st = make_geom(levels, d, P, 0, G)) != SGH_OK) return st;
+  if (!shards) return invalid("shards is NULL");
+  const int64_t E = lsa_window_elems(G);
+  if (!workspace || ws_bytes < size_t(E * 8) * size_t(P)) {
+    set_error("workspace smaller than nranks * sgh_sharded_lsa_window_bytes()");
+    return SGH_ERR_WORKSPACE;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double *ws = static_cast<double *>(workspace);
+  ReshardArgs a{};
+  a.C = G.C;
+  a.P = P;
+  for (int q = 0; q < P; ++q) a.peer[q] = ws + E * q;
+  for (int r = 0; r < P; ++r)
+    if (!shards[r] && G.rows[r] > 0) return invalid("shards[r] is NULL");
+  for (int r = 0; r < P; ++r) {
+    if ((st = local_axes(shards[r], G, r, inv, s)) != SGH_OK) return st;
+    a.shard = shards[r];
+    a.R = G.rows[r];
+    a.row_begin = G.row_begin[r];
+    if ((st = reshard_launch(false, false, a, nullptr, s)) != SGH_OK) return st;
+  }
+  for (int q = 0; q < P; ++q)
+    if ((st = slab_axis(a.peer[q], G, q, inv, s)) != SGH_OK) return st;
+  for (int r = 0; r < P; ++r) {
+    a.shard = shards[r];
+    a.R = G.rows[r];
+    a.row_begin = G.row_begin[r];
+    if ((st = reshard_launch(false, true, a, nullptr, s)) != SGH_OK) return st;
+  }
+  return SGH_OK;
+}
+
 }  // namespace sgh
 
 using namespace sgh;
@@ -616,6 +843,7 @@ sgh_status sgh_comm_create(void **comm, const void *nccl_unique_id, int32_t nran
 void sgh_comm_destroy(void *comm) {
   if (!comm) return;
   Comm *c = static_cast<Comm *>(comm);
+  if (c->nccl) lsa_release(c);
   if (c->nccl) ncclCommDestroy(c->nccl);
   delete c;
 }
@@ -678,6 +906,40 @@ sgh_status sgh_transform_sharded_loopback(double *const *shards, const int32_t *
   if (flags & ~uint32_t(SGH_FLAG_DEHIERARCHIZE)) return invalid("unknown flags");
   return sharded_loopback(shards, levels, d, nranks, workspace, ws_bytes, stream,
                           (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
+});
+}
+
+sgh_status sgh_comm_lsa_enable(void *comm, size_t window_bytes) {
+  return guarded([&]() -> sgh_status {
+  if (!comm) return invalid("comm is NULL");
+  return lsa_enable(static_cast<Comm *>(comm), window_bytes);
+});
+}
+
+size_t sgh_sharded_lsa_window_bytes(const int32_t *levels, int32_t d, int32_t nranks) {
+  return guarded_value<size_t>(0, [&]() -> size_t {
+  ShardGeom G;
+  if (validate_levels(levels, d, nullptr) != SGH_OK) return 0;
+  int64_t b, e;
+  if (shard_rows_impl(levels, d, nranks, 0, &b, &e) != SGH_OK) return 0;
+  if (make_geom(levels, d, nranks, 0, G) != SGH_OK) return 0;
+  return size_t(lsa_window_elems(G) * 8);
+});
+}
+
+sgh_status sgh_transform_sharded_lsa(double *shard, const int32_t *levels, int32_t d, void *comm, uint32_t flags,
+                                     void *stream) {
+  return guarded([&]() -> sgh_status {
+  return sharded_lsa(shard, levels, d, comm, stream, (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
+});
+}
+
+sgh_status sgh_transform_sharded_lsa_loopback(double *const *shards, const int32_t *levels, int32_t d,
+                                              int32_t nranks, uint32_t flags, void *workspace, size_t ws_bytes,
+                                              void *stream) {
+  return guarded([&]() -> sgh_status {
+  return sharded_lsa_loopback(shards, levels, d, nranks, workspace, ws_bytes, stream,
+                              (flags & SGH_FLAG_DEHIERARCHIZE) != 0);
 });
 }
 

@@ -527,6 +527,63 @@ def test_sharded_nccl_one_rank_bitwise(sgh, levels, inverse):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("levels,P", [((6, 5), 2), ((5, 4, 6), 8), ((3, 7), 8), ((8, 2, 3, 4), 4), ((4, 2), 2),
+                                      ((2, 3, 9), 16), ((14, 13), 8), ((14, 13), 2), ((7, 7, 8), 4), ((9, 6), 1)],
+                         ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_sharded_lsa_loopback_bitwise(sgh, levels, P, inverse):
+    """The device-API exchange kernels (SURVEY 8(f) 4 iii; push of rows(r) x C_q
+    into rank q's slab, pull back into the shard) for P virtual ranks on one
+    GPU: every rank's blocks land where the x_d pass needs them; bitwise vs the
+    single-grid oracle."""
+    N = si.num_points(levels)
+    u = si.fill_uniform(N, grid_id=83)
+    want = (oracle.dehierarchize if inverse else oracle.hierarchize)(u.copy(), levels)
+    C = N // ((1 << levels[-1]) - 1)
+    shards = []
+    for r in range(P):
+        b, e = sgh.shard_rows(levels, P, r)
+        shards.append(torch.from_numpy(u[b * C:e * C].copy()).cuda())
+    ws = torch.full((P * sgh.sharded_lsa_window_bytes(levels, P) // 8,), float("nan"), dtype=torch.float64,
+                    device="cuda")
+    sgh.transform_sharded_lsa_loopback(shards, levels, ws, inverse=inverse)
+    got = torch.cat(shards).cpu().numpy()
+    assert_bitwise(got, want)
+
+
+@pytest.mark.parametrize("levels", [(8, 8, 8), (14, 13), (5, 4, 6)], ids=str)
+@pytest.mark.parametrize("inverse", [False, True], ids=["hier", "dehier"])
+def test_sharded_lsa_one_rank_bitwise(sgh, levels, inverse):
+    """The NCCL device-API exchange itself on the one GPU the pool provides: a
+    one-rank communicator with a symmetric window and LSA barriers
+    (sgh_comm_lsa_enable); k_reshard pushes into / pulls from the window
+    through ncclGetLsaPointer; bitwise vs the oracle."""
+    import socket
+
+    import torch.distributed as dist
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        comm = sgh.ShardComm()
+        comm.enable_lsa(sgh.sharded_lsa_window_bytes(levels, 1))
+        N = si.num_points(levels)
+        u = si.fill_uniform(N, grid_id=92)
+        want = (oracle.dehierarchize if inverse else oracle.hierarchize)(u.copy(), levels)
+        g = torch.from_numpy(u.copy()).cuda()
+        comm.transform_lsa(g, levels, inverse=inverse)
+        torch.cuda.synchronize()
+        assert_bitwise(g.cpu().numpy(), want)
+        g2 = torch.from_numpy(u.copy()).cuda()       # a second call reuses the window and barriers
+        comm.transform_lsa(g2, levels, inverse=inverse)
+        torch.cuda.synchronize()
+        assert_bitwise(g2.cpu().numpy(), want)
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
 def test_survey_abi_spellings_bitwise(sgh):
     """The SURVEY 8(b) spellings: sgh_hierarchize_ex (workspace accepted,
     unused) and sgh_dehierarchize_batched / sgh_workspace_bytes, called through
