@@ -236,7 +236,7 @@ def main():
                     help="time dehierarchization (P:77) instead (reported under a 'dehierarchized' metric)")
     ap.add_argument("--per-axis", action="store_true",
                     help="one HBM round trip per axis (disable the multi-axis FUSED kernel)")
-    ap.add_argument("--sharded", default="halo", choices=["halo", "a2a"],
+    ap.add_argument("--sharded", default="halo", choices=["halo", "a2a", "lsa"],
                     help="C4 with N > 1 ranks: halo + coarse-lattice exchange (one all-gather of a row per rank, "
                          "SURVEY 8(f) 1; default) or the all-to-all re-shard (SURVEY 8(a) a7)")
     ap.add_argument("--dump-launch-keys", default=None,
@@ -295,7 +295,8 @@ def dry_run(args, rank, world, local_rank):
         import paper_1309_0392_b200 as sgh
         b, e = sgh.shard_rows(members[0], world, rank)
         info.update(path=("C4 sharded along x_d: " + ("halo + coarse-lattice all-gather" if args.sharded == "halo"
-                                                       else "NCCL all-to-all re-shard")),
+                                                       else "NCCL device-API (LSA) re-shard in kernels"
+                                                       if args.sharded == "lsa" else "NCCL all-to-all re-shard")),
                     rows=[b, e])
     else:
         info.update(path="replica of the single-grid workload" if world > 1 else "single GPU",
@@ -378,6 +379,10 @@ def sgh_arm(args, rank, world, local_rank):
             ws = torch.empty(sgh.sharded_halo_workspace_bytes(levels, world) // 8 + 1, dtype=torch.float64,
                              device=dev)
             step = lambda: comm.transform_halo(buf, levels, ws, inverse=args.inverse)  # noqa: E731
+        elif args.sharded == "lsa":     # the re-shard in kernels over NVLink peer memory (NCCL device API)
+            shard = torch.empty((e - b) * C, dtype=torch.float64, device=dev)
+            comm.enable_lsa(sgh.sharded_lsa_window_bytes(levels, world))
+            step = lambda: comm.transform_lsa(shard, levels, inverse=args.inverse)  # noqa: E731
         else:
             shard = torch.empty((e - b) * C, dtype=torch.float64, device=dev)
             ws = torch.empty(sgh.sharded_workspace_bytes(levels, world) // 8 + 1, dtype=torch.float64, device=dev)
@@ -547,7 +552,7 @@ def sgh_arm(args, rank, world, local_rank):
                           "parallelism": (f"grids LPT-balanced by planned time over {world} ranks" if args.workload == "C5" else
                                           f"contiguous grid blocks over {world} ranks, gather chain + broadcast"
                                           if args.workload == "C5cycle"
-                                          else ((f"sharded along x_d, {'halo + coarse-lattice all-gather' if args.sharded == 'halo' else 'NCCL all-to-all'}")
+                                          else ((f"sharded along x_d, {'halo + coarse-lattice all-gather' if args.sharded == 'halo' else 'NCCL device-API (LSA) re-shard' if args.sharded == 'lsa' else 'NCCL all-to-all'}")
                                                 if sharded else "replicas")),
                           "seed": si.SEED, **({"gather": gather_desc} if gather_desc else {})},
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,

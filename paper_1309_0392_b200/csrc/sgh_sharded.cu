@@ -530,8 +530,47 @@ struct ReshardArgs {
   double *shard;                 // [R][C]: read by the push, written by the pull
   int64_t R, C, row_begin;       // this rank's rows of x_d and their global offset
   int P;
+  int64_t nch;                   // chunks per (row, column block): ceil(max |C_q| / (kReshardU * kLsaThreads))
   double *peer[kLsaMaxP];        // loopback: every rank's window (LSA: unused)
 };
+
+// work items (i, q, k): chunk k (kReshardU * blockDim elements) of segment
+// (i, q) = row i of the shard, column block C_q -- contiguous on both sides
+// (shard row i, window row row_begin + i of width |C_q|); all of a thread's
+// loads are issued before its stores
+constexpr int kReshardU = 4;
+
+template <bool PULL>
+__device__ __forceinline__ void reshard_items(const ReshardArgs &a, double *const *base) {
+  const int64_t ch = int64_t(kReshardU) * blockDim.x;
+  const int64_t per_row = int64_t(a.P) * a.nch;
+  const int64_t nitems = a.R * per_row;
+  for (int64_t g = blockIdx.x; g < nitems; g += gridDim.x) {
+    const int64_t i = g / per_row;
+    const int64_t rem = g - i * per_row;
+    const int q = int(rem / a.nch);
+    const int64_t k = rem - int64_t(q) * a.nch;
+    const int64_t c0 = a.C * q / a.P, w = a.C * (q + 1) / a.P - c0;
+    const int64_t j0 = k * ch;
+    if (j0 >= w) continue;
+    double *wr = base[q] + (a.row_begin + i) * w + j0;
+    double *sh = a.shard + i * a.C + c0 + j0;
+    const double *src = PULL ? wr : sh;
+    double *dst = PULL ? sh : wr;
+    const int64_t n = w - j0 < ch ? w - j0 : ch;
+    double v[kReshardU];
+#pragma unroll
+    for (int u = 0; u < kReshardU; ++u) {
+      const int64_t j = threadIdx.x + int64_t(u) * blockDim.x;
+      if (j < n) v[u] = src[j];
+    }
+#pragma unroll
+    for (int u = 0; u < kReshardU; ++u) {
+      const int64_t j = threadIdx.x + int64_t(u) * blockDim.x;
+      if (j < n) dst[j] = v[u];
+    }
+  }
+}
 
 template <bool LSA, bool PULL>
 __global__ void __launch_bounds__(kLsaThreads) k_reshard(const __grid_constant__ ReshardArgs a,
@@ -546,33 +585,11 @@ __global__ void __launch_bounds__(kLsaThreads) k_reshard(const __grid_constant__
     __syncthreads();
     // segment (i, q): row i of the shard, column block C_q -- contiguous on
     // both sides (shard row i, window row row_begin + i of width |C_q|)
-    const int64_t nseg = a.R * a.P;
-    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-      const int64_t i = g / a.P;
-      const int q = int(g - i * a.P);
-      const int64_t c0 = a.C * q / a.P, w = a.C * (q + 1) / a.P - c0;
-      double *wr = base[q] + (a.row_begin + i) * w;
-      double *sh = a.shard + i * a.C + c0;
-      for (int64_t j = threadIdx.x; j < w; j += blockDim.x) {
-        if (PULL) sh[j] = wr[j];
-        else wr[j] = sh[j];
-      }
-    }
+    reshard_items<PULL>(a, base);
     if (!PULL) bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
   } else {
     __syncthreads();
-    const int64_t nseg = a.R * a.P;
-    for (int64_t g = blockIdx.x; g < nseg; g += gridDim.x) {
-      const int64_t i = g / a.P;
-      const int q = int(g - i * a.P);
-      const int64_t c0 = a.C * q / a.P, w = a.C * (q + 1) / a.P - c0;
-      double *wr = base[q] + (a.row_begin + i) * w;
-      double *sh = a.shard + i * a.C + c0;
-      for (int64_t j = threadIdx.x; j < w; j += blockDim.x) {
-        if (PULL) sh[j] = wr[j];
-        else wr[j] = sh[j];
-      }
-    }
+    reshard_items<PULL>(a, base);
   }
 }
 
@@ -593,8 +610,10 @@ static int lsa_ctas() {
 
 static int64_t lsa_window_elems(const ShardGeom &G) { return G.nd * max_cols(G); }
 
-static sgh_status reshard_launch(bool lsa, bool pull, const ReshardArgs &a, Comm *c, cudaStream_t s) {
-  const int grid = lsa ? lsa_ctas() : int(std::min<int64_t>(std::max<int64_t>(a.R * a.P, 1), 2 * 148));
+static sgh_status reshard_launch(bool lsa, bool pull, ReshardArgs a, Comm *c, cudaStream_t s) {
+  const int64_t ch = int64_t(kReshardU) * kLsaThreads;
+  a.nch = ((a.C + a.P - 1) / a.P + ch - 1) / ch;
+  const int grid = lsa ? lsa_ctas() : int(std::min<int64_t>(std::max<int64_t>(a.R * a.P * a.nch, 1), 2 * 148));
   ncclDevComm dc{};
   if (lsa) dc = c->dev;
   ncclWindow_t w = lsa ? c->win : nullptr;
