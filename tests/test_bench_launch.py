@@ -52,6 +52,14 @@ def test_self_launch_c4_sharded_rows():
     assert all(rows[i][1] == rows[i + 1][0] for i in range(3))
 
 
+@pytest.mark.parametrize("path,want", [("a2a", "NCCL all-to-all re-shard"),
+                                       ("lsa", "NCCL device-API (LSA) re-shard in kernels")])
+def test_self_launch_c4_sharded_transport(path, want):
+    lines = _bench(["--gpus", "2", "--workload", "C4", "--sharded", path, "--dry-run"])
+    assert sorted(d["rank"] for d in lines) == [0, 1]
+    assert all(d["path"].endswith(want) for d in lines)
+
+
 def test_world_size_mismatch_refused():
     _bench(["--gpus", "4", "--dry-run"], {"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"}, expect_rc=2)
 
