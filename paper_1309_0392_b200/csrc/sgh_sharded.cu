@@ -102,16 +102,25 @@ static sgh_status launch_phases(std::vector<Task> &phases, bool inv, cudaStream_
   return SGH_OK;
 }
 
-// step 1: axes 0..d-2 on the local row shard of `rank`
-static sgh_status local_axes(double *shard, const ShardGeom &G, int rank, bool inv, cudaStream_t s) {
-  std::vector<Task> phases;
-  for (int k = 0; k < G.d - 1; ++k) {
-    phases.clear();
-    plan_axis(shard, G.levels, G.d, k, phases, G.rows[rank]);
-    sgh_status st = launch_phases(phases, inv, s);
+// axes 0..d-2 of a row shard: `rows` stacked (d-1)-dimensional grids, planned
+// like one grid (plan_grid_rows: fused / blocked groups, the plan the
+// single-grid call takes for the leading axes) -- each point sees axes
+// 1..d-1 in order with the oracle's operations
+static sgh_status shard_rows_axes(double *shard, const int32_t *levels, int d, int64_t rows, bool inv,
+                                  cudaStream_t s) {
+  if (rows <= 0) return SGH_OK;
+  std::vector<std::vector<Task>> passes;
+  plan_grid_rows(shard, levels, d - 1, rows, inv ? uint32_t(SGH_FLAG_DEHIERARCHIZE) : 0u, passes);
+  for (auto &ph : passes) {
+    sgh_status st = launch_phases(ph, inv, s);
     if (st != SGH_OK) return st;
   }
   return SGH_OK;
+}
+
+// step 1: axes 0..d-2 on the local row shard of `rank`
+static sgh_status local_axes(double *shard, const ShardGeom &G, int rank, bool inv, cudaStream_t s) {
+  return shard_rows_axes(shard, G.levels, G.d, G.rows[rank], inv, s);
 }
 
 // pack: shard [rows][C] -> send, block q = [rows][cols_q] at offset rows*col_begin_q
@@ -357,14 +366,7 @@ static sgh_status make_halo_geom(const int32_t *levels, int32_t d, int P, HaloGe
 
 // axes 0..d-2 of rank r's shard (rows of x_d as the outer index)
 static sgh_status halo_local_axes(double *shard, const HaloGeom &H, int r, bool inv, cudaStream_t s) {
-  std::vector<Task> phases;
-  for (int k = 0; k < H.d - 1; ++k) {
-    phases.clear();
-    plan_axis(shard, H.levels, H.d, k, phases, H.rows[r]);
-    sgh_status st = launch_phases(phases, inv, s);
-    if (st != SGH_OK) return st;
-  }
-  return SGH_OK;
+  return shard_rows_axes(shard, H.levels, H.d, H.rows[r], inv, s);
 }
 
 // the interior of rank r's super-block along x_d
