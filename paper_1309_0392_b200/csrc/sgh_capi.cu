@@ -957,7 +957,15 @@ static double kind_bw_raw(const Task &t) {
         run = 1 << 20;
         if (t.bj >= 0) run = (t.Gj == t.A) ? int64_t(t.A) * t.ej : t.A;
       }
-      double bw = run >= 256 ? 5.2 : run >= 128 ? 4.6 : run >= 64 ? 4.3 : run >= 32 ? 4.0 : run >= 16 ? 3.3 : 2.2;
+// runs of 8 doubles (W = 8 column tiles): measured 2.6-2.8 TB/s on k_fused
+// in C5's grouped launches (round 2; the r1 table had 2.2) -- with it
+// (6,6,5,5), (7,5,5,5), (6,6,6,4) ... fuse their two trailing axes (W = 8)
+// instead of two STRIDED passes: C5 1.72 -> 1.68 planned passes, same speed
+#ifndef SGH_RUN8_BW
+#define SGH_RUN8_BW 2.7
+#endif
+      double bw = run >= 256 ? 5.2 : run >= 128 ? 4.6 : run >= 64 ? 4.3 : run >= 32 ? 4.0 : run >= 16 ? 3.3
+                : run >= 8 ? SGH_RUN8_BW : 2.2;
       // two blocked axes: two block transforms per tile (measured on C4's
       // 129 x 65 tiles: 2.84 TB/s with 256-thread CTAs, 3.35 TB/s with the
       // 128-thread ones -- then one round trip + cross phases beats the
