@@ -98,6 +98,19 @@ def test_workspace_sizing():
     assert sgh.sharded_workspace_bytes([14, 13], 8) >= 2 * 8 * 1024 * 16383
 
 
+@pytest.mark.parametrize("levels,P", [((14, 13), 8), ((10, 4, 4, 4, 4), 2), ((8, 8, 8), 4), ((6, 5), 1), ((3, 7), 8)],
+                         ids=str)
+def test_lsa_window_sizing(levels, P):
+    """The device-API re-shard's window is one slab n_d x max_q |C_q| (column
+    blocks C_q = [C q / P, C (q + 1) / P)); invalid arguments give 0."""
+    C = si.num_points(levels[:-1]) if len(levels) > 1 else 1
+    nd = (1 << levels[-1]) - 1
+    maxc = max(C * (q + 1) // P - C * q // P for q in range(P))
+    assert sgh.sharded_lsa_window_bytes(levels, P) == 8 * nd * maxc
+    assert sgh.lib.sgh_sharded_lsa_window_bytes(None, 2, P) == 0
+    assert sgh.sharded_lsa_window_bytes(levels, 3) == 0            # ranks must be a power of two
+
+
 def test_no_cpu_fallback():
     import torch
     with pytest.raises(TypeError):
