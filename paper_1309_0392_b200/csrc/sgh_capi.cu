@@ -964,8 +964,12 @@ static double kind_bw_raw(const Task &t) {
 #ifndef SGH_RUN8_BW
 #define SGH_RUN8_BW 2.7
 #endif
+// ... in tiles of <= 2 axes; a W = 8 tile of many short axes spends its time in
+// the barrier-separated per-axis phases: S10's (2,2,2,2,2,2) x 8 tiles ran at
+// 1.75 TB/s (profiles/r02, 62.7 vs 68 Gpoints/s with the three-pass plan)
+      const double run8 = t.m <= 2 ? SGH_RUN8_BW : t.m == 3 ? 2.2 : 1.75;
       double bw = run >= 256 ? 5.2 : run >= 128 ? 4.6 : run >= 64 ? 4.3 : run >= 32 ? 4.0 : run >= 16 ? 3.3
-                : run >= 8 ? SGH_RUN8_BW : 2.2;
+                : run >= 8 ? run8 : 2.2;
       // two blocked axes: two block transforms per tile (measured on C4's
       // 129 x 65 tiles: 2.84 TB/s with 256-thread CTAs, 3.35 TB/s with the
       // 128-thread ones -- then one round trip + cross phases beats the
