@@ -253,6 +253,24 @@ def test_sharded_plan_bytes_fused(levels, P):
     assert a2a <= 1.01 * (3 + (len(levels) - 1 if len(levels) < 3 else 1.1)) * per
 
 
+def test_plan_w8_tiles_by_axis_count():
+    """Cost model (DESIGN 7, "W = 8 column tiles at their measured rate"): runs
+    of 8 doubles are fused only in tiles of few axes -- the largest C5 shapes
+    fuse their two trailing axes in W = 8 tiles (2 round trips), S10 does not
+    take a W = 8 tile of six 3-point axes (measured 1.75 TB/s: three passes)."""
+    for levels in [(6, 6, 5, 5), (7, 5, 5, 5), (6, 6, 6, 4)]:
+        p = _plan_passes(levels)
+        assert len(p) == 2
+        (kind, a, _), = p[1]
+        assert kind == "FUSED" and a["W"] == "8" and a["levels"].count(",") == 1
+    for l1 in (8, 9):
+        p = _plan_passes((l1,) + (2,) * 9)
+        assert len(p) == 3
+        for ph in p:
+            for kind, a, _ in ph:
+                assert not (kind == "FUSED" and a["W"] == "8" and a["levels"].count(",") >= 3)
+
+
 def test_plan_c5_single_pass_plans_partition():
     """Every C5 member whose hierarchization plan is ONE pass with a second
     blocked axis (two-blocked / prefix two-blocked) writes each point exactly
