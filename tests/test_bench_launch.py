@@ -67,3 +67,10 @@ def test_world_size_mismatch_refused():
 def test_single_rank_default():
     (d,) = _bench(["--dry-run"])
     assert d["rank"] == 0 and d["world_size"] == 1 and d["path"] == "single GPU"
+
+
+def test_reference_arm_runs_on_rank_zero_only():
+    """--impl reference under N ranks: rank 0 times the oracle, the others idle."""
+    lines = sorted(_bench(["--gpus", "2", "--impl", "reference", "--dry-run"]), key=lambda d: d["rank"])
+    assert [d["path"] for d in lines] == ["oracle on host cores (rank 0 only)", "idle (rank > 0)"]
+    assert all(d["impl"] == "reference" and d["world_size"] == 2 for d in lines)
